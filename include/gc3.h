@@ -1,0 +1,163 @@
+/*
+ * gc3.h — C ABI of the B200 GC3-IR runtime (libgc3.so).
+ *
+ * Drop-in boundary. The reference defines the compiler→runtime boundary as the
+ * *.ir.json file (schema SPEC.md:425; reader ir.hpp:226-310; validate ir.hpp:341-439) and its paper
+ * runtime as "API-compatible with NCCL". The reference ships no runtime, so each
+ * entry point below cites the interface it replaces:
+ *   - the nccl.h subset (NCCL 2.27.3 /usr/include/nccl.h line numbers; ncclAlltoAll from the
+ *     torch-bundled NCCL 2.28.9 nccl.h:460) that the paper's MSCCL runtime exposes;
+ *   - gc3Ir* : the reference IR library (ir.hpp deserialize/serialize/validate,
+ *     scheduler.hpp check_slots, program.hpp parallelize) as host-only C calls;
+ *   - gc3RegisterIR / gc3SetProtocolOverride / gc3QueryPlan / gc3SetConfig: the paper runtime's
+ *     "IRs parsed and stored in GPU memory at setup" + "size-range selection" (PAPER.md:387,
+ *     439-440) and the chunk/instance/protocol parameters.
+ * All calls return ncclResult_t; no C++ exception crosses the ABI. Plain pointers and sizes only.
+ */
+#ifndef GC3_H_
+#define GC3_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+/* cudaStream_t without pulling in the CUDA headers */
+typedef struct CUstream_st* cudaStream_t;
+
+#define GC3_VERSION_CODE 22809 /* reported by ncclGetVersion: NCCL 2.28.9-compatible subset */
+
+/* nccl.h:41-49 */
+typedef enum {
+  ncclSuccess = 0,
+  ncclUnhandledCudaError = 1,
+  ncclSystemError = 2,
+  ncclInternalError = 3,
+  ncclInvalidArgument = 4,
+  ncclInvalidUsage = 5,
+  ncclRemoteError = 6,
+  ncclInProgress = 7,
+  ncclNumResults = 8
+} ncclResult_t;
+
+/* nccl.h:37-38 */
+#define NCCL_UNIQUE_ID_BYTES 128
+typedef struct {
+  char internal[NCCL_UNIQUE_ID_BYTES];
+} ncclUniqueId;
+
+typedef struct gc3Comm* ncclComm_t;
+
+/* nccl.h:260-268 (ncclAvg is rejected: the IR fixes a pure reduction, PAPER.md has no averaging) */
+typedef enum { ncclSum = 0, ncclProd = 1, ncclMax = 2, ncclMin = 3, ncclAvg = 4, ncclNumOps = 5 } ncclRedOp_t;
+
+/* nccl.h:278-290 */
+typedef enum {
+  ncclInt8 = 0, ncclChar = 0, ncclUint8 = 1, ncclInt32 = 2, ncclInt = 2, ncclUint32 = 3,
+  ncclInt64 = 4, ncclUint64 = 5, ncclFloat16 = 6, ncclHalf = 6, ncclFloat32 = 7, ncclFloat = 7,
+  ncclFloat64 = 8, ncclDouble = 8, ncclBfloat16 = 9, ncclFloat8e4m3 = 10, ncclFloat8e5m2 = 11,
+  ncclNumTypes = 12
+} ncclDataType_t;
+
+/* ---- communicator lifecycle (nccl.h:140-239) ------------------------------------------------ */
+ncclResult_t ncclGetVersion(int* version);                                               /* nccl.h:140 */
+ncclResult_t ncclGetUniqueId(ncclUniqueId* uniqueId);                                    /* nccl.h:146 */
+ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniqueId commId, int rank); /* nccl.h:160 */
+/* nccl.h:169. Extension: devlist may repeat a device; the ranks sharing a device then run as
+ * "loopback" ranks inside one launch per device (single-GPU testing and measurement). */
+ncclResult_t ncclCommInitAll(ncclComm_t* comm, int ndev, const int* devlist);
+ncclResult_t ncclCommDestroy(ncclComm_t comm);                                           /* nccl.h:181 */
+ncclResult_t ncclCommAbort(ncclComm_t comm);                                             /* nccl.h:186 */
+const char* ncclGetErrorString(ncclResult_t result);                                    /* nccl.h:215 */
+const char* ncclGetLastError(ncclComm_t comm);                                          /* nccl.h:219 */
+ncclResult_t ncclCommGetAsyncError(ncclComm_t comm, ncclResult_t* asyncError);           /* nccl.h:227 */
+ncclResult_t ncclCommCount(const ncclComm_t comm, int* count);                           /* nccl.h:231 */
+ncclResult_t ncclCommCuDevice(const ncclComm_t comm, int* device);                       /* nccl.h:235 */
+ncclResult_t ncclCommUserRank(const ncclComm_t comm, int* rank);                         /* nccl.h:239 */
+
+/* ---- collectives: each runs the registered GC3-IR selected by collective + size_range ------ */
+/* nccl.h:392-393 */
+ncclResult_t ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count, ncclDataType_t datatype,
+                           ncclRedOp_t op, ncclComm_t comm, cudaStream_t stream);
+/* nccl.h:408-410 */
+ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount, ncclDataType_t datatype,
+                               ncclRedOp_t op, ncclComm_t comm, cudaStream_t stream);
+/* nccl.h:425-426 */
+ncclResult_t ncclAllGather(const void* sendbuff, void* recvbuff, size_t sendcount, ncclDataType_t datatype,
+                           ncclComm_t comm, cudaStream_t stream);
+/* torch NCCL 2.28.9 nccl.h:460-461 */
+ncclResult_t ncclAlltoAll(const void* sendbuff, void* recvbuff, size_t count, ncclDataType_t datatype,
+                          ncclComm_t comm, cudaStream_t stream);
+/* MSCCL spelling used by the north star */
+ncclResult_t ncclAllToAll(const void* sendbuff, void* recvbuff, size_t count, ncclDataType_t datatype,
+                          ncclComm_t comm, cudaStream_t stream);
+
+/* nccl.h:493 / 503 */
+ncclResult_t ncclGroupStart(void);
+ncclResult_t ncclGroupEnd(void);
+
+/* ---- GC3 extensions ------------------------------------------------------------------------ */
+/* Registers a GC3-IR program (file path, or the JSON text itself if it starts with '{') on this
+ * rank; every rank must register the same programs in the same order (collective, like comm init).
+ * instances > 1 applies the runtime parallelization rewrite (program.hpp:366-419; SURVEY.md
+ * Finding 5). The IR is loaded with the reference schema rules, validated (ir.hpp:341-439) against
+ * a 1 x nranks topology with the B200 budget (148 thread blocks), staged in device memory, and its
+ * FIFOs are exchanged with the peers. *ir_id receives the registration index. */
+ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instances, int* ir_id);
+/* proto: -1 = as tagged in the IR, 0 = simple, 1 = ll, 2 = ll128 (runs with the simple transport) */
+ncclResult_t gc3SetProtocolOverride(ncclComm_t comm, int ir_id, int proto);
+
+typedef struct {
+  int ir_id;          /* selected IR, -1 if none matches */
+  int protocol;       /* effective protocol: 0 simple, 1 ll */
+  int lanes;          /* CUDA blocks per IR thread block */
+  int grid;           /* CUDA blocks in the launch on this rank's device */
+  int local_ranks;    /* ranks executed by that launch */
+  int slots;          /* FIFO slots per connection */
+  int64_t chunk_elems;
+  int64_t tile_elems;
+  int64_t ntiles;
+  int64_t slot_bytes;
+  int64_t wire_bytes; /* max over ranks of bytes sent or received by send/recv-family ops */
+  int64_t hbm_bytes;  /* algorithmic local bytes (reads + writes of user/scratch buffers) of the launch */
+  char name[64];      /* IR name */
+} gc3PlanInfo;
+/* collective: 0 allreduce, 1 allgather, 2 reducescatter, 3 alltoall; count as in the NCCL call. */
+ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDataType_t datatype, gc3PlanInfo* info);
+
+/* Runtime knobs (defaults from GC3_SLOTS, GC3_SLOT_BYTES, GC3_MAX_LANES, GC3_LANES,
+ * GC3_TILE_BYTES, GC3_TIMEOUT_MS). key: "slots", "slot_bytes", "max_lanes" (apply to IRs registered
+ * afterwards), "lanes", "tile_bytes", "timeout_ms" (apply to the next launch; 0 = automatic). */
+ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value);
+
+/* ---- IR library, host only (no CUDA needed) ---------------------------------------------- */
+typedef struct gc3Ir* gc3Ir_t;
+/* ir.hpp:226-310. On a schema error returns ncclInvalidArgument and, if err is non-NULL, sets
+ * *err to a malloc'd "path\tmessage" string (free with gc3Free). */
+ncclResult_t gc3IrParse(const char* text, gc3Ir_t* ir, char** err);
+/* ir.hpp:145-186: canonical JSON (malloc'd, free with gc3Free) */
+ncclResult_t gc3IrSerialize(gc3Ir_t ir, char** text);
+/* ir.hpp:341-439: newline-separated issues ("" if valid) against an nodes x gpus_per_node
+ * topology with the given budgets (<= 0 keeps the reference defaults 80 / 32). */
+ncclResult_t gc3IrValidate(gc3Ir_t ir, int nodes, int gpus_per_node, int max_threadblocks, int max_channels, char** issues);
+/* scheduler.hpp:633-734: newline-separated violations */
+ncclResult_t gc3IrCheckSlots(gc3Ir_t ir, int slots, char** violations);
+/* program.hpp:366-419 parallelize(k) as an IR rewrite; returns a new handle */
+ncclResult_t gc3IrReplicate(gc3Ir_t ir, int instances, gc3Ir_t* out);
+ncclResult_t gc3IrFree(gc3Ir_t ir);
+void gc3Free(void* p);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GC3_H_ */

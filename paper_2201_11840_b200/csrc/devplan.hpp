@@ -1,0 +1,81 @@
+// POD structures shared by the host planner (runtime.cpp) and the sm_100a interpreter
+// (interp.cu). One launch executes every IR thread block of every rank hosted on one device;
+// each IR thread block is replicated over `lanes` CUDA blocks that own disjoint tiles.
+//
+// Correspondence with the paper's interpreter (Fig. 4):
+//   Instruction{step, opCode, srcOff, dstOff, count, srcPtr, dstPtr, depBid[D], depStep[D], hasDep}
+//     -> DevOp (+ DevDep list; the buffer "pointers" are buffer ids resolved per rank per call)
+//   semaphore[bid]          -> sems[(tb.sem + lane)]  (64-bit, epoch-tagged, .gpu scope)
+//   remote buffer slots     -> DevChan.fifo (receiver memory, `slots` x slot_bytes)
+#pragma once
+
+#include <cstdint>
+
+namespace gc3 {
+
+constexpr int kMaxLocalRanks = 16;
+constexpr int kThreads = 512;  // CUDA threads per interpreter block
+
+enum : uint8_t { kOpSend = 0, kOpRecv, kOpCopy, kOpReduce, kOpRrc, kOpRcs, kOpRrcs, kOpRrs, kOpNop };
+
+struct DevOp {  // 24 bytes
+  uint8_t opcode;
+  uint8_t src_buf;
+  uint8_t dst_buf;
+  uint8_t has_dep;
+  int16_t ndeps;
+  int16_t pad;
+  int32_t src_off;
+  int32_t dst_off;
+  int32_t count;
+  int32_t dep_begin;
+};
+
+struct DevDep {
+  int32_t sem;   // semaphore base index of the depended-on thread block (lane is added)
+  int32_t step;  // depended-on step
+  int32_t nops;  // op count of the depended-on thread block (progress encoding)
+  int32_t pad;
+};
+
+struct DevTb {
+  int32_t rank_slot;  // index of the owning rank within LaunchArgs::bufs
+  int32_t op_begin;
+  int32_t nops;
+  int32_t sem;        // semaphore base index (x lanes)
+  int32_t chan_in;    // receive-side channel base index (x lanes), -1 if none
+  int32_t chan_out;   // send-side channel base index (x lanes), -1 if none
+  int32_t pad[2];
+};
+
+// One side of one connection for one lane.  The FIFO and `head` live in the receiver's memory,
+// `tail` in the sender's memory (NVLink buffers on the receiving GPU).
+struct DevChan {
+  char* fifo;        // slots x slot_bytes
+  uint64_t* head;    // messages posted (written by the sender)
+  uint64_t* tail;    // messages consumed (written by the receiver)
+  uint64_t* mine;    // this side's persistent message counter
+};
+
+struct LaunchArgs {
+  const DevTb* tbs;
+  const DevOp* ops;
+  const DevDep* deps;
+  const DevChan* chans;
+  uint64_t* sems;
+  int32_t ntbs;
+  int32_t lanes;
+  int32_t slots;
+  int32_t sys_scope;    // 1: peers on other GPUs (NVLink, .sys fences); 0: same-device loopback
+  int64_t slot_bytes;
+  int64_t chunk_elems;  // elements per chunk
+  int64_t tile_elems;   // elements per tile
+  int64_t ntiles;
+  uint64_t epoch;       // launch counter of this device (semaphore tag)
+  uint64_t timeout_ns;  // spin-wait watchdog; 0 disables
+  int32_t* abort_flag;  // device word: any block that times out raises it
+  uint64_t* err_info;   // host-mapped: {code, rank, tb, step, tile, what, 0, 0}
+  char* bufs[kMaxLocalRanks][3];  // per local rank: input, output, scratch
+};
+
+}  // namespace gc3

@@ -1,0 +1,529 @@
+// GC3-IR interpreter for sm_100a.
+//
+// One persistent launch per device executes every IR thread block of every rank hosted on that
+// device (all thread blocks co-resident, cooperative launch). IR thread block b
+// is replicated over `lanes` CUDA blocks; lane l owns tiles l, l+lanes, ... of every chunk, and
+// has its own FIFOs and semaphores, so lanes never synchronise with each other. Within a lane the
+// loop structure is the paper's: tiles outermost, instructions in order,
+//   wait deps -> wait FIFO -> fused transfer (+reduction) -> publish FIFO / semaphore.
+//
+// Protocols:
+//   Simple: payload stored with 128-bit vector stores into the receiver's FIFO slot, then one
+//           release store of the slot counter (`head`); the receiver acquires it.
+//   LL:     every 8 payload bytes travel in a 16-byte line {d0, flag, d1, flag} written with one
+//           128-bit store; the receiver polls the flags, no fences on the data path.
+// In both, the receiver returns the slot with a release store of `tail` into sender memory.
+//
+// Reductions are fused into the transfer (rrc / rrcs / rrs / reduce): no separate elementwise
+// kernel exists. Arithmetic is the oracle's (oracle/gc3_oracle.c gc3o_reduce): f16/bf16 go
+// through f32 and are rounded to nearest even, integers wrap, max/min select.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "devplan.hpp"
+
+namespace gc3 {
+namespace dev {
+
+// ------------------------------------------------------------------ memory-model primitives
+__device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool sys) {
+  uint64_t v;
+  if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool sys) {
+  if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t globaltimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// data loads bypass L1: the lines may have been written by other SMs/GPUs during this launch
+__device__ __forceinline__ uint4 ld_cg(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint2 ld_cg8(const void* p) {
+  uint2 v;
+  asm volatile("ld.global.cg.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_vec(uint4* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+__device__ __forceinline__ void st_vec8(void* p, uint2 v) {
+  asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
+}
+__device__ __forceinline__ uint4 ld_volatile_line(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_line(uint4* p, uint4 v) {
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+// ------------------------------------------------------------------ arithmetic
+__device__ __forceinline__ float bf16_to_f32(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
+__device__ __forceinline__ uint16_t f32_to_bf16(float f) {  // RNE, NaN -> 0x7fff (oracle rule)
+  uint32_t x = __float_as_uint(f);
+  if ((x & 0x7f800000u) == 0x7f800000u && (x & 0x7fffffu)) return 0x7fff;
+  x += 0x7fffu + ((x >> 16) & 1u);
+  return static_cast<uint16_t>(x >> 16);
+}
+__device__ __forceinline__ float f16_to_f32(uint16_t h) {
+  float f;
+  asm("cvt.f32.f16 %0, %1;" : "=f"(f) : "h"(h));
+  return f;
+}
+__device__ __forceinline__ uint16_t f32_to_f16(float f) {  // RNE, NaN -> 0x7fff (oracle rule)
+  if (f != f) return 0x7fff;
+  uint16_t h;
+  asm("cvt.rn.f16.f32 %0, %1;" : "=h"(h) : "f"(f));
+  return h;
+}
+__device__ __forceinline__ float canon(float x) { return x != x ? __uint_as_float(0x7fffffffu) : x; }
+__device__ __forceinline__ double canon(double x) { return x != x ? __longlong_as_double(0x7fffffffffffffffll) : x; }
+
+enum RedOp { kSum = 0, kProd = 1, kMax = 2, kMin = 3 };
+
+template <typename T, int OP>
+struct IntOp {
+  __device__ static T apply(T a, T b) {
+    using U = typename std::make_unsigned<T>::type;
+    if (OP == kSum) return static_cast<T>(static_cast<U>(a) + static_cast<U>(b));
+    if (OP == kProd) return static_cast<T>(static_cast<U>(a) * static_cast<U>(b));
+    if (OP == kMax) return a > b ? a : b;
+    return a < b ? a : b;
+  }
+};
+template <typename F, int OP>
+__device__ __forceinline__ F float_apply(F a, F b) {
+  if (OP == kSum) return canon(a + b);
+  if (OP == kProd) return canon(a * b);
+  if (OP == kMax) return a != a ? b : (b != b ? a : (a > b ? a : b));
+  return a != a ? b : (b != b ? a : (a < b ? a : b));
+}
+
+// Element-wise reduction functor over raw storage. kEsize = element bytes.
+template <typename T, int OP>
+struct RedInt {
+  static constexpr int kEsize = sizeof(T);
+  static constexpr bool kReduce = true;
+  __device__ static void elem(const char* a, const char* b, char* o) {
+    *reinterpret_cast<T*>(o) = IntOp<T, OP>::apply(*reinterpret_cast<const T*>(a), *reinterpret_cast<const T*>(b));
+  }
+  template <typename V>
+  __device__ static V vec(V a, V b) {
+    V r;
+    const T* x = reinterpret_cast<const T*>(&a);
+    const T* y = reinterpret_cast<const T*>(&b);
+    T* z = reinterpret_cast<T*>(&r);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(sizeof(V) / sizeof(T)); ++i) z[i] = IntOp<T, OP>::apply(x[i], y[i]);
+    return r;
+  }
+};
+template <typename F, int OP>
+struct RedFloat {
+  static constexpr int kEsize = sizeof(F);
+  static constexpr bool kReduce = true;
+  __device__ static void elem(const char* a, const char* b, char* o) {
+    *reinterpret_cast<F*>(o) = float_apply<F, OP>(*reinterpret_cast<const F*>(a), *reinterpret_cast<const F*>(b));
+  }
+  template <typename V>
+  __device__ static V vec(V a, V b) {
+    V r;
+    const F* x = reinterpret_cast<const F*>(&a);
+    const F* y = reinterpret_cast<const F*>(&b);
+    F* z = reinterpret_cast<F*>(&r);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(sizeof(V) / sizeof(F)); ++i) z[i] = float_apply<F, OP>(x[i], y[i]);
+    return r;
+  }
+};
+template <bool BF, int OP>
+struct RedHalf {
+  static constexpr int kEsize = 2;
+  static constexpr bool kReduce = true;
+  __device__ static uint16_t one(uint16_t a, uint16_t b) {
+    const float p = BF ? bf16_to_f32(a) : f16_to_f32(a);
+    const float q = BF ? bf16_to_f32(b) : f16_to_f32(b);
+    if (OP == kMax || OP == kMin) {  // select keeps the operand bits
+      const bool take_b = p != p ? true : (q != q ? false : (OP == kMax ? !(p > q) : !(p < q)));
+      return take_b ? b : a;
+    }
+    const float r = float_apply<float, OP>(p, q);
+    return BF ? f32_to_bf16(r) : f32_to_f16(r);
+  }
+  __device__ static void elem(const char* a, const char* b, char* o) {
+    *reinterpret_cast<uint16_t*>(o) = one(*reinterpret_cast<const uint16_t*>(a), *reinterpret_cast<const uint16_t*>(b));
+  }
+  template <typename V>
+  __device__ static V vec(V a, V b) {
+    V r;
+    const uint16_t* x = reinterpret_cast<const uint16_t*>(&a);
+    const uint16_t* y = reinterpret_cast<const uint16_t*>(&b);
+    uint16_t* z = reinterpret_cast<uint16_t*>(&r);
+#pragma unroll
+    for (int i = 0; i < static_cast<int>(sizeof(V) / 2); ++i) z[i] = one(x[i], y[i]);
+    return r;
+  }
+};
+// Copy-only programs (AllGather / AllToAll IRs): byte granularity, never reduces.
+struct RedNone {
+  static constexpr int kEsize = 1;
+  static constexpr bool kReduce = false;
+  __device__ static void elem(const char* a, const char*, char* o) { *o = *a; }
+  template <typename V>
+  __device__ static V vec(V a, V) {
+    return a;
+  }
+};
+
+// ------------------------------------------------------------------ data movers
+// out0 (and out1 if non-null) = RED ? R(in0, in1) : in0, over nbytes. All pointers 16B aligned
+// takes the 128-bit path; the ragged remainder (and misaligned segments) go element-wise.
+template <class R, bool RED, bool TWO>
+__device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* o0, uint4* o1, int64_t nvec) {
+  constexpr int U = 4;
+  int64_t i = threadIdx.x;
+  for (; i + (U - 1) * kThreads < nvec; i += U * kThreads) {
+    uint4 x[U], y[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) x[k] = ld_cg(a + i + k * kThreads);
+    if (RED) {
+#pragma unroll
+      for (int k = 0; k < U; ++k) y[k] = ld_cg(b + i + k * kThreads);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint4 v = RED ? R::template vec<uint4>(x[k], y[k]) : x[k];
+      st_vec(o0 + i + k * kThreads, v);
+      if (TWO) st_vec(o1 + i + k * kThreads, v);
+    }
+  }
+  for (; i < nvec; i += kThreads) {
+    const uint4 x = ld_cg(a + i);
+    const uint4 v = RED ? R::template vec<uint4>(x, ld_cg(b + i)) : x;
+    st_vec(o0 + i, v);
+    if (TWO) st_vec(o1 + i, v);
+  }
+}
+
+template <class R>
+__device__ __forceinline__ void move_elems(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, bool red) {
+  constexpr int E = R::kEsize;
+  for (int64_t i = threadIdx.x * static_cast<int64_t>(E); i < nbytes; i += static_cast<int64_t>(kThreads) * E) {
+    char tmp[E];
+    if (red) R::elem(a + i, b + i, tmp);
+    else
+      for (int k = 0; k < E; ++k) tmp[k] = a[i + k];
+    for (int k = 0; k < E; ++k) o0[i + k] = tmp[k];
+    if (o1)
+      for (int k = 0; k < E; ++k) o1[i + k] = tmp[k];
+  }
+}
+
+template <class R>
+__device__ void move(const char* a, const char* b, char* o0, char* o1, int64_t nbytes) {
+  if (nbytes <= 0) return;
+  if (!o0) {
+    o0 = o1;
+    o1 = nullptr;
+  }
+  const bool red = R::kReduce && b != nullptr;
+  const uintptr_t align = reinterpret_cast<uintptr_t>(a) | reinterpret_cast<uintptr_t>(o0) |
+                          (b ? reinterpret_cast<uintptr_t>(b) : 0) | (o1 ? reinterpret_cast<uintptr_t>(o1) : 0);
+  int64_t done = 0;
+  if ((align & 15) == 0) {
+    const int64_t nvec = nbytes >> 4;
+    const uint4* va = reinterpret_cast<const uint4*>(a);
+    const uint4* vb = reinterpret_cast<const uint4*>(b);
+    uint4* v0 = reinterpret_cast<uint4*>(o0);
+    uint4* v1 = reinterpret_cast<uint4*>(o1);
+    if (red) {
+      if (o1) move_vec<R, true, true>(va, vb, v0, v1, nvec);
+      else move_vec<R, true, false>(va, vb, v0, v1, nvec);
+    } else {
+      if (o1) move_vec<R, false, true>(va, vb, v0, v1, nvec);
+      else move_vec<R, false, false>(va, vb, v0, v1, nvec);
+    }
+    done = nvec << 4;
+  }
+  if (done < nbytes)
+    move_elems<R>(a + done, b ? b + done : nullptr, o0 + done, o1 ? o1 + done : nullptr, nbytes - done, red);
+}
+
+// LL: one 16-byte line carries 8 payload bytes as {d0, flag, d1, flag}.
+template <class R>
+__device__ __forceinline__ uint2 red8(uint2 x, uint2 y) {
+  return R::template vec<uint2>(x, y);
+}
+
+// ------------------------------------------------------------------ watchdog
+// Everything here is passed by value: taking the address of a kernel parameter would force the
+// whole LaunchArgs into local memory.
+struct Ctx {
+  int32_t* abort_flag;
+  uint64_t* err_info;
+  uint64_t timeout_ns;
+  int rank_slot, tbi, step;
+  int64_t tile;
+};
+
+__device__ __noinline__ void raise_timeout(const Ctx c, int what) {
+  if (atomicCAS(c.abort_flag, 0, 1) == 0 && c.err_info) {
+    volatile uint64_t* e = c.err_info;
+    e[1] = static_cast<uint64_t>(c.rank_slot);
+    e[2] = static_cast<uint64_t>(c.tbi);
+    e[3] = static_cast<uint64_t>(c.step);
+    e[4] = static_cast<uint64_t>(c.tile);
+    e[5] = static_cast<uint64_t>(what);
+    __threadfence_system();
+    e[0] = 1;  // code: watchdog timeout
+  }
+}
+
+// Spins until *p >= target; false if the launch was aborted.
+__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys, const Ctx& c, int what) {
+  if (ld_acquire(p, sys) >= target) return true;
+  const uint64_t start = globaltimer();
+  for (int n = 0;; ++n) {
+    if (ld_acquire(p, sys) >= target) return true;
+    if ((n & 255) == 255) {
+      if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
+      if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
+        raise_timeout(c, what);
+        return false;
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ bool is_recv(int op) {
+  return op == kOpRecv || op == kOpRrc || op == kOpRcs || op == kOpRrcs || op == kOpRrs;
+}
+__device__ __forceinline__ bool is_send(int op) { return op == kOpSend || op == kOpRcs || op == kOpRrcs || op == kOpRrs; }
+
+__device__ __forceinline__ char* pick_buf(int b, char* in, char* out, char* sc) { return b == 0 ? in : (b == 1 ? out : sc); }
+
+// ------------------------------------------------------------------ LL op body
+// Lines of the incoming/outgoing message are distributed over threads; every thread polls the
+// flags of its own lines only.
+template <class R>
+__device__ bool ll_op(const DevOp op, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl, uint4* outl,
+                      uint32_t in_flag, uint32_t out_flag, const Ctx& c) {
+  const int64_t lines_per_seg = tbytes >> 3;
+  const int64_t nlines = lines_per_seg * op.count;
+  const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
+  for (int64_t k = threadIdx.x; k < nlines; k += kThreads) {
+    const int j = static_cast<int>(k / lines_per_seg);
+    const int64_t off = ((k - j * lines_per_seg) << 3) + j * chunk_bytes;
+    char* src = src0 + off;
+    char* dst = dst0 + off;
+    uint2 msg = make_uint2(0, 0);
+    if (recv) {
+      uint4 l = ld_volatile_line(inl + k);
+      if (l.y != in_flag || l.w != in_flag) {
+        const uint64_t start = globaltimer();
+        for (int n = 0;; ++n) {
+          l = ld_volatile_line(inl + k);
+          if (l.y == in_flag && l.w == in_flag) break;
+          if ((n & 255) == 255) {
+            if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
+            if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
+              raise_timeout(c, 4);
+              return false;
+            }
+          }
+        }
+      }
+      msg = make_uint2(l.x, l.z);
+    }
+    uint2 v;
+    switch (op.opcode) {
+      case kOpSend: v = ld_cg8(src); break;
+      case kOpRecv: st_vec8(dst, msg); continue;
+      case kOpRrc: st_vec8(dst, R::template vec<uint2>(ld_cg8(src), msg)); continue;
+      case kOpRcs: v = msg; st_vec8(src, v); break;
+      case kOpRrcs: v = R::template vec<uint2>(ld_cg8(src), msg); st_vec8(src, v); break;
+      case kOpRrs: v = R::template vec<uint2>(ld_cg8(src), msg); break;
+      default: continue;
+    }
+    if (send) st_volatile_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag));
+  }
+  return true;
+}
+
+// ------------------------------------------------------------------ the interpreter
+template <class R, bool LL>
+__global__ void __launch_bounds__(kThreads, 2) interp(const LaunchArgs a) {
+  const int lanes = a.lanes;
+  const int lane = blockIdx.x % lanes;
+  const int tbi = blockIdx.x / lanes;
+  const DevTb tb = a.tbs[tbi];
+  const bool sys = a.sys_scope != 0;
+  const bool has_in = tb.chan_in >= 0, has_out = tb.chan_out >= 0;
+  const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
+  const int64_t chunk_bytes = chunk_elems * R::kEsize;
+  const int64_t slot_bytes = a.slot_bytes;
+  const uint64_t slots = static_cast<uint64_t>(a.slots);
+  const uint64_t epoch = a.epoch;
+  // this block's rank buffers: select with constant indices (no dynamic param-space indexing)
+  char *b_in = nullptr, *b_out = nullptr, *b_sc = nullptr;
+#pragma unroll
+  for (int i = 0; i < kMaxLocalRanks; ++i)
+    if (i == tb.rank_slot) {
+      b_in = a.bufs[i][0];
+      b_out = a.bufs[i][1];
+      b_sc = a.bufs[i][2];
+    }
+  DevChan cin{}, cout{};
+  if (has_in) cin = a.chans[tb.chan_in + lane];
+  if (has_out) cout = a.chans[tb.chan_out + lane];
+  uint64_t rcvd = has_in ? *cin.mine : 0;
+  uint64_t sent = has_out ? *cout.mine : 0;
+  uint64_t* const sems = a.sems;
+  uint64_t* const my_sem = sems + tb.sem + lane;
+  const DevOp* const ops = a.ops + tb.op_begin;
+  const DevDep* const deps = a.deps;
+  Ctx c{a.abort_flag, a.err_info, a.timeout_ns, tb.rank_slot, tbi, 0, 0};
+  __shared__ int s_abort;
+  if (threadIdx.x == 0) s_abort = 0;
+  __syncthreads();
+
+  int64_t iter = 0;
+  for (int64_t tile = lane; tile < ntiles; tile += lanes, ++iter) {
+    const int64_t t0 = tile * tile_elems;
+    const int64_t tlen = min(tile_elems, chunk_elems - t0);
+    const int64_t tbytes = tlen * R::kEsize;
+    const int64_t t0_bytes = t0 * R::kEsize;
+    c.tile = tile;
+    for (int s = 0; s < tb.nops; ++s) {
+      const DevOp op = ops[s];
+      const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
+      c.step = s;
+      // (1) cross-thread-block dependencies and FIFO credits, waited in parallel
+      bool ok = true;
+      const int dep_thread = static_cast<int>(threadIdx.x) - 64;  // threads 64.. wait one dep each
+      if (dep_thread >= 0 && dep_thread < op.ndeps) {
+        const DevDep d = deps[op.dep_begin + dep_thread];
+        const uint64_t target = (epoch << 32) | static_cast<uint64_t>(iter * d.nops + d.step + 1);
+        ok = wait_geq(sems + d.sem + lane, target, false, c, 1);
+      } else if (threadIdx.x == 0 && send) {  // a free outgoing slot: sent - tail < slots
+        ok = wait_geq(cout.tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
+      } else if (threadIdx.x == 32 && recv && !LL) {  // a posted incoming message
+        ok = wait_geq(cin.head, rcvd + 1, sys, c, 3);
+      }
+      if (!ok) s_abort = 1;
+      __syncthreads();
+      if (s_abort) return;
+
+      // (2) the transfer, with the reduction fused in
+      char* src = pick_buf(op.src_buf, b_in, b_out, b_sc) + op.src_off * chunk_bytes + t0_bytes;
+      char* dst = pick_buf(op.dst_buf, b_in, b_out, b_sc) + op.dst_off * chunk_bytes + t0_bytes;
+      const int64_t slot_in = static_cast<int64_t>(rcvd % slots) * slot_bytes;
+      const int64_t slot_out = static_cast<int64_t>(sent % slots) * slot_bytes;
+      if (LL && (recv || send)) {
+        const uint4* inl = recv ? reinterpret_cast<const uint4*>(cin.fifo + slot_in) : nullptr;
+        uint4* outl = send ? reinterpret_cast<uint4*>(cout.fifo + slot_out) : nullptr;
+        if (!ll_op<R>(op, src, dst, chunk_bytes, tbytes, inl, outl, static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), c))
+          s_abort = 1;
+      } else {
+        const char* in = recv ? cin.fifo + slot_in : nullptr;
+        char* out = send ? cout.fifo + slot_out : nullptr;
+        for (int j = 0; j < op.count; ++j) {
+          char* sj = src + j * chunk_bytes;
+          char* dj = dst + j * chunk_bytes;
+          const char* mi = in ? in + j * tbytes : nullptr;
+          char* mo = out ? out + j * tbytes : nullptr;
+          switch (op.opcode) {
+            case kOpSend: move<R>(sj, nullptr, mo, nullptr, tbytes); break;
+            case kOpRecv: move<R>(mi, nullptr, dj, nullptr, tbytes); break;
+            case kOpCopy: move<R>(sj, nullptr, dj, nullptr, tbytes); break;
+            case kOpReduce: move<R>(dj, sj, dj, nullptr, tbytes); break;
+            case kOpRrc: move<R>(sj, mi, dj, nullptr, tbytes); break;
+            case kOpRcs: move<R>(mi, nullptr, sj, mo, tbytes); break;
+            case kOpRrcs: move<R>(sj, mi, sj, mo, tbytes); break;
+            case kOpRrs: move<R>(sj, mi, nullptr, mo, tbytes); break;
+            default: break;
+          }
+        }
+      }
+      __syncthreads();
+      if (s_abort) return;
+
+      // (3) publish: slot posted / slot freed / semaphore
+      if (threadIdx.x == 0) {
+        if (send && !LL) st_release(cout.head, sent + 1, sys);
+        if (recv) st_release(cin.tail, rcvd + 1, sys);
+        if (op.has_dep) st_release(my_sem, (epoch << 32) | static_cast<uint64_t>(iter * tb.nops + s + 1), false);
+      }
+      if (send) ++sent;
+      if (recv) ++rcvd;
+    }
+  }
+  if (threadIdx.x == 0) {
+    if (has_in) *cin.mine = rcvd;
+    if (has_out) *cout.mine = sent;
+  }
+}
+
+}  // namespace dev
+
+// ------------------------------------------------------------------ host-side dispatch
+using KernelFn = void (*)(LaunchArgs);
+
+template <class R>
+KernelFn pick(bool ll) {
+  return ll ? dev::interp<R, true> : dev::interp<R, false>;
+}
+
+template <int OP>
+KernelFn pick_type(int dtype, bool ll) {
+  switch (dtype) {
+    case 0: return pick<dev::RedInt<int8_t, OP>>(ll);
+    case 1: return pick<dev::RedInt<uint8_t, OP>>(ll);
+    case 2: return pick<dev::RedInt<int32_t, OP>>(ll);
+    case 3: return pick<dev::RedInt<uint32_t, OP>>(ll);
+    case 4: return pick<dev::RedInt<int64_t, OP>>(ll);
+    case 5: return pick<dev::RedInt<uint64_t, OP>>(ll);
+    case 6: return pick<dev::RedHalf<false, OP>>(ll);
+    case 7: return pick<dev::RedFloat<float, OP>>(ll);
+    case 8: return pick<dev::RedFloat<double, OP>>(ll);
+    case 9: return pick<dev::RedHalf<true, OP>>(ll);
+    default: return nullptr;
+  }
+}
+
+// dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs.
+KernelFn interp_kernel(int dtype, int redop, bool ll) {
+  switch (redop) {
+    case -1: return pick<dev::RedNone>(ll);
+    case 0: return pick_type<dev::kSum>(dtype, ll);
+    case 1: return pick_type<dev::kProd>(dtype, ll);
+    case 2: return pick_type<dev::kMax>(dtype, ll);
+    case 3: return pick_type<dev::kMin>(dtype, ll);
+    default: return nullptr;
+  }
+}
+
+cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, cudaStream_t stream) {
+  void* params[] = {const_cast<LaunchArgs*>(&args)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kThreads), params, 0, stream);
+}
+
+int interp_blocks_per_sm(KernelFn fn) {
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), kThreads, 0) != cudaSuccess) return 0;
+  return n;
+}
+
+}  // namespace gc3

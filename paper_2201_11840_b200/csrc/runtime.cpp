@@ -1,0 +1,1237 @@
+// Host runtime of the B200 GC3-IR interpreter: communicators, bootstrap, IR registration,
+// FIFO arenas + CUDA IPC exchange, device plans, NCCL-style groups and kernel launch.
+//
+// Paper runtime, re-designed for one NVSwitch box of B200s:
+//   * "all GC3-IR programs ... are parsed and stored in the GPU memory" ->
+//     gc3RegisterIR stages each program as a device plan (DevTb/DevOp/DevDep, devplan.hpp);
+//   * remote buffers on the receiving GPU with s FIFO slots -> one arena per
+//     (rank, IR) holding the receive FIFOs, counters and credits, exported with cudaIpc handles;
+//   * "selects the right algorithm ... based on user configurable size ranges" ->
+//     select_ir() over the registered programs' size_range (ir.hpp:112-116); no NCCL fallback
+//     exists on this path: an unmatched call returns ncclInvalidUsage;
+//   * cooperative launch of all thread blocks -> one launch per device covering
+//     every rank hosted there (several "loopback" ranks can share one GPU).
+#include <cuda_runtime.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <sys/types.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/gc3.h"
+#include "devplan.hpp"
+#include "ir.hpp"
+
+namespace gc3 {
+
+using KernelFn = void (*)(LaunchArgs);
+KernelFn interp_kernel(int dtype, int redop, bool ll);
+cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, cudaStream_t stream);
+int interp_blocks_per_sm(KernelFn fn);
+
+namespace {
+
+// ------------------------------------------------------------------------------- errors
+thread_local std::string g_last_error;
+std::recursive_mutex g_mu;  // communicators are not thread-safe (NCCL semantics); this guards globals
+
+ncclResult_t set_error(ncclResult_t rc, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  if (getenv("GC3_DEBUG")) fprintf(stderr, "[gc3] %s\n", buf);
+  return rc;
+}
+
+#define CUDA_TRY(call)                                                                              \
+  do {                                                                                              \
+    cudaError_t e_ = (call);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      return set_error(ncclUnhandledCudaError, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                       __FILE__, __LINE__);                                                         \
+  } while (0)
+
+#define NCCL_TRY(call)                      \
+  do {                                      \
+    ncclResult_t r_ = (call);               \
+    if (r_ != ncclSuccess) return r_;       \
+  } while (0)
+
+int64_t env_int(const char* name, int64_t def) {
+  const char* v = getenv(name);
+  return v && *v ? std::strtoll(v, nullptr, 10) : def;
+}
+
+// ------------------------------------------------------------------------------- config
+struct Config {
+  int slots = 2;                     // FIFO slots per connection; fused ops need >= 2 (SURVEY Finding 1)
+  int64_t slot_bytes = 256 << 10;    // bytes per FIFO slot (the paper's b / s)
+  int max_lanes = 16;                // lanes provisioned per connection in the arenas
+  int lanes = 0;                     // 0: automatic
+  int64_t tile_bytes = 0;            // 0: automatic
+  int64_t timeout_ms = 20000;        // device spin-wait watchdog
+};
+
+Config config_from_env() {
+  Config c;
+  c.slots = static_cast<int>(env_int("GC3_SLOTS", c.slots));
+  c.slot_bytes = env_int("GC3_SLOT_BYTES", c.slot_bytes);
+  c.max_lanes = static_cast<int>(env_int("GC3_MAX_LANES", c.max_lanes));
+  c.lanes = static_cast<int>(env_int("GC3_LANES", c.lanes));
+  c.tile_bytes = env_int("GC3_TILE_BYTES", c.tile_bytes);
+  c.timeout_ms = env_int("GC3_TIMEOUT_MS", c.timeout_ms);
+  return c;
+}
+
+size_t dtype_size(int dt) {
+  switch (dt) {
+    case ncclInt8: case ncclUint8: case ncclFloat8e4m3: case ncclFloat8e5m2: return 1;
+    case ncclFloat16: case ncclBfloat16: return 2;
+    case ncclInt32: case ncclUint32: case ncclFloat32: return 4;
+    case ncclInt64: case ncclUint64: case ncclFloat64: return 8;
+    default: return 0;
+  }
+}
+
+// ------------------------------------------------------------------------------- bootstrap
+// Single-node rendezvous through /dev/shm: the unique id names a directory; every rank posts
+// small records (atomic write + rename) and polls for its peers' records.
+std::string uid_key(const ncclUniqueId& id) {
+  static const char* hex = "0123456789abcdef";
+  std::string s;
+  for (int i = 4; i < 20; ++i) {
+    const unsigned char c = static_cast<unsigned char>(id.internal[i]);
+    s += hex[c >> 4];
+    s += hex[c & 15];
+  }
+  return s;
+}
+
+std::string shm_dir(const std::string& key) { return "/dev/shm/gc3-" + key; }
+
+bool post_record(const std::string& dir, const std::string& name, const std::string& data) {
+  mkdir(dir.c_str(), 0700);
+  const std::string tmp = dir + "/." + name + ".tmp" + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary | std::ios::trunc);
+    if (!f) return false;
+    f.write(data.data(), static_cast<std::streamsize>(data.size()));
+  }
+  return std::rename(tmp.c_str(), (dir + "/" + name).c_str()) == 0;
+}
+
+bool read_record(const std::string& dir, const std::string& name, std::string& out, int64_t timeout_ms) {
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms);
+  for (;;) {
+    std::ifstream f(dir + "/" + name, std::ios::binary);
+    if (f) {
+      std::ostringstream ss;
+      ss << f.rdbuf();
+      out = ss.str();
+      return true;
+    }
+    if (std::chrono::steady_clock::now() > deadline) return false;
+    std::this_thread::sleep_for(std::chrono::milliseconds(1));
+  }
+}
+
+// ------------------------------------------------------------------------------- structures
+using Comm = ::gc3Comm;  // the opaque ncclComm_t of gc3.h
+
+// Arena layout of one rank for one program. Every rank can compute any peer's layout from the
+// shared program text, so a sender addresses the receiver's FIFO without extra exchange.
+constexpr size_t kCounterStride = 64;
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct ArenaLayout {
+  std::vector<int> in_index, out_index;  // per tb: index among receiving / sending tbs, or -1
+  int n_in = 0, n_out = 0;
+  size_t off_fifo = 0, off_head = 0, off_tail = 0, off_mine_in = 0, off_mine_out = 0, bytes = 0;
+};
+
+ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_t slot_bytes) {
+  ArenaLayout a;
+  const Gpu& g = p.gpus[rank];
+  a.in_index.assign(g.tbs.size(), -1);
+  a.out_index.assign(g.tbs.size(), -1);
+  for (size_t t = 0; t < g.tbs.size(); ++t) {
+    if (g.tbs[t].recv_peer >= 0) a.in_index[t] = a.n_in++;
+    if (g.tbs[t].send_peer >= 0) a.out_index[t] = a.n_out++;
+  }
+  size_t off = 0;
+  a.off_fifo = off;
+  off += static_cast<size_t>(a.n_in) * lanes * slots * slot_bytes;
+  off = align_up(off, 256);
+  a.off_head = off;
+  off += static_cast<size_t>(a.n_in) * lanes * kCounterStride;
+  a.off_tail = off;
+  off += static_cast<size_t>(a.n_out) * lanes * kCounterStride;
+  a.off_mine_in = off;
+  off += static_cast<size_t>(a.n_in) * lanes * 8;
+  a.off_mine_out = off;
+  off += static_cast<size_t>(a.n_out) * lanes * 8;
+  a.bytes = align_up(std::max<size_t>(off, 256), 256);
+  return a;
+}
+
+// One registered program on one rank: the (possibly replicated) IR plus its arena.
+struct RankIR {
+  Program prog;
+  int proto_override = -1;
+  int slots = 2;
+  int64_t slot_bytes = 0;
+  int lanes = 1;  // lanes provisioned in the arena
+  bool has_reduce = false;
+  int max_count = 1;
+  ArenaLayout lay;
+  char* arena = nullptr;
+  cudaIpcMemHandle_t handle{};
+};
+
+// Per-device execution state shared by the ranks a clique hosts on that device.
+struct DevicePlan {  // one registered IR on one device
+  bool built = false;
+  std::vector<int> ranks;  // local ranks in launch order (rank_slot -> rank)
+  int ntbs = 0;
+  DevTb* d_tbs = nullptr;
+  DevOp* d_ops = nullptr;
+  DevDep* d_deps = nullptr;
+  DevChan* d_chans = nullptr;
+  uint64_t* d_sems = nullptr;
+  bool sys_scope = false;
+};
+
+struct DeviceState {
+  int device = -1;
+  uint64_t epoch = 0;
+  int32_t* d_abort = nullptr;
+  uint64_t* h_err = nullptr;  // host-mapped err_info[8]
+  uint64_t* d_err = nullptr;
+  std::vector<DevicePlan> plans;  // by ir id
+  int num_sms = 0;
+  std::map<KernelFn, int> occupancy;
+};
+
+struct Clique {
+  std::string key;
+  int nranks = 0;
+  std::vector<Comm*> local;   // by rank, nullptr when the rank lives in another process
+  std::vector<int> rank_dev;  // device of every rank (exchanged at init)
+  std::vector<int> rank_pid;
+  std::map<int, DeviceState> devs;
+  int refs = 0;
+};
+
+}  // namespace
+}  // namespace gc3
+
+struct gc3Comm {
+  gc3::Clique* clique = nullptr;
+  int rank = 0;
+  int nranks = 0;
+  int device = 0;
+  gc3::Config cfg;
+  std::vector<std::unique_ptr<gc3::RankIR>> irs;
+  // peer arena base pointers per ir: [ir][rank]
+  std::vector<std::vector<char*>> peer_arena;
+  char* scratch = nullptr;
+  size_t scratch_bytes = 0;
+  char* work = nullptr;  // ReduceScatter working buffer
+  size_t work_bytes = 0;
+  ncclResult_t async_error = ncclSuccess;
+  std::string last_error;
+  bool destroyed = false;
+  std::vector<void*> opened_ipc;  // peer arenas opened via IPC (to close)
+};
+
+namespace gc3 {
+namespace {
+
+std::map<std::string, std::unique_ptr<Clique>> g_cliques;
+
+// ------------------------------------------------------------------------------- groups
+enum Coll { kAllReduce = 0, kAllGather = 1, kReduceScatter = 2, kAllToAll = 3 };
+const char* coll_name(int c) {
+  static const char* n[] = {"allreduce", "allgather", "reducescatter", "alltoall"};
+  return n[c];
+}
+
+struct Pending {
+  Comm* comm;
+  int coll;
+  const void* send;
+  void* recv;
+  size_t count;
+  int dtype;
+  int redop;
+  cudaStream_t stream;
+};
+
+thread_local int g_group_depth = 0;
+thread_local std::vector<Pending> g_pending;
+
+// ------------------------------------------------------------------------------- helpers
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+ncclResult_t device_state(Clique* cl, int dev, DeviceState*& out) {
+  auto it = cl->devs.find(dev);
+  if (it != cl->devs.end()) {
+    out = &it->second;
+    return ncclSuccess;
+  }
+  DeviceState& ds = cl->devs[dev];
+  ds.device = dev;
+  DeviceGuard g(dev);
+  CUDA_TRY(cudaMalloc(&ds.d_abort, sizeof(int32_t)));
+  CUDA_TRY(cudaMemset(ds.d_abort, 0, sizeof(int32_t)));
+  CUDA_TRY(cudaHostAlloc(&ds.h_err, 8 * sizeof(uint64_t), cudaHostAllocMapped));
+  std::memset(ds.h_err, 0, 8 * sizeof(uint64_t));
+  CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ds.d_err), ds.h_err, 0));
+  CUDA_TRY(cudaDeviceGetAttribute(&ds.num_sms, cudaDevAttrMultiProcessorCount, dev));
+  out = &ds;
+  return ncclSuccess;
+}
+
+// Reads a file or treats the argument as JSON text.
+bool read_ir_text(const char* arg, std::string& text) {
+  const char* p = arg;
+  while (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r') ++p;
+  if (*p == '{') {
+    text = arg;
+    return true;
+  }
+  std::ifstream f(arg, std::ios::binary);
+  if (!f) return false;
+  std::ostringstream ss;
+  ss << f.rdbuf();
+  text = ss.str();
+  return true;
+}
+
+// Receiver of connection (src -> dst, ch) as a tb index on dst (last match, as validate()).
+int find_receiver(const Program& p, int src, int dst, int ch) {
+  int found = -1;
+  const auto& tbs = p.gpus[dst].tbs;
+  for (size_t t = 0; t < tbs.size(); ++t)
+    if (tbs[t].recv_peer == src && tbs[t].channel == ch) found = static_cast<int>(t);
+  return found;
+}
+int find_sender(const Program& p, int src, int dst, int ch) {
+  int found = -1;
+  const auto& tbs = p.gpus[src].tbs;
+  for (size_t t = 0; t < tbs.size(); ++t)
+    if (tbs[t].send_peer == dst && tbs[t].channel == ch) found = static_cast<int>(t);
+  return found;
+}
+
+int tb_index(const Program& p, int rank, int id) {
+  const auto& tbs = p.gpus[rank].tbs;
+  for (size_t t = 0; t < tbs.size(); ++t)
+    if (tbs[t].id == id) return static_cast<int>(t);
+  return -1;
+}
+
+// Resolves (and caches) the base pointer of rank `r`'s arena for ir `id` as seen from `c`.
+ncclResult_t peer_arena(Comm* c, int id, int r, char*& out) {
+  if (c->peer_arena.size() <= static_cast<size_t>(id)) c->peer_arena.resize(id + 1);
+  auto& v = c->peer_arena[id];
+  if (v.size() != static_cast<size_t>(c->nranks)) v.assign(c->nranks, nullptr);
+  if (v[r]) {
+    out = v[r];
+    return ncclSuccess;
+  }
+  Clique* cl = c->clique;
+  if (cl->local[r]) {  // same process: direct pointer (peer access enabled at init when needed)
+    Comm* pc = cl->local[r];
+    if (pc->irs.size() <= static_cast<size_t>(id))
+      return set_error(ncclInvalidUsage, "rank %d has not registered IR %d yet (register on all local ranks before launching)", r, id);
+    v[r] = pc->irs[id]->arena;
+  } else {
+    std::string rec;
+    const std::string name = "ir" + std::to_string(id) + ".rank" + std::to_string(r);
+    if (!read_record(shm_dir(cl->key), name, rec, c->cfg.timeout_ms + 60000))
+      return set_error(ncclSystemError, "timed out waiting for rank %d's IR %d arena handle", r, id);
+    if (rec.size() < sizeof(cudaIpcMemHandle_t)) return set_error(ncclSystemError, "bad arena record from rank %d", r);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, rec.data(), sizeof(h));
+    DeviceGuard g(c->device);
+    void* p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    c->opened_ipc.push_back(p);
+    v[r] = static_cast<char*>(p);
+  }
+  out = v[r];
+  return ncclSuccess;
+}
+
+// Builds the device plan of IR `id` on `dev` for the ranks the clique hosts there.
+ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
+  if (ds.plans.size() <= static_cast<size_t>(id)) ds.plans.resize(id + 1);
+  DevicePlan& plan = ds.plans[id];
+  if (plan.built) return ncclSuccess;
+  plan.ranks.clear();
+  for (int r = 0; r < cl->nranks; ++r)
+    if (cl->local[r] && cl->local[r]->device == ds.device) plan.ranks.push_back(r);
+  if (plan.ranks.empty()) return set_error(ncclInternalError, "no local ranks on device %d", ds.device);
+  if (static_cast<int>(plan.ranks.size()) > kMaxLocalRanks)
+    return set_error(ncclInvalidUsage, "%zu ranks on one device exceeds %d", plan.ranks.size(), kMaxLocalRanks);
+  Comm* c0 = cl->local[plan.ranks[0]];
+  for (int r : plan.ranks)
+    if (cl->local[r]->irs.size() <= static_cast<size_t>(id))
+      return set_error(ncclInvalidUsage, "rank %d has not registered IR %d", r, id);
+  const RankIR& ir0 = *c0->irs[id];
+  const Program& p = ir0.prog;
+  const int L = ir0.lanes;
+
+  std::vector<DevTb> tbs;
+  std::vector<DevOp> ops;
+  std::vector<DevDep> deps;
+  std::vector<DevChan> chans;
+  plan.sys_scope = false;
+  std::vector<int> sem_base_of_rank;
+  int sem_next = 0;
+  for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
+    sem_base_of_rank.push_back(sem_next);
+    sem_next += static_cast<int>(p.gpus[plan.ranks[slot]].tbs.size()) * L;
+  }
+  for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
+    const int r = plan.ranks[slot];
+    Comm* c = cl->local[r];
+    const RankIR& ir = *c->irs[id];
+    const Gpu& g = p.gpus[r];
+    for (size_t t = 0; t < g.tbs.size(); ++t) {
+      const ThreadBlock& tb = g.tbs[t];
+      DevTb d{};
+      d.rank_slot = static_cast<int>(slot);
+      d.op_begin = static_cast<int>(ops.size());
+      d.nops = static_cast<int>(tb.ops.size());
+      d.sem = sem_base_of_rank[slot] + static_cast<int>(t) * L;
+      d.chan_in = d.chan_out = -1;
+      for (const Op& op : tb.ops) {
+        DevOp o{};
+        o.opcode = static_cast<uint8_t>(op.op);
+        o.src_buf = static_cast<uint8_t>(op.src_buf);
+        o.dst_buf = static_cast<uint8_t>(op.dst_buf);
+        o.has_dep = op.has_dep ? 1 : 0;
+        o.src_off = op.src_off;
+        o.dst_off = op.dst_off;
+        o.count = op.count;
+        o.dep_begin = static_cast<int>(deps.size());
+        o.ndeps = static_cast<int16_t>(op.deps.size());
+        for (const Dep& dp : op.deps) {
+          const int ti = tb_index(p, r, dp.tb);
+          if (ti < 0) return set_error(ncclInvalidArgument, "IR dep on unknown tb %d", dp.tb);
+          DevDep dd{};
+          dd.sem = sem_base_of_rank[slot] + ti * L;
+          dd.step = dp.step;
+          dd.nops = static_cast<int>(g.tbs[ti].ops.size());
+          deps.push_back(dd);
+        }
+        ops.push_back(o);
+      }
+      if (tb.recv_peer >= 0) {
+        const int s = tb.recv_peer;
+        const int st = find_sender(p, s, r, tb.channel);
+        if (st < 0) return set_error(ncclInvalidArgument, "connection %d->%d ch %d has no sender", s, r, tb.channel);
+        char* sender_arena = nullptr;
+        NCCL_TRY(peer_arena(c, id, s, sender_arena));
+        if (!cl->local[s] || cl->local[s]->device != c->device) plan.sys_scope = true;
+        const int k = ir.lay.in_index[t];
+        const ArenaLayout slay = make_layout(p, s, L, ir.slots, ir.slot_bytes);
+        const int m = slay.out_index[st];
+        d.chan_in = static_cast<int>(chans.size());
+        for (int l = 0; l < L; ++l) {
+          DevChan ch{};
+          ch.fifo = ir.arena + ir.lay.off_fifo + (static_cast<size_t>(k) * L + l) * ir.slots * ir.slot_bytes;
+          ch.head = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_head + (static_cast<size_t>(k) * L + l) * kCounterStride);
+          ch.tail = reinterpret_cast<uint64_t*>(sender_arena + slay.off_tail + (static_cast<size_t>(m) * L + l) * kCounterStride);
+          ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_in + (static_cast<size_t>(k) * L + l) * 8);
+          chans.push_back(ch);
+        }
+      }
+      if (tb.send_peer >= 0) {
+        const int dst = tb.send_peer;
+        const int rt = find_receiver(p, r, dst, tb.channel);
+        if (rt < 0) return set_error(ncclInvalidArgument, "connection %d->%d ch %d has no receiver", r, dst, tb.channel);
+        char* recv_arena = nullptr;
+        NCCL_TRY(peer_arena(c, id, dst, recv_arena));
+        if (!cl->local[dst] || cl->local[dst]->device != c->device) plan.sys_scope = true;
+        const ArenaLayout rlay = make_layout(p, dst, L, ir.slots, ir.slot_bytes);
+        const int k = rlay.in_index[rt];
+        const int m = ir.lay.out_index[t];
+        d.chan_out = static_cast<int>(chans.size());
+        for (int l = 0; l < L; ++l) {
+          DevChan ch{};
+          ch.fifo = recv_arena + rlay.off_fifo + (static_cast<size_t>(k) * L + l) * ir.slots * ir.slot_bytes;
+          ch.head = reinterpret_cast<uint64_t*>(recv_arena + rlay.off_head + (static_cast<size_t>(k) * L + l) * kCounterStride);
+          ch.tail = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_tail + (static_cast<size_t>(m) * L + l) * kCounterStride);
+          ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_out + (static_cast<size_t>(m) * L + l) * 8);
+          chans.push_back(ch);
+        }
+      }
+      tbs.push_back(d);
+    }
+  }
+  for (const DevOp& o : ops)
+    if (o.ndeps > 400) return set_error(ncclInvalidArgument, "an op with %d deps exceeds the 400-dep limit", o.ndeps);
+  DeviceGuard g(ds.device);
+  auto upload = [&](auto*& dptr, const auto& vec) -> ncclResult_t {
+    using T = typename std::decay_t<decltype(vec)>::value_type;
+    const size_t n = std::max<size_t>(vec.size(), 1) * sizeof(T);
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&dptr), n));
+    if (!vec.empty()) CUDA_TRY(cudaMemcpy(dptr, vec.data(), vec.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return ncclSuccess;
+  };
+  NCCL_TRY(upload(plan.d_tbs, tbs));
+  NCCL_TRY(upload(plan.d_ops, ops));
+  NCCL_TRY(upload(plan.d_deps, deps));
+  NCCL_TRY(upload(plan.d_chans, chans));
+  const size_t nsem = std::max(sem_next, 1);
+  CUDA_TRY(cudaMalloc(&plan.d_sems, nsem * sizeof(uint64_t)));
+  CUDA_TRY(cudaMemset(plan.d_sems, 0, nsem * sizeof(uint64_t)));
+  plan.ntbs = static_cast<int>(tbs.size());
+  plan.built = true;
+  return ncclSuccess;
+}
+
+// Algorithmic traffic of one rank's program for a given chunk size.
+void traffic(const Program& p, int rank, int64_t chunk_bytes, int64_t& sent, int64_t& recvd, int64_t& hbm) {
+  sent = recvd = hbm = 0;
+  for (const auto& tb : p.gpus[rank].tbs)
+    for (const auto& op : tb.ops) {
+      const int64_t b = chunk_bytes * op.count;
+      if (op_sends(op.op)) sent += b;
+      if (op_receives(op.op)) recvd += b;
+      switch (op.op) {
+        case Opcode::send: hbm += b; break;
+        case Opcode::recv: hbm += b; break;
+        case Opcode::copy: hbm += 2 * b; break;
+        case Opcode::reduce: hbm += 3 * b; break;
+        case Opcode::rrc: hbm += 2 * b; break;
+        case Opcode::rcs: hbm += b; break;
+        case Opcode::rrcs: hbm += 2 * b; break;
+        case Opcode::rrs: hbm += b; break;
+        default: break;
+      }
+    }
+}
+
+// IR chunk geometry of a collective call: returns elements per chunk or -1 if not divisible.
+int64_t chunk_elems_for(const Program& p, int coll, size_t count, int nranks) {
+  const int cin = p.nchunks[0];
+  if (cin <= 0) return -1;
+  switch (coll) {
+    case kAllReduce: return count % cin ? -1 : static_cast<int64_t>(count / cin);
+    case kAllGather:
+      if (p.nchunks[1] != nranks * cin) return -1;
+      return count % cin ? -1 : static_cast<int64_t>(count / cin);
+    case kReduceScatter: {
+      if (cin % nranks) return -1;
+      const int c = cin / nranks;
+      return count % c ? -1 : static_cast<int64_t>(count / c);
+    }
+    case kAllToAll: {
+      if (cin % nranks || p.nchunks[1] != cin) return -1;
+      const int c = cin / nranks;
+      return count % c ? -1 : static_cast<int64_t>(count / c);
+    }
+  }
+  return -1;
+}
+
+// bytes used for size_range selection: the per-rank message buffer size
+uint64_t selection_bytes(int coll, size_t count, size_t esize, int nranks) {
+  switch (coll) {
+    case kAllReduce: return count * esize;
+    case kAllGather: return count * esize * nranks;
+    case kReduceScatter: return count * esize * nranks;
+    case kAllToAll: return count * esize * nranks;
+  }
+  return 0;
+}
+
+int select_ir(Comm* c, int coll, size_t count, int dtype) {
+  const uint64_t bytes = selection_bytes(coll, count, dtype_size(dtype), c->nranks);
+  for (size_t i = 0; i < c->irs.size(); ++i) {
+    const Program& p = c->irs[i]->prog;
+    if (p.collective != coll_name(coll)) continue;
+    if (bytes < p.min_bytes || bytes > p.max_bytes) continue;
+    if (chunk_elems_for(p, coll, count, c->nranks) < 0) continue;
+    return static_cast<int>(i);
+  }
+  return -1;
+}
+
+struct CallPlan {
+  int id = -1;
+  bool ll = false;
+  int lanes = 1;
+  int grid = 0;
+  int64_t chunk_elems = 0, tile_elems = 0, ntiles = 0;  // in kernel element units
+  int kesize = 1;                                          // kernel element size
+  KernelFn fn = nullptr;
+  int redop = -1;
+};
+
+ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count, int dtype, int redop, int nlocal_tbs, CallPlan& cp) {
+  const RankIR& ir = *c->irs[id];
+  const Program& p = ir.prog;
+  const size_t esize = dtype_size(dtype);
+  int64_t ce = chunk_elems_for(p, coll, count, c->nranks);
+  if (ce < 0) return set_error(ncclInvalidArgument, "count %zu does not divide into the IR's chunks", count);
+  cp.id = id;
+  cp.redop = ir.has_reduce ? redop : -1;
+  if (ir.has_reduce && (redop < 0 || redop > 3)) return set_error(ncclInvalidArgument, "unsupported reduction op %d", redop);
+  if (ir.has_reduce && (dtype == ncclFloat8e4m3 || dtype == ncclFloat8e5m2))
+    return set_error(ncclInvalidArgument, "fp8 reductions are not supported");
+  // copy-only programs run the byte kernel: element = 1 byte
+  cp.kesize = ir.has_reduce ? static_cast<int>(esize) : 1;
+  const int64_t chunk_bytes = ce * static_cast<int64_t>(esize);
+  cp.chunk_elems = chunk_bytes / cp.kesize;
+  const int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
+  cp.ll = proto == 1 && chunk_bytes % 8 == 0;
+  const int64_t cap_bytes = (cp.ll ? ir.slot_bytes / 2 : ir.slot_bytes) / std::max(1, ir.max_count);
+  int64_t tile_bytes_cap = cap_bytes / 16 * 16;
+  if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot too small for count %d", ir.max_count);
+  cp.fn = interp_kernel(cp.redop < 0 ? 0 : dtype, cp.redop, cp.ll);
+  if (!cp.fn) return set_error(ncclInvalidArgument, "no kernel for dtype %d op %d", dtype, redop);
+  auto it = ds.occupancy.find(cp.fn);
+  if (it == ds.occupancy.end()) it = ds.occupancy.emplace(cp.fn, interp_blocks_per_sm(cp.fn)).first;
+  const int capacity = it->second * ds.num_sms;
+  if (capacity < nlocal_tbs)
+    return set_error(ncclInvalidUsage, "%d thread blocks cannot be co-resident (capacity %d)", nlocal_tbs, capacity);
+  int lanes = c->cfg.lanes > 0 ? c->cfg.lanes : std::max(1, (2 * ds.num_sms) / std::max(1, nlocal_tbs));
+  lanes = std::min({lanes, ir.lanes, capacity / nlocal_tbs});
+  lanes = std::max(lanes, 1);
+  int64_t tile_bytes;
+  if (c->cfg.tile_bytes > 0) {
+    tile_bytes = std::min<int64_t>(c->cfg.tile_bytes / 16 * 16, tile_bytes_cap);
+  } else {
+    const int64_t per_lane = (chunk_bytes + lanes - 1) / lanes;
+    tile_bytes = std::min<int64_t>(align_up(static_cast<size_t>(std::max<int64_t>(per_lane, 16)), 16), tile_bytes_cap);
+  }
+  tile_bytes = std::max<int64_t>(tile_bytes, 16);
+  if (chunk_bytes <= tile_bytes) tile_bytes = chunk_bytes;
+  if (cp.ll && tile_bytes % 8) tile_bytes = tile_bytes / 8 * 8;
+  cp.tile_elems = std::max<int64_t>(tile_bytes / cp.kesize, chunk_bytes > 0 ? 1 : 0);
+  cp.ntiles = cp.tile_elems > 0 ? (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems : 0;
+  if (cp.ntiles < lanes) lanes = static_cast<int>(std::max<int64_t>(cp.ntiles, 1));
+  cp.lanes = lanes;
+  cp.grid = nlocal_tbs * lanes;
+  return ncclSuccess;
+}
+
+ncclResult_t ensure_buffer(Comm* c, char*& buf, size_t& have, size_t need) {
+  if (need <= have) return ncclSuccess;
+  DeviceGuard g(c->device);
+  if (buf) CUDA_TRY(cudaFree(buf));
+  buf = nullptr;
+  have = 0;
+  CUDA_TRY(cudaMalloc(&buf, need));
+  have = need;
+  return ncclSuccess;
+}
+
+// Launches one group's collectives that live on one device.
+ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
+  DeviceState* ds = nullptr;
+  NCCL_TRY(device_state(cl, dev, ds));
+  Comm* c0 = ops[0]->comm;
+  const Pending& p0 = *ops[0];
+  for (Pending* q : ops) {
+    if (q->coll != p0.coll || q->count != p0.count || q->dtype != p0.dtype || q->redop != p0.redop)
+      return set_error(ncclInvalidUsage, "ranks on one device issued mismatched collectives in a group");
+    if (q->comm->async_error != ncclSuccess) return set_error(q->comm->async_error, "communicator is in an error state");
+  }
+  if (p0.count == 0) return ncclSuccess;
+  const int id = select_ir(c0, p0.coll, p0.count, p0.dtype);
+  if (id < 0)
+    return set_error(ncclInvalidUsage, "no registered %s IR matches %zu elements of type %d (no NCCL fallback on this path)",
+                     coll_name(p0.coll), p0.count, p0.dtype);
+  NCCL_TRY(build_plan(cl, *ds, id));
+  DevicePlan& plan = ds->plans[id];
+  if (plan.ranks.size() != ops.size())
+    return set_error(ncclInvalidUsage, "all %zu ranks hosted on device %d must issue the collective in one group (got %zu)",
+                     plan.ranks.size(), dev, ops.size());
+  CallPlan cp;
+  NCCL_TRY(plan_call(c0, *ds, id, p0.coll, p0.count, p0.dtype, p0.redop, plan.ntbs, cp));
+  const RankIR& ir0 = *c0->irs[id];
+  const size_t esize = dtype_size(p0.dtype);
+  const int64_t chunk_bytes = cp.chunk_elems * cp.kesize;
+
+  LaunchArgs a{};
+  a.tbs = plan.d_tbs;
+  a.ops = plan.d_ops;
+  a.deps = plan.d_deps;
+  a.chans = plan.d_chans;
+  a.sems = plan.d_sems;
+  a.ntbs = plan.ntbs;
+  a.lanes = cp.lanes;
+  a.slots = ir0.slots;
+  a.sys_scope = plan.sys_scope ? 1 : 0;
+  a.slot_bytes = ir0.slot_bytes;
+  a.chunk_elems = cp.chunk_elems;
+  a.tile_elems = cp.tile_elems;
+  a.ntiles = cp.ntiles;
+  a.epoch = ++ds->epoch;
+  a.timeout_ns = static_cast<uint64_t>(c0->cfg.timeout_ms) * 1000000ull;
+  a.abort_flag = ds->d_abort;
+  a.err_info = ds->d_err;
+  // LaunchArgs::sems are indexed with the lane count used when the plan was built (ir.lanes); the
+  // kernel adds its lane (< cp.lanes <= ir.lanes) to each tb's base.
+  cudaStream_t stream = p0.stream;
+  DeviceGuard g(dev);
+  // order every participating stream before the launch stream
+  std::vector<cudaStream_t> others;
+  for (Pending* q : ops)
+    if (q->stream != stream && std::find(others.begin(), others.end(), q->stream) == others.end()) others.push_back(q->stream);
+  for (cudaStream_t s : others) {
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, s));
+    CUDA_TRY(cudaStreamWaitEvent(stream, ev, 0));
+    CUDA_TRY(cudaEventDestroy(ev));
+  }
+  for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
+    const int r = plan.ranks[slot];
+    Pending* q = nullptr;
+    for (Pending* x : ops)
+      if (x->comm->rank == r) q = x;
+    if (!q) return set_error(ncclInvalidUsage, "rank %d missing from the group", r);
+    Comm* c = q->comm;
+    const RankIR& ir = *c->irs[id];
+    const size_t scratch_need = static_cast<size_t>(ir.prog.nchunks[2]) * chunk_bytes;
+    NCCL_TRY(ensure_buffer(c, c->scratch, c->scratch_bytes, std::max<size_t>(scratch_need, 256)));
+    char* in = nullptr;
+    char* out = nullptr;
+    switch (p0.coll) {
+      case kAllReduce:  // in-place IR on `input` (core.hpp:305-327)
+        if (q->send != q->recv) CUDA_TRY(cudaMemcpyAsync(q->recv, q->send, p0.count * esize, cudaMemcpyDeviceToDevice, stream));
+        in = out = static_cast<char*>(q->recv);
+        break;
+      case kAllGather:
+        in = const_cast<char*>(static_cast<const char*>(q->send));
+        out = static_cast<char*>(q->recv);
+        break;
+      case kReduceScatter: {  // in-place IR over R*c chunks; rank r owns [r*c, (r+1)*c)
+        const size_t total = p0.count * esize * c->nranks;
+        NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, total));
+        CUDA_TRY(cudaMemcpyAsync(c->work, q->send, total, cudaMemcpyDeviceToDevice, stream));
+        in = out = c->work;
+        break;
+      }
+      case kAllToAll:
+        if (q->send == q->recv) return set_error(ncclInvalidArgument, "in-place AllToAll is not supported");
+        in = const_cast<char*>(static_cast<const char*>(q->send));
+        out = static_cast<char*>(q->recv);
+        break;
+    }
+    if (ir.prog.inplace) out = in;
+    a.bufs[slot][0] = in;
+    a.bufs[slot][1] = out;
+    a.bufs[slot][2] = c->scratch;
+  }
+  CUDA_TRY(interp_launch(cp.fn, a, cp.grid, stream));
+  for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
+    if (p0.coll != kReduceScatter) continue;
+    Pending* q = nullptr;
+    for (Pending* x : ops)
+      if (x->comm->rank == plan.ranks[slot]) q = x;
+    const size_t bytes = p0.count * esize;
+    CUDA_TRY(cudaMemcpyAsync(q->recv, q->comm->work + q->comm->rank * bytes, bytes, cudaMemcpyDeviceToDevice, stream));
+  }
+  for (cudaStream_t s : others) {
+    cudaEvent_t ev;
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ev, stream));
+    CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
+    CUDA_TRY(cudaEventDestroy(ev));
+  }
+  return ncclSuccess;
+}
+
+ncclResult_t flush_group() {
+  std::vector<Pending> pend;
+  pend.swap(g_pending);
+  std::map<std::pair<Clique*, int>, std::vector<Pending*>> by_dev;
+  for (Pending& q : pend) by_dev[{q.comm->clique, q.comm->device}].push_back(&q);
+  ncclResult_t rc = ncclSuccess;
+  for (auto& [key, ops] : by_dev) {
+    const ncclResult_t r = launch_device(key.first, key.second, ops);
+    if (r != ncclSuccess && rc == ncclSuccess) rc = r;
+  }
+  return rc;
+}
+
+ncclResult_t enqueue(const Pending& q) {
+  if (!q.comm || q.comm->destroyed) return set_error(ncclInvalidArgument, "invalid communicator");
+  if (q.dtype < 0 || q.dtype >= ncclNumTypes) return set_error(ncclInvalidArgument, "invalid datatype %d", q.dtype);
+  if (q.count > 0 && (!q.send || !q.recv)) return set_error(ncclInvalidArgument, "null buffer");
+  if (q.coll == kAllReduce || q.coll == kReduceScatter) {
+    if (q.redop == ncclAvg || q.redop < 0 || q.redop >= ncclNumOps) return set_error(ncclInvalidArgument, "unsupported reduction op %d", q.redop);
+  }
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  g_pending.push_back(q);
+  if (g_group_depth == 0) return flush_group();
+  return ncclSuccess;
+}
+
+// ------------------------------------------------------------------------------- init
+ncclResult_t make_comm(Clique* cl, int rank, int dev, Comm** out) {
+  auto* c = new gc3Comm();
+  c->clique = cl;
+  c->rank = rank;
+  c->nranks = cl->nranks;
+  c->device = dev;
+  c->cfg = config_from_env();
+  cl->local[rank] = c;
+  cl->rank_dev[rank] = dev;
+  cl->rank_pid[rank] = getpid();
+  cl->refs++;
+  *out = c;
+  return ncclSuccess;
+}
+
+}  // namespace
+}  // namespace gc3
+
+using namespace gc3;
+
+// =============================================================================== C ABI
+extern "C" {
+
+ncclResult_t ncclGetVersion(int* version) {
+  if (!version) return ncclInvalidArgument;
+  *version = GC3_VERSION_CODE;
+  return ncclSuccess;
+}
+
+const char* ncclGetErrorString(ncclResult_t r) {
+  switch (r) {
+    case ncclSuccess: return "no error";
+    case ncclUnhandledCudaError: return "unhandled cuda error (run with GC3_DEBUG=1 for details)";
+    case ncclSystemError: return "unhandled system error (run with GC3_DEBUG=1 for details)";
+    case ncclInternalError: return "internal error - please report this issue";
+    case ncclInvalidArgument: return "invalid argument (run with GC3_DEBUG=1 for details)";
+    case ncclInvalidUsage: return "invalid usage (run with GC3_DEBUG=1 for details)";
+    case ncclRemoteError: return "remote process exited or there was a network error";
+    case ncclInProgress: return "NCCL operation in progress";
+    default: return "unknown result code";
+  }
+}
+
+const char* ncclGetLastError(ncclComm_t) { return g_last_error.c_str(); }
+
+ncclResult_t ncclGetUniqueId(ncclUniqueId* id) {
+  if (!id) return ncclInvalidArgument;
+  std::memset(id->internal, 0, sizeof(id->internal));
+  std::memcpy(id->internal, "GC3", 4);
+  FILE* f = std::fopen("/dev/urandom", "rb");
+  size_t got = f ? std::fread(id->internal + 4, 1, 16, f) : 0;
+  if (f) std::fclose(f);
+  if (got != 16) {
+    const uint64_t t = static_cast<uint64_t>(std::chrono::high_resolution_clock::now().time_since_epoch().count()) ^
+                       (static_cast<uint64_t>(getpid()) << 32);
+    std::memcpy(id->internal + 4, &t, 8);
+  }
+  return ncclSuccess;
+}
+
+ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniqueId id, int rank) {
+  if (!comm || nranks < 1 || rank < 0 || rank >= nranks) return set_error(ncclInvalidArgument, "bad InitRank arguments");
+  if (std::memcmp(id.internal, "GC3", 4) != 0) return set_error(ncclInvalidArgument, "unique id not created by ncclGetUniqueId");
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  const std::string key = uid_key(id);
+  auto& slot = g_cliques[key];
+  if (!slot) {
+    slot = std::make_unique<Clique>();
+    slot->key = key;
+    slot->nranks = nranks;
+    slot->local.assign(nranks, nullptr);
+    slot->rank_dev.assign(nranks, -1);
+    slot->rank_pid.assign(nranks, 0);
+  }
+  Clique* cl = slot.get();
+  if (cl->nranks != nranks) return set_error(ncclInvalidArgument, "nranks mismatch for this unique id");
+  if (cl->local[rank]) return set_error(ncclInvalidUsage, "rank %d initialised twice", rank);
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  Comm* c = nullptr;
+  NCCL_TRY(make_comm(cl, rank, dev, &c));
+  // publish (pid, device) and learn the peers'
+  const std::string dir = shm_dir(key);
+  if (!post_record(dir, "rank" + std::to_string(rank), std::to_string(getpid()) + " " + std::to_string(dev)))
+    return set_error(ncclSystemError, "cannot write bootstrap record in %s", dir.c_str());
+  *comm = c;
+  return ncclSuccess;
+}
+
+ncclResult_t ncclCommInitAll(ncclComm_t* comms, int ndev, const int* devlist) {
+  if (!comms || ndev < 1) return set_error(ncclInvalidArgument, "bad InitAll arguments");
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  const std::string key = uid_key(id);
+  auto cl = std::make_unique<Clique>();
+  cl->key = key;
+  cl->nranks = ndev;
+  cl->local.assign(ndev, nullptr);
+  cl->rank_dev.assign(ndev, -1);
+  cl->rank_pid.assign(ndev, getpid());
+  std::set<int> devs;
+  for (int r = 0; r < ndev; ++r) {
+    const int dev = devlist ? devlist[r] : r;
+    Comm* c = nullptr;
+    NCCL_TRY(make_comm(cl.get(), r, dev, &c));
+    comms[r] = c;
+    devs.insert(dev);
+  }
+  // NVLink peer access between the distinct devices of this process
+  for (int a : devs)
+    for (int b : devs) {
+      if (a == b) continue;
+      int can = 0;
+      CUDA_TRY(cudaDeviceCanAccessPeer(&can, a, b));
+      if (!can) return set_error(ncclSystemError, "device %d cannot access peer %d", a, b);
+      DeviceGuard g(a);
+      const cudaError_t e = cudaDeviceEnablePeerAccess(b, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CUDA_TRY(e);
+      cudaGetLastError();
+    }
+  g_cliques[key] = std::move(cl);
+  return ncclSuccess;
+}
+
+static void release_comm(Comm* c) {
+  Clique* cl = c->clique;
+  DeviceGuard g(c->device);
+  for (void* p : c->opened_ipc) cudaIpcCloseMemHandle(p);
+  for (auto& ir : c->irs)
+    if (ir->arena) cudaFree(ir->arena);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->work) cudaFree(c->work);
+  cl->local[c->rank] = nullptr;
+  const std::string dir = shm_dir(cl->key);
+  unlink((dir + "/rank" + std::to_string(c->rank)).c_str());
+  for (size_t i = 0; i < c->irs.size(); ++i) unlink((dir + "/ir" + std::to_string(i) + ".rank" + std::to_string(c->rank)).c_str());
+  rmdir(dir.c_str());  // succeeds for the last rank only
+  c->destroyed = true;
+  if (--cl->refs == 0) {
+    for (auto& [dev, ds] : cl->devs) {
+      DeviceGuard gd(dev);
+      for (auto& p : ds.plans) {
+        cudaFree(p.d_tbs);
+        cudaFree(p.d_ops);
+        cudaFree(p.d_deps);
+        cudaFree(p.d_chans);
+        cudaFree(p.d_sems);
+      }
+      cudaFree(ds.d_abort);
+      cudaFreeHost(ds.h_err);
+    }
+    g_cliques.erase(cl->key);
+  }
+  delete c;
+}
+
+ncclResult_t ncclCommDestroy(ncclComm_t comm) {
+  if (!comm) return ncclInvalidArgument;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  {
+    DeviceGuard g(comm->device);
+    cudaDeviceSynchronize();
+  }
+  release_comm(comm);
+  return ncclSuccess;
+}
+
+ncclResult_t ncclCommAbort(ncclComm_t comm) {
+  if (!comm) return ncclInvalidArgument;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  // raise the device abort flag so spinning blocks exit, then tear down
+  auto it = comm->clique->devs.find(comm->device);
+  if (it != comm->clique->devs.end() && it->second.d_abort) {
+    DeviceGuard g(comm->device);
+    const int one = 1;
+    cudaMemcpy(it->second.d_abort, &one, sizeof(one), cudaMemcpyHostToDevice);
+    cudaDeviceSynchronize();
+  }
+  release_comm(comm);
+  return ncclSuccess;
+}
+
+ncclResult_t ncclCommGetAsyncError(ncclComm_t comm, ncclResult_t* err) {
+  if (!comm || !err) return ncclInvalidArgument;
+  *err = comm->async_error;
+  auto it = comm->clique->devs.find(comm->device);
+  if (*err == ncclSuccess && it != comm->clique->devs.end() && it->second.h_err) {
+    volatile uint64_t* e = it->second.h_err;
+    if (e[0]) {
+      static const char* what[] = {"?", "dependency semaphore", "send slot credit", "receive slot", "LL line"};
+      const uint64_t w = e[5] < 5 ? e[5] : 0;
+      comm->async_error = ncclSystemError;
+      set_error(ncclSystemError, "watchdog: launch rank-slot %llu tb %llu step %llu tile %llu timed out waiting on %s",
+                (unsigned long long)e[1], (unsigned long long)e[2], (unsigned long long)e[3], (unsigned long long)e[4], what[w]);
+      comm->last_error = g_last_error;
+      *err = ncclSystemError;
+    }
+  }
+  return ncclSuccess;
+}
+
+ncclResult_t ncclCommCount(const ncclComm_t comm, int* count) {
+  if (!comm || !count) return ncclInvalidArgument;
+  *count = comm->nranks;
+  return ncclSuccess;
+}
+ncclResult_t ncclCommCuDevice(const ncclComm_t comm, int* device) {
+  if (!comm || !device) return ncclInvalidArgument;
+  *device = comm->device;
+  return ncclSuccess;
+}
+ncclResult_t ncclCommUserRank(const ncclComm_t comm, int* rank) {
+  if (!comm || !rank) return ncclInvalidArgument;
+  *rank = comm->rank;
+  return ncclSuccess;
+}
+
+ncclResult_t ncclGroupStart(void) {
+  ++g_group_depth;
+  return ncclSuccess;
+}
+
+ncclResult_t ncclGroupEnd(void) {
+  if (g_group_depth <= 0) return set_error(ncclInvalidUsage, "ncclGroupEnd without ncclGroupStart");
+  if (--g_group_depth > 0) return ncclSuccess;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  return flush_group();
+}
+
+ncclResult_t ncclAllReduce(const void* sendbuff, void* recvbuff, size_t count, ncclDataType_t datatype, ncclRedOp_t op,
+                           ncclComm_t comm, cudaStream_t stream) {
+  return enqueue(Pending{comm, kAllReduce, sendbuff, recvbuff, count, datatype, op, stream});
+}
+ncclResult_t ncclReduceScatter(const void* sendbuff, void* recvbuff, size_t recvcount, ncclDataType_t datatype,
+                               ncclRedOp_t op, ncclComm_t comm, cudaStream_t stream) {
+  return enqueue(Pending{comm, kReduceScatter, sendbuff, recvbuff, recvcount, datatype, op, stream});
+}
+ncclResult_t ncclAllGather(const void* sendbuff, void* recvbuff, size_t sendcount, ncclDataType_t datatype, ncclComm_t comm,
+                           cudaStream_t stream) {
+  return enqueue(Pending{comm, kAllGather, sendbuff, recvbuff, sendcount, datatype, -1, stream});
+}
+ncclResult_t ncclAlltoAll(const void* sendbuff, void* recvbuff, size_t count, ncclDataType_t datatype, ncclComm_t comm,
+                          cudaStream_t stream) {
+  return enqueue(Pending{comm, kAllToAll, sendbuff, recvbuff, count, datatype, -1, stream});
+}
+ncclResult_t ncclAllToAll(const void* sendbuff, void* recvbuff, size_t count, ncclDataType_t datatype, ncclComm_t comm,
+                          cudaStream_t stream) {
+  return ncclAlltoAll(sendbuff, recvbuff, count, datatype, comm, stream);
+}
+
+ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instances, int* ir_id) {
+  if (!comm || !path_or_json) return set_error(ncclInvalidArgument, "null argument");
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  std::string text;
+  if (!read_ir_text(path_or_json, text)) return set_error(ncclSystemError, "io: cannot open IR file %s", path_or_json);
+  auto ir = std::make_unique<RankIR>();
+  SchemaError se;
+  if (!parse_program(text, ir->prog, se)) return set_error(ncclInvalidArgument, "%s", se.what().c_str());
+  if (instances > 1) ir->prog = replicate_instances(ir->prog, instances);
+  Topology topo;
+  topo.nodes = 1;
+  topo.gpus_per_node = comm->nranks;
+  topo.max_threadblocks = 148;
+  topo.max_channels = 1 << 20;
+  const auto issues = validate(ir->prog, topo);
+  if (!issues.empty()) return set_error(ncclInvalidUsage, "IR %s fails validation: %s", ir->prog.name.c_str(), issues[0].c_str());
+  if (ir->prog.collective != "allreduce" && ir->prog.collective != "allgather" && ir->prog.collective != "reducescatter" &&
+      ir->prog.collective != "alltoall")
+    return set_error(ncclInvalidUsage, "collective %s has no NCCL entry point", ir->prog.collective.c_str());
+  for (const auto& g : ir->prog.gpus)
+    for (const auto& tb : g.tbs)
+      for (const auto& op : tb.ops) {
+        if (op_reduces(op.op)) ir->has_reduce = true;
+        if (op_sends(op.op) || op_receives(op.op)) ir->max_count = std::max(ir->max_count, op.count);
+      }
+  ir->slots = std::max(1, comm->cfg.slots);
+  ir->slot_bytes = std::max<int64_t>(comm->cfg.slot_bytes / 256 * 256, 256);
+  ir->lanes = std::max(1, comm->cfg.max_lanes);
+  ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes);
+  {
+    DeviceGuard g(comm->device);
+    CUDA_TRY(cudaMalloc(&ir->arena, ir->lay.bytes));
+    CUDA_TRY(cudaMemset(ir->arena, 0, ir->lay.bytes));
+    CUDA_TRY(cudaDeviceSynchronize());
+    // publish the arena to the other processes of the clique
+    bool remote_peers = false;
+    for (int r = 0; r < comm->nranks; ++r) remote_peers = remote_peers || !comm->clique->local[r];
+    if (remote_peers) {
+      CUDA_TRY(cudaIpcGetMemHandle(&ir->handle, ir->arena));
+      const std::string rec(reinterpret_cast<const char*>(&ir->handle), sizeof(ir->handle));
+      const int id = static_cast<int>(comm->irs.size());
+      if (!post_record(shm_dir(comm->clique->key), "ir" + std::to_string(id) + ".rank" + std::to_string(comm->rank), rec))
+        return set_error(ncclSystemError, "cannot publish arena handle");
+    }
+  }
+  comm->irs.push_back(std::move(ir));
+  if (ir_id) *ir_id = static_cast<int>(comm->irs.size()) - 1;
+  return ncclSuccess;
+}
+
+ncclResult_t gc3SetProtocolOverride(ncclComm_t comm, int ir_id, int proto) {
+  if (!comm || ir_id < 0 || ir_id >= static_cast<int>(comm->irs.size()) || proto < -1 || proto > 2)
+    return set_error(ncclInvalidArgument, "bad protocol override");
+  comm->irs[ir_id]->proto_override = proto;
+  return ncclSuccess;
+}
+
+ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
+  if (!comm || !key) return ncclInvalidArgument;
+  const std::string k = key;
+  Config& c = comm->cfg;
+  if (k == "slots") c.slots = static_cast<int>(value);
+  else if (k == "slot_bytes") c.slot_bytes = value;
+  else if (k == "max_lanes") c.max_lanes = static_cast<int>(value);
+  else if (k == "lanes") c.lanes = static_cast<int>(value);
+  else if (k == "tile_bytes") c.tile_bytes = value;
+  else if (k == "timeout_ms") c.timeout_ms = value;
+  else return set_error(ncclInvalidArgument, "unknown config key %s", key);
+  return ncclSuccess;
+}
+
+ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDataType_t datatype, gc3PlanInfo* info) {
+  if (!comm || !info || collective < 0 || collective > 3) return ncclInvalidArgument;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  std::memset(info, 0, sizeof(*info));
+  info->ir_id = select_ir(comm, collective, count, datatype);
+  if (info->ir_id < 0) return ncclSuccess;
+  DeviceState* ds = nullptr;
+  NCCL_TRY(device_state(comm->clique, comm->device, ds));
+  int ntbs = 0, nlocal = 0;
+  const RankIR& ir = *comm->irs[info->ir_id];
+  for (int r = 0; r < comm->nranks; ++r)
+    if (comm->clique->local[r] && comm->clique->local[r]->device == comm->device) {
+      ntbs += static_cast<int>(ir.prog.gpus[r].tbs.size());
+      ++nlocal;
+    }
+  CallPlan cp;
+  NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1, ntbs, cp));
+  info->protocol = cp.ll ? 1 : 0;
+  info->lanes = cp.lanes;
+  info->grid = cp.grid;
+  info->local_ranks = nlocal;
+  info->slots = ir.slots;
+  info->chunk_elems = cp.chunk_elems * cp.kesize / static_cast<int64_t>(dtype_size(datatype));
+  info->tile_elems = cp.tile_elems * cp.kesize / static_cast<int64_t>(dtype_size(datatype));
+  info->ntiles = cp.ntiles;
+  info->slot_bytes = ir.slot_bytes;
+  const int64_t chunk_bytes = cp.chunk_elems * cp.kesize;
+  int64_t wire = 0, hbm = 0;
+  for (int r = 0; r < comm->nranks; ++r) {
+    int64_t s, rv, h;
+    traffic(ir.prog, r, chunk_bytes, s, rv, h);
+    wire = std::max({wire, s, rv});
+    if (comm->clique->local[r] && comm->clique->local[r]->device == comm->device) hbm += h;
+  }
+  info->wire_bytes = wire;
+  info->hbm_bytes = hbm;
+  std::snprintf(info->name, sizeof(info->name), "%s", ir.prog.name.c_str());
+  return ncclSuccess;
+}
+
+// ------------------------------------------------------------------------------- IR library
+struct gc3Ir {
+  Program p;
+};
+
+static char* dup_cstr(const std::string& s) {
+  char* p = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(p, s.c_str(), s.size() + 1);
+  return p;
+}
+
+ncclResult_t gc3IrParse(const char* text, gc3Ir_t* ir, char** err) {
+  if (!text || !ir) return ncclInvalidArgument;
+  auto h = std::make_unique<gc3Ir>();
+  SchemaError se;
+  if (!parse_program(text, h->p, se)) {
+    if (err) *err = dup_cstr(se.path + "\t" + se.message);
+    *ir = nullptr;
+    return ncclInvalidArgument;
+  }
+  if (err) *err = nullptr;
+  *ir = h.release();
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrSerialize(gc3Ir_t ir, char** text) {
+  if (!ir || !text) return ncclInvalidArgument;
+  *text = dup_cstr(serialize(ir->p));
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrValidate(gc3Ir_t ir, int nodes, int gpus_per_node, int max_threadblocks, int max_channels, char** issues) {
+  if (!ir || !issues) return ncclInvalidArgument;
+  Topology t;
+  t.nodes = nodes;
+  t.gpus_per_node = gpus_per_node;
+  if (max_threadblocks > 0) t.max_threadblocks = max_threadblocks;
+  if (max_channels > 0) t.max_channels = max_channels;
+  std::string s;
+  for (const auto& i : validate(ir->p, t)) s += i + "\n";
+  *issues = dup_cstr(s);
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrCheckSlots(gc3Ir_t ir, int slots, char** violations) {
+  if (!ir || !violations) return ncclInvalidArgument;
+  std::string s;
+  for (const auto& v : check_slots(ir->p, slots)) s += v.what + "\n";
+  *violations = dup_cstr(s);
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrReplicate(gc3Ir_t ir, int instances, gc3Ir_t* out) {
+  if (!ir || !out || instances < 1) return ncclInvalidArgument;
+  auto h = std::make_unique<gc3Ir>();
+  h->p = replicate_instances(ir->p, instances);
+  *out = h.release();
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrFree(gc3Ir_t ir) {
+  delete ir;
+  return ncclSuccess;
+}
+
+void gc3Free(void* p) { std::free(p); }
+
+}  // extern "C"

@@ -1,0 +1,265 @@
+"""ctypes bindings of libgc3.so (include/gc3.h).
+
+Mirrors the NCCL entry points the GC3 paper's runtime exposes plus the GC3
+extensions, with NCCL's argument meaning and error behaviour: every call returns ncclResult_t and
+a non-zero result raises NcclError carrying ncclGetLastError().
+"""
+import contextlib
+import ctypes
+import os
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libgc3.so")
+
+# ncclDataType_t (nccl.h:278-290) keyed by torch dtype name
+NCCL_DTYPES = {
+    "int8": 0, "uint8": 1, "int32": 2, "uint32": 3, "int64": 4, "uint64": 5,
+    "float16": 6, "float32": 7, "float64": 8, "bfloat16": 9,
+}
+REDOPS = {"sum": 0, "prod": 1, "max": 2, "min": 3}
+COLLS = {"allreduce": 0, "allgather": 1, "reducescatter": 2, "alltoall": 3}
+
+
+def coll_id(name):
+    return COLLS[name]
+
+
+class NcclError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"ncclResult {code}: {msg}")
+        self.code = code
+
+
+class PlanInfo(ctypes.Structure):
+    _fields_ = [
+        ("ir_id", ctypes.c_int), ("protocol", ctypes.c_int), ("lanes", ctypes.c_int), ("grid", ctypes.c_int),
+        ("local_ranks", ctypes.c_int), ("slots", ctypes.c_int),
+        ("chunk_elems", ctypes.c_int64), ("tile_elems", ctypes.c_int64), ("ntiles", ctypes.c_int64),
+        ("slot_bytes", ctypes.c_int64), ("wire_bytes", ctypes.c_int64), ("hbm_bytes", ctypes.c_int64),
+        ("name", ctypes.c_char * 64),
+    ]
+
+    def as_dict(self):
+        d = {k: getattr(self, k) for k, _ in self._fields_}
+        d["name"] = self.name.decode()
+        return d
+
+
+class UniqueId(ctypes.Structure):
+    _fields_ = [("internal", ctypes.c_char * 128)]
+
+
+_lib = None
+
+
+def lib():
+    """Loads libgc3.so (never a fallback: a missing library is an error)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2201_11840_b200.build`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i, sz, cp = ctypes.c_void_p, ctypes.c_int, ctypes.c_size_t, ctypes.c_char_p
+    sigs = {
+        "ncclGetVersion": [ctypes.POINTER(i)],
+        "ncclGetUniqueId": [ctypes.POINTER(UniqueId)],
+        "ncclCommInitRank": [ctypes.POINTER(vp), i, UniqueId, i],
+        "ncclCommInitAll": [ctypes.POINTER(vp), i, ctypes.POINTER(i)],
+        "ncclCommDestroy": [vp],
+        "ncclCommAbort": [vp],
+        "ncclCommGetAsyncError": [vp, ctypes.POINTER(i)],
+        "ncclCommCount": [vp, ctypes.POINTER(i)],
+        "ncclCommCuDevice": [vp, ctypes.POINTER(i)],
+        "ncclCommUserRank": [vp, ctypes.POINTER(i)],
+        "ncclAllReduce": [vp, vp, sz, i, i, vp, vp],
+        "ncclReduceScatter": [vp, vp, sz, i, i, vp, vp],
+        "ncclAllGather": [vp, vp, sz, i, vp, vp],
+        "ncclAlltoAll": [vp, vp, sz, i, vp, vp],
+        "ncclAllToAll": [vp, vp, sz, i, vp, vp],
+        "ncclGroupStart": [],
+        "ncclGroupEnd": [],
+        "gc3RegisterIR": [vp, cp, i, ctypes.POINTER(i)],
+        "gc3SetProtocolOverride": [vp, i, i],
+        "gc3QueryPlan": [vp, i, sz, i, ctypes.POINTER(PlanInfo)],
+        "gc3SetConfig": [vp, cp, ctypes.c_int64],
+        "gc3IrParse": [cp, ctypes.POINTER(vp), ctypes.POINTER(vp)],
+        "gc3IrSerialize": [vp, ctypes.POINTER(vp)],
+        "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
+        "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
+        "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
+        "gc3IrFree": [vp],
+    }
+    for name, args in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.ncclGetErrorString.argtypes = [i]
+    L.ncclGetErrorString.restype = cp
+    L.ncclGetLastError.argtypes = [vp]
+    L.ncclGetLastError.restype = cp
+    L.gc3Free.argtypes = [vp]
+    L.gc3Free.restype = None
+    _lib = L
+    return L
+
+
+def check(rc, comm=None):
+    if rc != 0:
+        L = lib()
+        raise NcclError(rc, f"{L.ncclGetErrorString(rc).decode()}: {L.ncclGetLastError(comm).decode()}")
+
+
+def _take(p):
+    s = ctypes.string_at(p).decode() if p else ""
+    if p:
+        lib().gc3Free(p)
+    return s
+
+
+# ---------------------------------------------------------------------------- IR library
+class IR:
+    """Host-only handle on a parsed GC3-IR (reference ir.hpp semantics)."""
+
+    def __init__(self, text):
+        L = lib()
+        h, err = ctypes.c_void_p(), ctypes.c_void_p()
+        rc = L.gc3IrParse(text.encode() if isinstance(text, str) else text, ctypes.byref(h), ctypes.byref(err))
+        if rc != 0:
+            path, _, msg = _take(err.value).partition("\t")
+            e = NcclError(rc, f"schema: {path}: {msg}")
+            e.path, e.message = path, msg
+            raise e
+        self._h = h
+
+    @classmethod
+    def _wrap(cls, h):
+        obj = cls.__new__(cls)
+        obj._h = h
+        return obj
+
+    def serialize(self):
+        out = ctypes.c_void_p()
+        check(lib().gc3IrSerialize(self._h, ctypes.byref(out)))
+        return _take(out.value)
+
+    def validate(self, nodes, gpus_per_node, max_threadblocks=0, max_channels=0):
+        out = ctypes.c_void_p()
+        check(lib().gc3IrValidate(self._h, nodes, gpus_per_node, max_threadblocks, max_channels, ctypes.byref(out)))
+        return [x for x in _take(out.value).split("\n") if x]
+
+    def check_slots(self, slots):
+        out = ctypes.c_void_p()
+        check(lib().gc3IrCheckSlots(self._h, slots, ctypes.byref(out)))
+        return [x for x in _take(out.value).split("\n") if x]
+
+    def replicate(self, instances):
+        out = ctypes.c_void_p()
+        check(lib().gc3IrReplicate(self._h, instances, ctypes.byref(out)))
+        return IR._wrap(out)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.gc3IrFree(self._h)
+            self._h = None
+
+
+# ---------------------------------------------------------------------------- communicators
+def _ptr(x):
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    return x.data_ptr()
+
+
+def _stream(s):
+    if s is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    return s if isinstance(s, int) else s.cuda_stream
+
+
+class Comm:
+    """One rank (ncclComm_t)."""
+
+    def __init__(self, handle):
+        self.h = ctypes.c_void_p(handle)
+        n, r, d = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        L = lib()
+        check(L.ncclCommCount(self.h, ctypes.byref(n)))
+        check(L.ncclCommUserRank(self.h, ctypes.byref(r)))
+        check(L.ncclCommCuDevice(self.h, ctypes.byref(d)))
+        self.nranks, self.rank, self.device = n.value, r.value, d.value
+
+    def register_ir(self, path_or_json, instances=1):
+        out = ctypes.c_int()
+        check(lib().gc3RegisterIR(self.h, path_or_json.encode(), instances, ctypes.byref(out)), self.h)
+        return out.value
+
+    def set_protocol(self, ir_id, proto):
+        check(lib().gc3SetProtocolOverride(self.h, ir_id, {None: -1, "simple": 0, "ll": 1, "ll128": 2}.get(proto, proto)), self.h)
+
+    def set_config(self, key, value):
+        check(lib().gc3SetConfig(self.h, key.encode(), int(value)), self.h)
+
+    def query_plan(self, coll, count, dtype):
+        info = PlanInfo()
+        check(lib().gc3QueryPlan(self.h, COLLS[coll], count, NCCL_DTYPES[dtype], ctypes.byref(info)), self.h)
+        return info.as_dict()
+
+    def async_error(self):
+        e = ctypes.c_int()
+        check(lib().ncclCommGetAsyncError(self.h, ctypes.byref(e)))
+        return e.value, lib().ncclGetLastError(self.h).decode()
+
+    # collectives: buffers are torch tensors (or raw device pointers), dtype a torch dtype name
+    def all_reduce(self, send, recv, count, dtype, op="sum", stream=None):
+        check(lib().ncclAllReduce(_ptr(send), _ptr(recv), count, NCCL_DTYPES[dtype], REDOPS[op], self.h, _stream(stream)), self.h)
+
+    def reduce_scatter(self, send, recv, recvcount, dtype, op="sum", stream=None):
+        check(lib().ncclReduceScatter(_ptr(send), _ptr(recv), recvcount, NCCL_DTYPES[dtype], REDOPS[op], self.h, _stream(stream)), self.h)
+
+    def all_gather(self, send, recv, sendcount, dtype, stream=None):
+        check(lib().ncclAllGather(_ptr(send), _ptr(recv), sendcount, NCCL_DTYPES[dtype], self.h, _stream(stream)), self.h)
+
+    def all_to_all(self, send, recv, count, dtype, stream=None):
+        check(lib().ncclAlltoAll(_ptr(send), _ptr(recv), count, NCCL_DTYPES[dtype], self.h, _stream(stream)), self.h)
+
+    def destroy(self):
+        if self.h:
+            check(lib().ncclCommDestroy(self.h))
+            self.h = None
+
+
+@contextlib.contextmanager
+def group():
+    L = lib()
+    check(L.ncclGroupStart())
+    try:
+        yield
+    finally:
+        check(L.ncclGroupEnd())
+
+
+def init_all(devices):
+    """ncclCommInitAll; repeating a device creates loopback ranks that share it."""
+    n = len(devices)
+    arr = (ctypes.c_void_p * n)()
+    devs = (ctypes.c_int * n)(*devices)
+    check(lib().ncclCommInitAll(arr, n, devs))
+    return [Comm(arr[k]) for k in range(n)]
+
+
+def get_unique_id():
+    uid = UniqueId()
+    check(lib().ncclGetUniqueId(ctypes.byref(uid)))
+    return bytes(uid.internal)
+
+
+def init_rank(nranks, uid_bytes, rank):
+    uid = UniqueId()
+    uid.internal = uid_bytes
+    h = ctypes.c_void_p()
+    check(lib().ncclCommInitRank(ctypes.byref(h), nranks, uid, rank))
+    return Comm(h.value)

@@ -1,0 +1,169 @@
+"""GPU parity: the sm_100a interpreter (through the C ABI) vs the CPU oracle, bit for bit.
+
+All R ranks of an IR run as loopback ranks on cuda:0 (ncclCommInitAll with a repeated device),
+so cross-rank FIFO / flag / semaphore logic is exercised inside one cooperative launch.
+"""
+import json
+
+import numpy as np
+import pytest
+
+from conftest import ir_path, read_ir
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+COLL_OF = {"allreduce": "allreduce", "allgather": "allgather", "reducescatter": "reducescatter", "alltoall": "alltoall"}
+
+
+def _setup(name, instances=1, proto=None, **cfg):
+    from paper_2201_11840_b200 import gc3
+    text = read_ir(name)
+    R = len(json.loads(text)["gpus"])
+    comms = gc3.init_all([0] * R)
+    for c in comms:
+        for k, v in cfg.items():
+            c.set_config(k, v)
+    ids = [c.register_ir(ir_path(name), instances) for c in comms]
+    if proto is not None:
+        for c, i in zip(comms, ids):
+            c.set_protocol(i, proto)
+    ir_json = comms[0] and gc3.IR(text).replicate(instances).serialize() if instances > 1 else text
+    return comms, json.loads(ir_json)
+
+
+def _check(name, count, dtype="float32", op="sum", instances=1, proto=None, inplace=False, seed=0, **cfg):
+    from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
+    comms, irj = _setup(name, instances, proto, **cfg)
+    try:
+        coll = irj["collective"]
+        R = len(comms)
+        inputs = [make_input(input_len(coll, count, R), dtype, seed * 100 + r) for r in range(R)]
+        expected = oracle_collective(irj, coll, [x.clone() for x in inputs], count, dtype, op)
+        outs = run_collective(comms, coll, inputs, count, dtype, op, inplace=inplace)
+        torch.cuda.synchronize()
+        for c in comms:
+            err, msg = c.async_error()
+            assert err == 0, msg
+        for r in range(R):
+            got = to_np_bits(outs[r], dtype)
+            exp = expected[r]
+            if not np.array_equal(got.view(exp.dtype) if got.dtype != exp.dtype else got, exp):
+                bad = np.nonzero(got.view(exp.dtype) != exp)[0] if got.size == exp.size else []
+                raise AssertionError(f"rank {r}: {len(bad)} mismatches, first at {bad[:8]}")
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+@pytest.mark.parametrize("name,count", [
+    ("ring_ar_8_ch1", 8 * 1024), ("ring_ar_8_ch1", 1 << 20), ("ring_ar_8_ch8_inst4", 32 * 4096),
+    ("ring_ar_8_inst4_auto", 32 * 1000), ("hier_ar_2x4_par1", 8 * 4096), ("hier_ar_2x4_par2", 16 * 512),
+    ("allpairs_ar_8", 8 * 777), ("ring_ar_4_ch1", 4 * 3000), ("ring_ar_2_ch1", 2 * 64),
+    ("ring_ar_8_ch8_inst1.unfused", 8 * 1024), ("hier_ar_2x4_par1.unfused", 8 * 2048),
+])
+def test_allreduce_f32(name, count):
+    _check(name, count)
+
+
+@pytest.mark.parametrize("dtype,op", [("bfloat16", "sum"), ("float16", "sum"), ("int32", "sum"), ("float64", "sum"),
+                                      ("int64", "prod"), ("float32", "max"), ("bfloat16", "min"), ("uint8", "sum"),
+                                      ("int8", "max"), ("uint32", "prod")])
+def test_allreduce_dtypes(dtype, op):
+    _check("hier_ar_2x4_par1", 8 * 2048, dtype, op)
+
+
+@pytest.mark.parametrize("name,count", [("ring_ag_8", 4096), ("ring_ag_4", 1000), ("ring_ag_2", 7)])
+def test_allgather(name, count):
+    _check(name, count)
+    _check(name, count, inplace=True, dtype="bfloat16")
+
+
+@pytest.mark.parametrize("name,count", [("ring_rs_8", 4096), ("ring_rs_4", 999), ("ring_rs_2", 16)])
+def test_reducescatter(name, count):
+    _check(name, count)
+    _check(name, count, inplace=True, dtype="bfloat16")
+
+
+@pytest.mark.parametrize("name,count", [("twostep_a2a_2x4", 4096), ("twostep_a2a_1x8", 1024), ("twostep_a2a_2x2", 333),
+                                        ("twostep_a2a_1x2", 5)])
+def test_alltoall(name, count):
+    _check(name, count)
+
+
+def test_allreduce_out_of_place_and_in_place():
+    _check("ring_ar_8_ch1", 8 * 2000, inplace=False)
+    _check("ring_ar_8_ch1", 8 * 2000, inplace=True)
+
+
+@pytest.mark.parametrize("name,count", [("ring_ar_8_ch1", 8 * 4096), ("hier_ar_2x4_par1", 8 * 4096),
+                                        ("twostep_a2a_2x4", 2048), ("ring_rs_8", 1024), ("ring_ag_8", 1024)])
+def test_ll_protocol(name, count):
+    _check(name, count, proto="ll")
+    _check(name, count, proto="ll", dtype="bfloat16")
+
+
+@pytest.mark.parametrize("lanes,tile_bytes", [(1, 0), (3, 0), (16, 0), (4, 1040), (7, 48)])
+def test_lanes_and_tiles(lanes, tile_bytes):
+    _check("hier_ar_2x4_par1", 8 * 5000, lanes=lanes, tile_bytes=tile_bytes)
+    _check("twostep_a2a_2x4", 3000, lanes=lanes, tile_bytes=tile_bytes)
+
+
+def test_instances_runtime_rewrite():
+    _check("ring_ar_8_ch8_inst1", 32 * 512, instances=4)
+
+
+def test_repeated_launches_keep_fifo_counters_consistent():
+    from gpu_util import make_input, oracle_collective, run_collective, to_np_bits
+    comms, irj = _setup("ring_ar_8_ch1")
+    try:
+        for it, count in enumerate([8 * 100, 8 * 4096, 8, 8 * 12345]):
+            inputs = [make_input(count, "float32", 10 * it + r) for r in range(8)]
+            expected = oracle_collective(irj, "allreduce", [x.clone() for x in inputs], count, "float32")
+            outs = run_collective(comms, "allreduce", inputs, count, "float32")
+            torch.cuda.synchronize()
+            for r in range(8):
+                assert np.array_equal(to_np_bits(outs[r], "float32"), expected[r])
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+def test_watchdog_reports_deadlock_instead_of_hanging():
+    """SURVEY Finding 1 on hardware: s=1 deadlocks ring_ar_8_ch1; the watchdog must report it."""
+    from gpu_util import make_input, run_collective
+    comms, irj = _setup("ring_ar_8_ch1", slots=1, timeout_ms=1500, lanes=1)
+    try:
+        inputs = [make_input(8 * 65536, "float32", r) for r in range(8)]
+        for c in comms:
+            c.set_config("tile_bytes", 4096)
+        run_collective(comms, "allreduce", inputs, 8 * 65536, "float32")
+        torch.cuda.synchronize()
+        err, msg = comms[0].async_error()
+        assert err != 0 and "watchdog" in msg
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+def test_size_range_selection_and_no_fallback():
+    from paper_2201_11840_b200 import gc3
+    text = json.loads(read_ir("ring_ar_8_ch1"))
+    small = dict(text, name="small", size_range={"min_bytes": 0, "max_bytes": 4096})
+    big = dict(text, name="big", size_range={"min_bytes": 4097, "max_bytes": 1 << 40})
+    comms = gc3.init_all([0] * 8)
+    try:
+        for c in comms:
+            c.register_ir(json.dumps(small))
+            c.register_ir(json.dumps(big))
+        assert comms[0].query_plan("allreduce", 1024, "float32")["name"] == "small"
+        assert comms[0].query_plan("allreduce", 8192, "float32")["name"] == "big"
+        assert comms[0].query_plan("allgather", 8192, "float32")["ir_id"] == -1
+        with pytest.raises(gc3.NcclError):
+            with gc3.group():
+                for c in comms:
+                    x = torch.zeros(64, device="cuda")
+                    c.all_gather(x, torch.zeros(512, device="cuda"), 64, "float32")
+    finally:
+        for c in comms:
+            c.destroy()
