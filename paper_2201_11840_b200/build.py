@@ -15,15 +15,17 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-BUILD = os.path.join(PKG, "_build")
-LIB = os.path.join(PKG, "libgc3.so")
+BUILD = os.path.join(PKG, "_build" + os.environ.get("GC3_BUILD_TAG", ""))
+LIB = os.environ.get("GC3_LIB_OUT", os.path.join(PKG, "libgc3.so"))
+# extra nvcc defines for tuning builds, e.g. GC3_NVCC_DEFS="-DGC3_THREADS=256 -DGC3_UNROLL=8"
+NVCC_DEFS = os.environ.get("GC3_NVCC_DEFS", "").split()
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CXX_SRCS = ["json.cpp", "ir.cpp", "runtime.cpp"]
-CU_SRCS = ["interp.cu"]
-HEADERS = ["json.hpp", "ir.hpp", "devplan.hpp"]
+CU_SRCS = ["interp_launch.cu", "interp_k_copy.cu", "interp_k_sum.cu", "interp_k_prod.cu", "interp_k_max.cu", "interp_k_min.cu"]
+HEADERS = ["json.hpp", "ir.hpp", "devplan.hpp", "interp.cuh"]
 
 ORACLE_DIR = os.path.join(REPO, "oracle")
 ORACLE_LIB = os.path.join(ORACLE_DIR, "liboracle.so")
@@ -74,13 +76,13 @@ def build(force=False, verbose=False):
         objs.append(obj)
         if force or _newer(obj, [src] + hdrs):
             jobs.append(["g++", "-std=c++17", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
-                         "-Wno-unused-parameter", "-I" + os.path.join(CUDA, "include"), "-c", src, "-o", obj])
+                         "-Wno-unused-parameter", "-I" + os.path.join(CUDA, "include"), *NVCC_DEFS, "-c", src, "-o", obj])
     for s in CU_SRCS:
         src, obj = os.path.join(CSRC, s), os.path.join(BUILD, s + ".o")
         objs.append(obj)
         if force or _newer(obj, [src] + hdrs):
             jobs.append([NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
-                         "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr", "-c", src, "-o", obj])
+                         "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr", *NVCC_DEFS, "-c", src, "-o", obj])
     logs = []
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:

@@ -14,7 +14,10 @@
 namespace gc3 {
 
 constexpr int kMaxLocalRanks = 16;
-constexpr int kThreads = 512;  // CUDA threads per interpreter block
+#ifndef GC3_THREADS
+#define GC3_THREADS 512
+#endif
+constexpr int kThreads = GC3_THREADS;  // CUDA threads per interpreter block
 
 enum : uint8_t { kOpSend = 0, kOpRecv, kOpCopy, kOpReduce, kOpRrc, kOpRcs, kOpRrcs, kOpRrs, kOpNop };
 

@@ -17,12 +17,20 @@
 // Reductions are fused into the transfer (rrc / rrcs / rrs / reduce): no separate elementwise
 // kernel exists. Arithmetic is the oracle's (oracle/gc3_oracle.c gc3o_reduce): f16/bf16 go
 // through f32 and are rounded to nearest even, integers wrap, max/min select.
+#pragma once
 #include <cuda_runtime.h>
 
 #include <cstdint>
 #include <type_traits>
 
 #include "devplan.hpp"
+
+#ifndef GC3_UNROLL
+#define GC3_UNROLL 4
+#endif
+#ifndef GC3_MINBLOCKS
+#define GC3_MINBLOCKS 2
+#endif
 
 namespace gc3 {
 namespace dev {
@@ -192,7 +200,7 @@ struct RedNone {
 // takes the 128-bit path; the ragged remainder (and misaligned segments) go element-wise.
 template <class R, bool RED, bool TWO>
 __device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* o0, uint4* o1, int64_t nvec) {
-  constexpr int U = 4;
+  constexpr int U = GC3_UNROLL;
   int64_t i = threadIdx.x;
   for (; i + (U - 1) * kThreads < nvec; i += U * kThreads) {
     uint4 x[U], y[U];
@@ -278,7 +286,7 @@ struct Ctx {
   int64_t tile;
 };
 
-__device__ __noinline__ void raise_timeout(const Ctx c, int what) {
+static __device__ __noinline__ void raise_timeout(const Ctx c, int what) {
   if (atomicCAS(c.abort_flag, 0, 1) == 0 && c.err_info) {
     volatile uint64_t* e = c.err_info;
     e[1] = static_cast<uint64_t>(c.rank_slot);
@@ -364,7 +372,7 @@ __device__ bool ll_op(const DevOp op, char* src0, char* dst0, int64_t chunk_byte
 
 // ------------------------------------------------------------------ the interpreter
 template <class R, bool LL>
-__global__ void __launch_bounds__(kThreads, 2) interp(const LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
   const int lanes = a.lanes;
   const int lane = blockIdx.x % lanes;
   const int tbi = blockIdx.x / lanes;
@@ -477,53 +485,5 @@ __global__ void __launch_bounds__(kThreads, 2) interp(const LaunchArgs a) {
 }
 
 }  // namespace dev
-
-// ------------------------------------------------------------------ host-side dispatch
-using KernelFn = void (*)(LaunchArgs);
-
-template <class R>
-KernelFn pick(bool ll) {
-  return ll ? dev::interp<R, true> : dev::interp<R, false>;
-}
-
-template <int OP>
-KernelFn pick_type(int dtype, bool ll) {
-  switch (dtype) {
-    case 0: return pick<dev::RedInt<int8_t, OP>>(ll);
-    case 1: return pick<dev::RedInt<uint8_t, OP>>(ll);
-    case 2: return pick<dev::RedInt<int32_t, OP>>(ll);
-    case 3: return pick<dev::RedInt<uint32_t, OP>>(ll);
-    case 4: return pick<dev::RedInt<int64_t, OP>>(ll);
-    case 5: return pick<dev::RedInt<uint64_t, OP>>(ll);
-    case 6: return pick<dev::RedHalf<false, OP>>(ll);
-    case 7: return pick<dev::RedFloat<float, OP>>(ll);
-    case 8: return pick<dev::RedFloat<double, OP>>(ll);
-    case 9: return pick<dev::RedHalf<true, OP>>(ll);
-    default: return nullptr;
-  }
-}
-
-// dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs.
-KernelFn interp_kernel(int dtype, int redop, bool ll) {
-  switch (redop) {
-    case -1: return pick<dev::RedNone>(ll);
-    case 0: return pick_type<dev::kSum>(dtype, ll);
-    case 1: return pick_type<dev::kProd>(dtype, ll);
-    case 2: return pick_type<dev::kMax>(dtype, ll);
-    case 3: return pick_type<dev::kMin>(dtype, ll);
-    default: return nullptr;
-  }
-}
-
-cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, cudaStream_t stream) {
-  void* params[] = {const_cast<LaunchArgs*>(&args)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kThreads), params, 0, stream);
-}
-
-int interp_blocks_per_sm(KernelFn fn) {
-  int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), kThreads, 0) != cudaSuccess) return 0;
-  return n;
-}
 
 }  // namespace gc3

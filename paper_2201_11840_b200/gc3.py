@@ -9,7 +9,7 @@ import ctypes
 import os
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libgc3.so")
+LIB_PATH = os.environ.get("GC3_LIB_PATH", os.path.join(PKG, "libgc3.so"))
 
 # ncclDataType_t (nccl.h:278-290) keyed by torch dtype name
 NCCL_DTYPES = {
