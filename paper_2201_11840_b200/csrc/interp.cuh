@@ -371,6 +371,18 @@ __device__ bool ll_op(const DevOp op, char* src0, char* dst0, int64_t chunk_byte
 }
 
 // ------------------------------------------------------------------ the interpreter
+// Warp-asynchronous execution of one (IR thread block, lane): every warp walks the same
+// (tile, op) sequence and moves its share of each op's bytes; there is no block-wide barrier in
+// the op loop. Each warp waits for the op's preconditions itself (deps, FIFO credit, posted
+// message), fences its own stores, and arrives on a per-op shared-memory counter; the last warp
+// to arrive publishes the op (FIFO head / tail, semaphore). Warps may therefore overlap the loads
+// of op k+1 with the stores of op k. Thread->byte mapping is identical for every op, so a warp
+// always re-reads what it wrote itself (sequential semantics inside the thread block hold per
+// thread). A drift bound keeps warps within kDrift ops of the last published op.
+constexpr int kWarps = kThreads / 32;
+constexpr int kRing = 16;
+constexpr int kDrift = 6;
+
 template <class R, bool LL>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
   const int lanes = a.lanes;
@@ -384,6 +396,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int64_t slot_bytes = a.slot_bytes;
   const uint64_t slots = static_cast<uint64_t>(a.slots);
   const uint64_t epoch = a.epoch;
+  const int wid = threadIdx.x >> 5, wl = threadIdx.x & 31;
   // this block's rank buffers: select with constant indices (no dynamic param-space indexing)
   char *b_in = nullptr, *b_out = nullptr, *b_sc = nullptr;
 #pragma unroll
@@ -403,10 +416,19 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const DevOp* const ops = a.ops + tb.op_begin;
   const DevDep* const deps = a.deps;
   Ctx c{a.abort_flag, a.err_info, a.timeout_ns, tb.rank_slot, tbi, 0, 0};
-  __shared__ int s_abort;
-  if (threadIdx.x == 0) s_abort = 0;
+  __shared__ unsigned s_arrive[kRing];
+  __shared__ volatile int s_posted;  // ops published so far
+  __shared__ volatile int s_abort;
+  if (threadIdx.x < kRing) s_arrive[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    s_posted = 0;
+    s_abort = 0;
+  }
   __syncthreads();
 
+  const int my_tiles = ntiles > lane ? static_cast<int>((ntiles - 1 - lane) / lanes + 1) : 0;
+  const int total_ops = my_tiles * tb.nops;
+  int q = 0;  // op sequence number within this block
   int64_t iter = 0;
   for (int64_t tile = lane; tile < ntiles; tile += lanes, ++iter) {
     const int64_t t0 = tile * tile_elems;
@@ -414,27 +436,32 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
     const int64_t tbytes = tlen * R::kEsize;
     const int64_t t0_bytes = t0 * R::kEsize;
     c.tile = tile;
-    for (int s = 0; s < tb.nops; ++s) {
+    for (int s = 0; s < tb.nops; ++s, ++q) {
       const DevOp op = ops[s];
       const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
       c.step = s;
-      // (1) cross-thread-block dependencies and FIFO credits, waited in parallel
-      bool ok = true;
-      const int dep_thread = static_cast<int>(threadIdx.x) - 64;  // threads 64.. wait one dep each
-      if (dep_thread >= 0 && dep_thread < op.ndeps) {
-        const DevDep d = deps[op.dep_begin + dep_thread];
-        const uint64_t target = (epoch << 32) | static_cast<uint64_t>(iter * d.nops + d.step + 1);
-        ok = wait_geq(sems + d.sem + lane, target, false, c, 1);
-      } else if (threadIdx.x == 0 && send) {  // a free outgoing slot: sent - tail < slots
-        ok = wait_geq(cout.tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
-      } else if (threadIdx.x == 32 && recv && !LL) {  // a posted incoming message
-        ok = wait_geq(cin.head, rcvd + 1, sys, c, 3);
+      // drift bound (also keeps the arrival ring from wrapping onto an unpublished op)
+      if (q - s_posted > kDrift) {
+        while (q - s_posted > kDrift) {
+          if (s_abort || *reinterpret_cast<volatile int*>(c.abort_flag)) return;
+        }
       }
-      if (!ok) s_abort = 1;
-      __syncthreads();
-      if (s_abort) return;
+      // (1) preconditions, per warp: deps, a free outgoing slot, a posted message
+      bool ok = true;
+      for (int d = wl; d < op.ndeps; d += 32) {
+        const DevDep dd = deps[op.dep_begin + d];
+        const uint64_t target = (epoch << 32) | static_cast<uint64_t>(iter * dd.nops + dd.step + 1);
+        ok = ok && wait_geq(sems + dd.sem + lane, target, false, c, 1);
+      }
+      if (wl == 0 && send) ok = wait_geq(cout.tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
+      if (wl == 1 && recv && !LL) ok = wait_geq(cin.head, rcvd + 1, sys, c, 3);
+      if (!__all_sync(0xffffffffu, ok)) {
+        s_abort = 1;
+        return;
+      }
+      __syncwarp();  // orders the other lanes' data accesses after lanes 0/1's acquires
 
-      // (2) the transfer, with the reduction fused in
+      // (2) this warp's share of the transfer, with the reduction fused in
       char* src = pick_buf(op.src_buf, b_in, b_out, b_sc) + op.src_off * chunk_bytes + t0_bytes;
       char* dst = pick_buf(op.dst_buf, b_in, b_out, b_sc) + op.dst_off * chunk_bytes + t0_bytes;
       const int64_t slot_in = static_cast<int64_t>(rcvd % slots) * slot_bytes;
@@ -442,8 +469,11 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       if (LL && (recv || send)) {
         const uint4* inl = recv ? reinterpret_cast<const uint4*>(cin.fifo + slot_in) : nullptr;
         uint4* outl = send ? reinterpret_cast<uint4*>(cout.fifo + slot_out) : nullptr;
-        if (!ll_op<R>(op, src, dst, chunk_bytes, tbytes, inl, outl, static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), c))
+        ok = ll_op<R>(op, src, dst, chunk_bytes, tbytes, inl, outl, static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), c);
+        if (!__all_sync(0xffffffffu, ok)) {
           s_abort = 1;
+          return;
+        }
       } else {
         const char* in = recv ? cin.fifo + slot_in : nullptr;
         char* out = send ? cout.fifo + slot_out : nullptr;
@@ -465,22 +495,32 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
           }
         }
       }
-      __syncthreads();
-      if (s_abort) return;
 
-      // (3) publish: slot posted / slot freed / semaphore
-      if (threadIdx.x == 0) {
-        if (send && !LL) st_release(cout.head, sent + 1, sys);
-        if (recv) st_release(cin.tail, rcvd + 1, sys);
-        if (op.has_dep) st_release(my_sem, (epoch << 32) | static_cast<uint64_t>(iter * tb.nops + s + 1), false);
+      // (3) arrive; the last warp publishes: slot posted / slot freed / semaphore
+      const bool publishes = (send && !LL) || recv || op.has_dep;
+      if (publishes) {
+        if (sys) __threadfence_system();
+        else __threadfence();
+      }
+      __syncwarp();
+      if (wl == 0) {
+        const unsigned prev = atomicAdd(&s_arrive[q % kRing], 1u);
+        if (prev == kWarps - 1) {
+          s_arrive[q % kRing] = 0;
+          if (send && !LL) st_release(cout.head, sent + 1, sys);
+          if (recv) st_release(cin.tail, rcvd + 1, sys);
+          if (op.has_dep) st_release(my_sem, (epoch << 32) | static_cast<uint64_t>(iter * tb.nops + s + 1), false);
+          if (q + 1 == total_ops) {  // persistent FIFO counters for the next launch
+            if (has_in) *cin.mine = rcvd + (recv ? 1 : 0);
+            if (has_out) *cout.mine = sent + (send ? 1 : 0);
+          }
+          __threadfence_block();
+          s_posted = q + 1;
+        }
       }
       if (send) ++sent;
       if (recv) ++rcvd;
     }
-  }
-  if (threadIdx.x == 0) {
-    if (has_in) *cin.mine = rcvd;
-    if (has_out) *cout.mine = sent;
   }
 }
 
