@@ -136,6 +136,13 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
  * afterwards), "lanes", "tile_bytes", "timeout_ms" (apply to the next launch; 0 = automatic). */
 ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value);
 
+/* In-kernel event log of the last launch on comm's device when config "trace" (GC3_TRACE) is set
+ * (SURVEY.md §5 tracing): for CUDA block b and its q-th op, out[(b*ops_per_block + q)*4 + k] holds
+ * %globaltimer ns at k = 0 start, 1 preconditions met, 2 warp 0's data done, 3 published (0 if not
+ * reached). Block b executes IR thread block b / lanes (ranks of the device in rank order, thread
+ * blocks in IR order), lane b % lanes. With out == NULL only the shape is returned. Synchronizes. */
+ncclResult_t gc3GetTrace(ncclComm_t comm, uint64_t* out, size_t max_words, int* grid, int* ops_per_block, int* lanes);
+
 /* ---- IR library, host only (no CUDA needed) ---------------------------------------------- */
 typedef struct gc3Ir* gc3Ir_t;
 /* ir.hpp:226-310. On a schema error returns ncclInvalidArgument and, if err is non-NULL, sets

@@ -426,6 +426,12 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   }
   __syncthreads();
 
+  // event log (gc3SetConfig "trace"): per op {start, preconditions met, warp 0 data done, published}
+  uint64_t* const trace = a.trace;
+  const int trace_ops = a.trace_ops;
+  auto stamp = [&](int qq, int k) {
+    if (trace && qq < trace_ops) trace[(static_cast<int64_t>(blockIdx.x) * trace_ops + qq) * 4 + k] = globaltimer();
+  };
   const int my_tiles = ntiles > lane ? static_cast<int>((ntiles - 1 - lane) / lanes + 1) : 0;
   const int total_ops = my_tiles * tb.nops;
   int q = 0;  // op sequence number within this block
@@ -447,6 +453,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         }
       }
       // (1) preconditions, per warp: deps, a free outgoing slot, a posted message
+      if (threadIdx.x == 0) stamp(q, 0);
       bool ok = true;
       for (int d = wl; d < op.ndeps; d += 32) {
         const DevDep dd = deps[op.dep_begin + d];
@@ -460,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         return;
       }
       __syncwarp();  // orders the other lanes' data accesses after lanes 0/1's acquires
+      if (threadIdx.x == 0) stamp(q, 1);
 
       // (2) this warp's share of the transfer, with the reduction fused in
       char* src = pick_buf(op.src_buf, b_in, b_out, b_sc) + op.src_off * chunk_bytes + t0_bytes;
@@ -498,6 +506,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
 
       // (3) arrive; the last warp publishes: slot posted / slot freed / semaphore
       const bool publishes = (send && !LL) || recv || op.has_dep;
+      if (threadIdx.x == 0) stamp(q, 2);
       if (publishes) {
         if (sys) __threadfence_system();
         else __threadfence();
@@ -514,6 +523,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
             if (has_in) *cin.mine = rcvd + (recv ? 1 : 0);
             if (has_out) *cout.mine = sent + (send ? 1 : 0);
           }
+          stamp(q, 3);
           __threadfence_block();
           s_posted = q + 1;
         }

@@ -89,6 +89,7 @@ struct Config {
   int lanes = 0;                     // 0: automatic
   int64_t tile_bytes = 0;            // 0: automatic
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
+  int trace = 0;                     // record the in-kernel %globaltimer event log
 };
 
 Config config_from_env() {
@@ -99,6 +100,7 @@ Config config_from_env() {
   c.lanes = static_cast<int>(env_int("GC3_LANES", c.lanes));
   c.tile_bytes = env_int("GC3_TILE_BYTES", c.tile_bytes);
   c.timeout_ms = env_int("GC3_TIMEOUT_MS", c.timeout_ms);
+  c.trace = static_cast<int>(env_int("GC3_TRACE", 0));
   return c;
 }
 
@@ -229,6 +231,9 @@ struct DeviceState {
   std::vector<DevicePlan> plans;  // by ir id
   int num_sms = 0;
   std::map<KernelFn, int> occupancy;
+  uint64_t* d_trace = nullptr;  // event log of the last traced launch
+  size_t trace_bytes = 0;
+  int trace_grid = 0, trace_ops = 0, trace_lanes = 0;
 };
 
 struct Clique {
@@ -705,6 +710,27 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.timeout_ns = static_cast<uint64_t>(c0->cfg.timeout_ms) * 1000000ull;
   a.abort_flag = ds->d_abort;
   a.err_info = ds->d_err;
+  if (c0->cfg.trace) {
+    int max_nops = 0;
+    for (int r : plan.ranks)
+      for (const auto& tb : c0->irs[id]->prog.gpus[r].tbs) max_nops = std::max(max_nops, static_cast<int>(tb.ops.size()));
+    const int ops_per_block = static_cast<int>(std::min<int64_t>((cp.ntiles + cp.lanes - 1) / cp.lanes * max_nops, 1 << 20));
+    const size_t need = static_cast<size_t>(cp.grid) * ops_per_block * 4 * sizeof(uint64_t);
+    DeviceGuard gt(dev);
+    if (need > ds->trace_bytes) {
+      if (ds->d_trace) cudaFree(ds->d_trace);
+      ds->d_trace = nullptr;
+      ds->trace_bytes = 0;
+      CUDA_TRY(cudaMalloc(&ds->d_trace, need));
+      ds->trace_bytes = need;
+    }
+    CUDA_TRY(cudaMemsetAsync(ds->d_trace, 0, need, p0.stream));
+    a.trace = ds->d_trace;
+    a.trace_ops = ops_per_block;
+    ds->trace_grid = cp.grid;
+    ds->trace_ops = ops_per_block;
+    ds->trace_lanes = cp.lanes;
+  }
   // LaunchArgs::sems are indexed with the lane count used when the plan was built (ir.lanes); the
   // kernel adds its lane (< cp.lanes <= ir.lanes) to each tb's base.
   cudaStream_t stream = p0.stream;
@@ -955,6 +981,7 @@ static void release_comm(Comm* c) {
         cudaFree(p.d_sems);
       }
       cudaFree(ds.d_abort);
+      if (ds.d_trace) cudaFree(ds.d_trace);
       cudaFreeHost(ds.h_err);
     }
     g_cliques.erase(cl->key);
@@ -1123,7 +1150,26 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "lanes") c.lanes = static_cast<int>(value);
   else if (k == "tile_bytes") c.tile_bytes = value;
   else if (k == "timeout_ms") c.timeout_ms = value;
+  else if (k == "trace") c.trace = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
+  return ncclSuccess;
+}
+
+ncclResult_t gc3GetTrace(ncclComm_t comm, uint64_t* out, size_t max_words, int* grid, int* ops_per_block, int* lanes) {
+  if (!comm || !grid || !ops_per_block || !lanes) return ncclInvalidArgument;
+  std::lock_guard<std::recursive_mutex> lk(g_mu);
+  auto it = comm->clique->devs.find(comm->device);
+  if (it == comm->clique->devs.end() || !it->second.d_trace) return set_error(ncclInvalidUsage, "no traced launch on this device");
+  DeviceState& ds = it->second;
+  *grid = ds.trace_grid;
+  *ops_per_block = ds.trace_ops;
+  *lanes = ds.trace_lanes;
+  const size_t words = static_cast<size_t>(ds.trace_grid) * ds.trace_ops * 4;
+  if (out) {
+    DeviceGuard g(comm->device);
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(out, ds.d_trace, std::min(words, max_words) * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  }
   return ncclSuccess;
 }
 

@@ -83,6 +83,7 @@ def lib():
         "gc3SetProtocolOverride": [vp, i, i],
         "gc3QueryPlan": [vp, i, sz, i, ctypes.POINTER(PlanInfo)],
         "gc3SetConfig": [vp, cp, ctypes.c_int64],
+        "gc3GetTrace": [vp, ctypes.c_void_p, sz, ctypes.POINTER(i), ctypes.POINTER(i), ctypes.POINTER(i)],
         "gc3IrParse": [cp, ctypes.POINTER(vp), ctypes.POINTER(vp)],
         "gc3IrSerialize": [vp, ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
@@ -207,6 +208,15 @@ class Comm:
         info = PlanInfo()
         check(lib().gc3QueryPlan(self.h, COLLS[coll], count, NCCL_DTYPES[dtype], ctypes.byref(info)), self.h)
         return info.as_dict()
+
+    def trace(self):
+        """Event log of the last traced launch: (numpy [grid, ops, 4] uint64 ns, lanes)."""
+        import numpy as np
+        g, o, ln = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(lib().gc3GetTrace(self.h, None, 0, ctypes.byref(g), ctypes.byref(o), ctypes.byref(ln)), self.h)
+        buf = np.zeros(g.value * o.value * 4, dtype=np.uint64)
+        check(lib().gc3GetTrace(self.h, buf.ctypes.data, buf.size, ctypes.byref(g), ctypes.byref(o), ctypes.byref(ln)), self.h)
+        return buf.reshape(g.value, o.value, 4), ln.value
 
     def async_error(self):
         e = ctypes.c_int()
