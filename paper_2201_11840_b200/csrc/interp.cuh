@@ -42,6 +42,16 @@ __device__ __forceinline__ uint64_t ld_acquire(const uint64_t* p, bool sys) {
   else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t* p, bool sys) {
+  uint64_t v;
+  if (sys) asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  else asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel(bool sys) {
+  if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
+  else asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
 __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool sys) {
   if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -299,12 +309,19 @@ static __device__ __noinline__ void raise_timeout(const Ctx c, int what) {
   }
 }
 
-// Spins until *p >= target; false if the launch was aborted.
+// Spins until *p >= target; false if the launch was aborted. Polls with relaxed loads (an acquire
+// load would invalidate L1 on every iteration) and acquires once with a fence when satisfied.
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys, const Ctx& c, int what) {
-  if (ld_acquire(p, sys) >= target) return true;
+  if (ld_relaxed(p, sys) >= target) {
+    fence_acq_rel(sys);
+    return true;
+  }
   const uint64_t start = globaltimer();
   for (int n = 0;; ++n) {
-    if (ld_acquire(p, sys) >= target) return true;
+    if (ld_relaxed(p, sys) >= target) {
+      fence_acq_rel(sys);
+      return true;
+    }
     if ((n & 255) == 255) {
       if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
       if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
@@ -507,15 +524,15 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       // (3) arrive; the last warp publishes: slot posted / slot freed / semaphore
       const bool publishes = (send && !LL) || recv || op.has_dep;
       if (threadIdx.x == 0) stamp(q, 2);
-      if (publishes) {
-        if (sys) __threadfence_system();
-        else __threadfence();
-      }
+      // every warp releases its stores at CTA scope; the publisher's gpu/sys-scope release is
+      // cumulative over what it acquired through the arrival counter (PTX causality order)
       __syncwarp();
       if (wl == 0) {
-        const unsigned prev = atomicAdd(&s_arrive[q % kRing], 1u);
+        unsigned prev;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;" : "=r"(prev) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(&s_arrive[q % kRing]))) : "memory");
         if (prev == kWarps - 1) {
           s_arrive[q % kRing] = 0;
+          if (publishes) fence_acq_rel(sys);
           if (send && !LL) st_release(cout.head, sent + 1, sys);
           if (recv) st_release(cin.tail, rcvd + 1, sys);
           if (op.has_dep) st_release(my_sem, (epoch << 32) | static_cast<uint64_t>(iter * tb.nops + s + 1), false);
