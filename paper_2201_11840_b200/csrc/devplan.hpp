@@ -54,10 +54,11 @@ struct DevTb {
 // One side of one connection for one lane.  The FIFO and `head` live in the receiver's memory,
 // `tail` in the sender's memory (NVLink buffers on the receiving GPU).
 struct DevChan {
-  char* fifo;        // slots x slot_bytes
-  uint64_t* head;    // messages posted (written by the sender)
-  uint64_t* tail;    // messages consumed (written by the receiver)
-  uint64_t* mine;    // this side's persistent message counter
+  char* fifo;          // slots x slot_bytes
+  uint64_t* head;      // messages posted (written by the sender)
+  uint64_t* tail;      // messages consumed (written by the receiver)
+  uint64_t* mine;      // this side's persistent message counter
+  int64_t slot_bytes;  // bytes of one slot: tile unit x the connection's largest count
 };
 
 struct LaunchArgs {
@@ -70,7 +71,6 @@ struct LaunchArgs {
   int32_t lanes;
   int32_t slots;
   int32_t sys_scope;    // 1: peers on other GPUs (NVLink, .sys fences); 0: same-device loopback
-  int64_t slot_bytes;
   int64_t chunk_elems;  // elements per chunk
   int64_t tile_elems;   // elements per tile
   int64_t ntiles;

@@ -28,6 +28,9 @@
 #ifndef GC3_UNROLL
 #define GC3_UNROLL 4
 #endif
+#ifndef GC3_UNROLL_COPY
+#define GC3_UNROLL_COPY 8
+#endif
 #ifndef GC3_MINBLOCKS
 #define GC3_MINBLOCKS 2
 #endif
@@ -210,7 +213,7 @@ struct RedNone {
 // takes the 128-bit path; the ragged remainder (and misaligned segments) go element-wise.
 template <class R, bool RED, bool TWO>
 __device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* o0, uint4* o1, int64_t nvec) {
-  constexpr int U = GC3_UNROLL;
+  constexpr int U = R::kReduce ? GC3_UNROLL : GC3_UNROLL_COPY;  // 128-bit loads in flight per thread
   int64_t i = threadIdx.x;
   for (; i + (U - 1) * kThreads < nvec; i += U * kThreads) {
     uint4 x[U], y[U];
@@ -410,7 +413,6 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const bool has_in = tb.chan_in >= 0, has_out = tb.chan_out >= 0;
   const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
   const int64_t chunk_bytes = chunk_elems * R::kEsize;
-  const int64_t slot_bytes = a.slot_bytes;
   const uint64_t slots = static_cast<uint64_t>(a.slots);
   const uint64_t epoch = a.epoch;
   const int wid = threadIdx.x >> 5, wl = threadIdx.x & 31;
@@ -489,8 +491,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       // (2) this warp's share of the transfer, with the reduction fused in
       char* src = pick_buf(op.src_buf, b_in, b_out, b_sc) + op.src_off * chunk_bytes + t0_bytes;
       char* dst = pick_buf(op.dst_buf, b_in, b_out, b_sc) + op.dst_off * chunk_bytes + t0_bytes;
-      const int64_t slot_in = static_cast<int64_t>(rcvd % slots) * slot_bytes;
-      const int64_t slot_out = static_cast<int64_t>(sent % slots) * slot_bytes;
+      const int64_t slot_in = static_cast<int64_t>(rcvd % slots) * cin.slot_bytes;
+      const int64_t slot_out = static_cast<int64_t>(sent % slots) * cout.slot_bytes;
       if (LL && (recv || send)) {
         const uint4* inl = recv ? reinterpret_cast<const uint4*>(cin.fifo + slot_in) : nullptr;
         uint4* outl = send ? reinterpret_cast<uint4*>(cout.fifo + slot_out) : nullptr;

@@ -84,8 +84,8 @@ int64_t env_int(const char* name, int64_t def) {
 // ------------------------------------------------------------------------------- config
 struct Config {
   int slots = 2;                     // FIFO slots per connection; fused ops need >= 2 (SURVEY Finding 1)
-  int64_t slot_bytes = 256 << 10;    // bytes per FIFO slot (the paper's b / s)
-  int max_lanes = 16;                // lanes provisioned per connection in the arenas
+  int64_t slot_bytes = 256 << 10;    // FIFO slot unit: max bytes of one tile (a slot holds count tiles)
+  int max_lanes = 64;                // cap on lanes provisioned per connection in the arenas
   int lanes = 0;                     // 0: automatic
   int64_t tile_bytes = 0;            // 0: automatic
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
@@ -166,22 +166,32 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
   std::vector<int> in_index, out_index;  // per tb: index among receiving / sending tbs, or -1
+  std::vector<size_t> fifo_off;          // per receiving tb: offset of its FIFOs (lanes x slots)
+  std::vector<int64_t> slot_stride;      // per receiving tb: bytes of one slot = unit x max count
   int n_in = 0, n_out = 0;
-  size_t off_fifo = 0, off_head = 0, off_tail = 0, off_mine_in = 0, off_mine_out = 0, bytes = 0;
+  size_t off_head = 0, off_tail = 0, off_mine_in = 0, off_mine_out = 0, bytes = 0;
 };
 
-ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_t slot_bytes) {
+// FIFO slots are sized per connection: one slot holds a message of `count` tiles, each at most
+// `unit` bytes, so the tile size does not shrink with the aggregation count.
+ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_t unit) {
   ArenaLayout a;
   const Gpu& g = p.gpus[rank];
   a.in_index.assign(g.tbs.size(), -1);
   a.out_index.assign(g.tbs.size(), -1);
+  size_t off = 0;
   for (size_t t = 0; t < g.tbs.size(); ++t) {
-    if (g.tbs[t].recv_peer >= 0) a.in_index[t] = a.n_in++;
+    if (g.tbs[t].recv_peer >= 0) {
+      a.in_index[t] = a.n_in++;
+      int maxc = 1;
+      for (const Op& op : g.tbs[t].ops)
+        if (op_receives(op.op)) maxc = std::max(maxc, op.count);
+      a.fifo_off.push_back(off);
+      a.slot_stride.push_back(unit * maxc);
+      off += static_cast<size_t>(lanes) * slots * unit * maxc;
+    }
     if (g.tbs[t].send_peer >= 0) a.out_index[t] = a.n_out++;
   }
-  size_t off = 0;
-  a.off_fifo = off;
-  off += static_cast<size_t>(a.n_in) * lanes * slots * slot_bytes;
   off = align_up(off, 256);
   a.off_head = off;
   off += static_cast<size_t>(a.n_in) * lanes * kCounterStride;
@@ -475,7 +485,8 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         d.chan_in = static_cast<int>(chans.size());
         for (int l = 0; l < L; ++l) {
           DevChan ch{};
-          ch.fifo = ir.arena + ir.lay.off_fifo + (static_cast<size_t>(k) * L + l) * ir.slots * ir.slot_bytes;
+          ch.fifo = ir.arena + ir.lay.fifo_off[k] + static_cast<size_t>(l) * ir.slots * ir.lay.slot_stride[k];
+          ch.slot_bytes = ir.lay.slot_stride[k];
           ch.head = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_head + (static_cast<size_t>(k) * L + l) * kCounterStride);
           ch.tail = reinterpret_cast<uint64_t*>(sender_arena + slay.off_tail + (static_cast<size_t>(m) * L + l) * kCounterStride);
           ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_in + (static_cast<size_t>(k) * L + l) * 8);
@@ -495,7 +506,8 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         d.chan_out = static_cast<int>(chans.size());
         for (int l = 0; l < L; ++l) {
           DevChan ch{};
-          ch.fifo = recv_arena + rlay.off_fifo + (static_cast<size_t>(k) * L + l) * ir.slots * ir.slot_bytes;
+          ch.fifo = recv_arena + rlay.fifo_off[k] + static_cast<size_t>(l) * ir.slots * rlay.slot_stride[k];
+          ch.slot_bytes = rlay.slot_stride[k];
           ch.head = reinterpret_cast<uint64_t*>(recv_arena + rlay.off_head + (static_cast<size_t>(k) * L + l) * kCounterStride);
           ch.tail = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_tail + (static_cast<size_t>(m) * L + l) * kCounterStride);
           ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_out + (static_cast<size_t>(m) * L + l) * 8);
@@ -623,9 +635,9 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.chunk_elems = chunk_bytes / cp.kesize;
   const int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
   cp.ll = proto == 1 && chunk_bytes % 8 == 0;
-  const int64_t cap_bytes = (cp.ll ? ir.slot_bytes / 2 : ir.slot_bytes) / std::max(1, ir.max_count);
+  const int64_t cap_bytes = cp.ll ? ir.slot_bytes / 2 : ir.slot_bytes;  // per tile (slots scale with count)
   int64_t tile_bytes_cap = cap_bytes / 16 * 16;
-  if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot too small for count %d", ir.max_count);
+  if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot unit too small");
   cp.fn = interp_kernel(cp.redop < 0 ? 0 : dtype, cp.redop, cp.ll);
   if (!cp.fn) return set_error(ncclInvalidArgument, "no kernel for dtype %d op %d", dtype, redop);
   auto it = ds.occupancy.find(cp.fn);
@@ -702,7 +714,6 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.lanes = cp.lanes;
   a.slots = ir0.slots;
   a.sys_scope = plan.sys_scope ? 1 : 0;
-  a.slot_bytes = ir0.slot_bytes;
   a.chunk_elems = cp.chunk_elems;
   a.tile_elems = cp.tile_elems;
   a.ntiles = cp.ntiles;
@@ -1110,7 +1121,13 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
       }
   ir->slots = std::max(1, comm->cfg.slots);
   ir->slot_bytes = std::max<int64_t>(comm->cfg.slot_bytes / 256 * 256, 256);
-  ir->lanes = std::max(1, comm->cfg.max_lanes);
+  {  // lanes provisioned: enough for ~2 CUDA blocks per SM when one rank owns a device
+    int max_tbs = 1;
+    for (const auto& g : ir->prog.gpus) max_tbs = std::max(max_tbs, static_cast<int>(g.tbs.size()));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
+    ir->lanes = std::max(1, std::min(comm->cfg.max_lanes, (2 * sms + max_tbs - 1) / max_tbs));
+  }
   ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes);
   {
     DeviceGuard g(comm->device);
