@@ -20,6 +20,7 @@ constexpr int kMaxLocalRanks = 16;
 constexpr int kThreads = GC3_THREADS;  // CUDA threads per interpreter block
 
 enum : uint8_t { kOpSend = 0, kOpRecv, kOpCopy, kOpReduce, kOpRrc, kOpRcs, kOpRrcs, kOpRrs, kOpNop };
+enum : uint8_t { kInDirect = 1, kOutDirect = 2 };
 
 struct DevOp {  // 24 bytes
   uint8_t opcode;
@@ -27,7 +28,9 @@ struct DevOp {  // 24 bytes
   uint8_t dst_buf;
   uint8_t has_dep;
   int16_t ndeps;
-  int16_t pad;
+  uint8_t direct;  // bit 0: the incoming message is already in place (in_direct);
+                   // bit 1: write the outgoing message into the receiver's buffer (out_direct)
+  uint8_t pad;
   int32_t src_off;
   int32_t dst_off;
   int32_t count;
@@ -48,7 +51,8 @@ struct DevTb {
   int32_t sem;        // semaphore base index (x lanes)
   int32_t chan_in;    // receive-side channel base index (x lanes), -1 if none
   int32_t chan_out;   // send-side channel base index (x lanes), -1 if none
-  int32_t pad[2];
+  int32_t peer_slot;  // rank slot of the send peer when it runs in the same launch, else -1
+  int32_t pad;
 };
 
 // One side of one connection for one lane.  The FIFO and `head` live in the receiver's memory,

@@ -345,19 +345,21 @@ __device__ __forceinline__ char* pick_buf(int b, char* in, char* out, char* sc) 
 // ------------------------------------------------------------------ LL op body
 // Lines of the incoming/outgoing message are distributed over threads; every thread polls the
 // flags of its own lines only.
+// inl == nullptr: the incoming message is in place (direct) or absent; outl == nullptr: the
+// outgoing message goes to outd (direct, plain stores) or is absent.
 template <class R>
 __device__ bool ll_op(const DevOp op, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl, uint4* outl,
-                      uint32_t in_flag, uint32_t out_flag, const Ctx& c) {
+                      char* outd, uint32_t in_flag, uint32_t out_flag, const Ctx& c) {
   const int64_t lines_per_seg = tbytes >> 3;
   const int64_t nlines = lines_per_seg * op.count;
-  const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
+  const bool send = is_send(op.opcode);
   for (int64_t k = threadIdx.x; k < nlines; k += kThreads) {
     const int j = static_cast<int>(k / lines_per_seg);
     const int64_t off = ((k - j * lines_per_seg) << 3) + j * chunk_bytes;
     char* src = src0 + off;
     char* dst = dst0 + off;
     uint2 msg = make_uint2(0, 0);
-    if (recv) {
+    if (inl) {
       uint4 l = ld_volatile_line(inl + k);
       if (l.y != in_flag || l.w != in_flag) {
         const uint64_t start = globaltimer();
@@ -378,14 +380,26 @@ __device__ bool ll_op(const DevOp op, char* src0, char* dst0, int64_t chunk_byte
     uint2 v;
     switch (op.opcode) {
       case kOpSend: v = ld_cg8(src); break;
-      case kOpRecv: st_vec8(dst, msg); continue;
+      case kOpRecv:
+        if (inl) st_vec8(dst, msg);
+        continue;
       case kOpRrc: st_vec8(dst, R::template vec<uint2>(ld_cg8(src), msg)); continue;
-      case kOpRcs: v = msg; st_vec8(src, v); break;
+      case kOpRcs:
+        if (inl) {
+          v = msg;
+          st_vec8(src, v);
+        } else {
+          v = ld_cg8(src);  // direct: the message is already in the local span
+        }
+        break;
       case kOpRrcs: v = R::template vec<uint2>(ld_cg8(src), msg); st_vec8(src, v); break;
       case kOpRrs: v = R::template vec<uint2>(ld_cg8(src), msg); break;
       default: continue;
     }
-    if (send) st_volatile_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag));
+    if (send) {
+      if (outl) st_volatile_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag));
+      else st_vec8(outd + off, v);
+    }
   }
   return true;
 }
@@ -418,13 +432,20 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int wid = threadIdx.x >> 5, wl = threadIdx.x & 31;
   // this block's rank buffers: select with constant indices (no dynamic param-space indexing)
   char *b_in = nullptr, *b_out = nullptr, *b_sc = nullptr;
+  char *p_in = nullptr, *p_out = nullptr, *p_sc = nullptr;  // send peer's buffers (direct writes)
 #pragma unroll
-  for (int i = 0; i < kMaxLocalRanks; ++i)
+  for (int i = 0; i < kMaxLocalRanks; ++i) {
     if (i == tb.rank_slot) {
       b_in = a.bufs[i][0];
       b_out = a.bufs[i][1];
       b_sc = a.bufs[i][2];
     }
+    if (i == tb.peer_slot) {
+      p_in = a.bufs[i][0];
+      p_out = a.bufs[i][1];
+      p_sc = a.bufs[i][2];
+    }
+  }
   DevChan cin{}, cout{};
   if (has_in) cin = a.chans[tb.chan_in + lane];
   if (has_out) cout = a.chans[tb.chan_out + lane];
@@ -479,8 +500,10 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         const uint64_t target = (epoch << 32) | static_cast<uint64_t>(iter * dd.nops + dd.step + 1);
         ok = ok && wait_geq(sems + dd.sem + lane, target, false, c, 1);
       }
-      if (wl == 0 && send) ok = wait_geq(cout.tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
-      if (wl == 1 && recv && !LL) ok = wait_geq(cin.head, rcvd + 1, sys, c, 3);
+      const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
+      const bool ll_in = LL && recv && !in_d, ll_out = LL && send && !out_d;  // LL lines carry the payload
+      if (wl == 0 && send && !out_d) ok = wait_geq(cout.tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
+      if (wl == 1 && recv && !ll_in) ok = wait_geq(cin.head, rcvd + 1, sys, c, 3);
       if (!__all_sync(0xffffffffu, ok)) {
         s_abort = 1;
         return;
@@ -493,29 +516,38 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       char* dst = pick_buf(op.dst_buf, b_in, b_out, b_sc) + op.dst_off * chunk_bytes + t0_bytes;
       const int64_t slot_in = static_cast<int64_t>(rcvd % slots) * cin.slot_bytes;
       const int64_t slot_out = static_cast<int64_t>(sent % slots) * cout.slot_bytes;
-      if (LL && (recv || send)) {
-        const uint4* inl = recv ? reinterpret_cast<const uint4*>(cin.fifo + slot_in) : nullptr;
-        uint4* outl = send ? reinterpret_cast<uint4*>(cout.fifo + slot_out) : nullptr;
-        ok = ll_op<R>(op, src, dst, chunk_bytes, tbytes, inl, outl, static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), c);
+      // a direct outgoing message lands in the receiver's own span (the send op's dst fields name it,
+      // lowering.hpp:71); a direct incoming one is already in this rank's write span
+      char* peer_dst = out_d ? pick_buf(op.dst_buf, p_in, p_out, p_sc) + op.dst_off * chunk_bytes + t0_bytes : nullptr;
+      if (ll_in || ll_out) {
+        const uint4* inl = ll_in ? reinterpret_cast<const uint4*>(cin.fifo + slot_in) : nullptr;
+        uint4* outl = ll_out ? reinterpret_cast<uint4*>(cout.fifo + slot_out) : nullptr;
+        ok = ll_op<R>(op, src, dst, chunk_bytes, tbytes, inl, outl, peer_dst, static_cast<uint32_t>(rcvd + 1),
+                      static_cast<uint32_t>(sent + 1), c);
         if (!__all_sync(0xffffffffu, ok)) {
           s_abort = 1;
           return;
         }
       } else {
-        const char* in = recv ? cin.fifo + slot_in : nullptr;
-        char* out = send ? cout.fifo + slot_out : nullptr;
+        const char* in = recv && !in_d ? cin.fifo + slot_in : nullptr;
+        char* out = send && !out_d ? cout.fifo + slot_out : nullptr;
         for (int j = 0; j < op.count; ++j) {
           char* sj = src + j * chunk_bytes;
           char* dj = dst + j * chunk_bytes;
           const char* mi = in ? in + j * tbytes : nullptr;
-          char* mo = out ? out + j * tbytes : nullptr;
+          char* mo = out_d ? peer_dst + j * chunk_bytes : (out ? out + j * tbytes : nullptr);
           switch (op.opcode) {
             case kOpSend: move<R>(sj, nullptr, mo, nullptr, tbytes); break;
-            case kOpRecv: move<R>(mi, nullptr, dj, nullptr, tbytes); break;
+            case kOpRecv:
+              if (!in_d) move<R>(mi, nullptr, dj, nullptr, tbytes);
+              break;
             case kOpCopy: move<R>(sj, nullptr, dj, nullptr, tbytes); break;
             case kOpReduce: move<R>(dj, sj, dj, nullptr, tbytes); break;
             case kOpRrc: move<R>(sj, mi, dj, nullptr, tbytes); break;
-            case kOpRcs: move<R>(mi, nullptr, sj, mo, tbytes); break;
+            case kOpRcs:
+              if (in_d) move<R>(sj, nullptr, mo, nullptr, tbytes);
+              else move<R>(mi, nullptr, sj, mo, tbytes);
+              break;
             case kOpRrcs: move<R>(sj, mi, sj, mo, tbytes); break;
             case kOpRrs: move<R>(sj, mi, nullptr, mo, tbytes); break;
             default: break;
@@ -524,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       }
 
       // (3) arrive; the last warp publishes: slot posted / slot freed / semaphore
-      const bool publishes = (send && !LL) || recv || op.has_dep;
+      const bool publishes = (send && !ll_out) || recv || op.has_dep;
       if (threadIdx.x == 0) stamp(q, 2);
       // every warp releases its stores at CTA scope; the publisher's gpu/sys-scope release is
       // cumulative over what it acquired through the arrival counter (PTX causality order)
@@ -535,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         if (prev == kWarps - 1) {
           s_arrive[q % kRing] = 0;
           if (publishes) fence_acq_rel(sys);
-          if (send && !LL) st_release(cout.head, sent + 1, sys);
+          if (send && !ll_out) st_release(cout.head, sent + 1, sys);
           if (recv) st_release(cin.tail, rcvd + 1, sys);
           if (op.has_dep) st_release(my_sem, (epoch << 32) | static_cast<uint64_t>(iter * tb.nops + s + 1), false);
           if (q + 1 == total_ops) {  // persistent FIFO counters for the next launch

@@ -90,6 +90,7 @@ struct Config {
   int64_t tile_bytes = 0;            // 0: automatic
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
   int trace = 0;                     // record the in-kernel %globaltimer event log
+  int direct = 1;                    // write dead receive spans directly (see direct_messages)
 };
 
 Config config_from_env() {
@@ -101,6 +102,7 @@ Config config_from_env() {
   c.tile_bytes = env_int("GC3_TILE_BYTES", c.tile_bytes);
   c.timeout_ms = env_int("GC3_TIMEOUT_MS", c.timeout_ms);
   c.trace = static_cast<int>(env_int("GC3_TRACE", 0));
+  c.direct = static_cast<int>(env_int("GC3_DIRECT", 1));
   return c;
 }
 
@@ -408,6 +410,120 @@ ncclResult_t peer_arena(Comm* c, int id, int r, char*& out) {
 }
 
 // Builds the device plan of IR `id` on `dev` for the ranks the clique hosts there.
+// Direct messages. A receive that only stores the message (recv, rcs) may have it written by the
+// sender straight into the receive's local span when no op of the receiving rank touches that span
+// before the receive, and none touches it unordered with it: the span is then dead until the
+// receive, so writing it early is indistinguishable from writing it at the receive. Order is the
+// happens-before relation of sequential execution, declared deps and the k-th send -> k-th receive
+// matching (the graph of scheduler.hpp:652-717). The sender addresses the span through its own
+// op's dst fields (lowering.hpp:71), which must name it exactly.
+// Returns flags[rank][tb index][step] with kInDirect on such receives and kOutDirect on their sends.
+std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p) {
+  const int R = p.ranks();
+  std::vector<std::vector<std::vector<uint8_t>>> flags(R);
+  std::vector<std::vector<int>> base(R);  // unit index of (rank, tb, 0)
+  int n = 0;
+  for (int r = 0; r < R; ++r) {
+    flags[r].resize(p.gpus[r].tbs.size());
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      flags[r][t].assign(p.gpus[r].tbs[t].ops.size(), 0);
+      base[r].push_back(n);
+      n += static_cast<int>(p.gpus[r].tbs[t].ops.size());
+    }
+  }
+  if (n == 0 || n > 65536) return flags;
+  std::vector<std::vector<int>> succ(n);
+  struct Ref {
+    int rank, tb, step;
+  };
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<Ref>, std::vector<Ref>>> conns;
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        const int u = base[r][t] + static_cast<int>(s);
+        if (s + 1 < tb.ops.size()) succ[u].push_back(u + 1);
+        for (const Dep& d : tb.ops[s].deps) {
+          const int ti = tb_index(p, r, d.tb);
+          if (ti >= 0 && d.step >= 0 && d.step < static_cast<int>(p.gpus[r].tbs[ti].ops.size())) succ[base[r][ti] + d.step].push_back(u);
+        }
+        if (op_sends(tb.ops[s].op) && tb.send_peer >= 0) conns[{r, tb.send_peer, tb.channel}].first.push_back({r, static_cast<int>(t), static_cast<int>(s)});
+        if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0) conns[{tb.recv_peer, r, tb.channel}].second.push_back({r, static_cast<int>(t), static_cast<int>(s)});
+      }
+    }
+  for (auto& [key, c] : conns) {
+    if (c.first.size() != c.second.size()) return flags;  // unbalanced: no direct messages at all
+    for (size_t k = 0; k < c.first.size(); ++k)
+      succ[base[c.first[k].rank][c.first[k].tb] + c.first[k].step].push_back(base[c.second[k].rank][c.second[k].tb] + c.second[k].step);
+  }
+  // reachability (reverse topological order); a cycle means no static order, so nothing is direct
+  std::vector<int> indeg(n, 0), order;
+  for (int u = 0; u < n; ++u)
+    for (int v : succ[u]) ++indeg[v];
+  for (int u = 0; u < n; ++u)
+    if (!indeg[u]) order.push_back(u);
+  for (size_t i = 0; i < order.size(); ++i)
+    for (int v : succ[order[i]])
+      if (--indeg[v] == 0) order.push_back(v);
+  if (static_cast<int>(order.size()) != n) return flags;
+  const size_t words = (n + 63) / 64;
+  std::vector<uint64_t> reach(static_cast<size_t>(n) * words, 0);
+  for (auto it = order.rbegin(); it != order.rend(); ++it) {
+    uint64_t* ru = &reach[static_cast<size_t>(*it) * words];
+    ru[*it / 64] |= 1ull << (*it % 64);
+    for (int v : succ[*it])
+      for (size_t w = 0; w < words; ++w) ru[w] |= reach[static_cast<size_t>(v) * words + w];
+  }
+  auto reaches = [&](int a, int b) { return (reach[static_cast<size_t>(a) * words + b / 64] >> (b % 64)) & 1; };
+  auto storage = [&](Buf b) { return p.inplace && b == Buf::output ? Buf::input : b; };
+  struct Span {
+    Buf b;
+    int off, count;
+  };
+  auto overlaps = [&](const Span& x, const Span& y) {
+    return storage(x.b) == storage(y.b) && x.off < y.off + y.count && y.off < x.off + x.count;
+  };
+  auto accesses = [&](const Op& op, std::vector<Span>& out) {  // local reads + writes (lowering.hpp:96-119)
+    out.clear();
+    switch (op.op) {
+      case Opcode::send: case Opcode::rrs: out.push_back({op.src_buf, op.src_off, op.count}); break;
+      case Opcode::recv: out.push_back({op.dst_buf, op.dst_off, op.count}); break;
+      case Opcode::rcs: case Opcode::rrcs: out.push_back({op.src_buf, op.src_off, op.count}); break;
+      case Opcode::copy: case Opcode::reduce: case Opcode::rrc:
+        out.push_back({op.src_buf, op.src_off, op.count});
+        out.push_back({op.dst_buf, op.dst_off, op.count});
+        break;
+      default: break;
+    }
+  };
+  std::vector<Span> acc;
+  for (auto& [key, c] : conns) {
+    for (size_t k = 0; k < c.second.size(); ++k) {
+      const Ref rx = c.second[k], tx = c.first[k];
+      const Op& rop = p.gpus[rx.rank].tbs[rx.tb].ops[rx.step];
+      const Op& sop = p.gpus[tx.rank].tbs[tx.tb].ops[tx.step];
+      if (rop.op != Opcode::recv && rop.op != Opcode::rcs) continue;
+      const Span x = rop.op == Opcode::recv ? Span{rop.dst_buf, rop.dst_off, rop.count} : Span{rop.src_buf, rop.src_off, rop.count};
+      if (storage(sop.dst_buf) != storage(x.b) || sop.dst_off != x.off || sop.count != x.count) continue;
+      const int ru = base[rx.rank][rx.tb] + rx.step;
+      bool ok = true;
+      for (size_t t = 0; t < p.gpus[rx.rank].tbs.size() && ok; ++t)
+        for (size_t s = 0; s < p.gpus[rx.rank].tbs[t].ops.size() && ok; ++s) {
+          const int u = base[rx.rank][t] + static_cast<int>(s);
+          if (u == ru) continue;
+          accesses(p.gpus[rx.rank].tbs[t].ops[s], acc);
+          for (const Span& y : acc)
+            if (overlaps(x, y) && !reaches(ru, u)) ok = false;  // before or unordered with the receive
+        }
+      if (ok) {
+        flags[rx.rank][rx.tb][rx.step] |= kInDirect;
+        flags[tx.rank][tx.tb][tx.step] |= kOutDirect;
+      }
+    }
+  }
+  return flags;
+}
+
 ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   if (ds.plans.size() <= static_cast<size_t>(id)) ds.plans.resize(id + 1);
   DevicePlan& plan = ds.plans[id];
@@ -431,6 +547,13 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   std::vector<DevDep> deps;
   std::vector<DevChan> chans;
   plan.sys_scope = false;
+  // direct messages only between ranks of this launch: the sender needs the receiver's buffers
+  const auto direct = c0->cfg.direct ? direct_messages(p) : std::vector<std::vector<std::vector<uint8_t>>>();
+  auto slot_of = [&](int rank) {
+    for (size_t i = 0; i < plan.ranks.size(); ++i)
+      if (plan.ranks[i] == rank) return static_cast<int>(i);
+    return -1;
+  };
   std::vector<int> sem_base_of_rank;
   int sem_next = 0;
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
@@ -450,8 +573,16 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       d.nops = static_cast<int>(tb.ops.size());
       d.sem = sem_base_of_rank[slot] + static_cast<int>(t) * L;
       d.chan_in = d.chan_out = -1;
-      for (const Op& op : tb.ops) {
+      d.peer_slot = tb.send_peer >= 0 ? slot_of(tb.send_peer) : -1;
+      const bool in_local = tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0;
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        const Op& op = tb.ops[s];
         DevOp o{};
+        if (!direct.empty()) {
+          const uint8_t f = direct[r][t][s];
+          if ((f & kInDirect) && in_local) o.direct |= kInDirect;
+          if ((f & kOutDirect) && d.peer_slot >= 0) o.direct |= kOutDirect;
+        }
         o.opcode = static_cast<uint8_t>(op.op);
         o.src_buf = static_cast<uint8_t>(op.src_buf);
         o.dst_buf = static_cast<uint8_t>(op.dst_buf);
@@ -1168,6 +1299,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "tile_bytes") c.tile_bytes = value;
   else if (k == "timeout_ms") c.timeout_ms = value;
   else if (k == "trace") c.trace = static_cast<int>(value);
+  else if (k == "direct") c.direct = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }

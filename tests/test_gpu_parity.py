@@ -167,3 +167,16 @@ def test_size_range_selection_and_no_fallback():
     finally:
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("name,count", [("twostep_a2a_2x4", 2048), ("ring_ag_8", 1024), ("ring_ar_8_ch1", 8 * 1024)])
+def test_fifo_only_path(name, count):
+    """direct=0 forces every message through the receiver FIFO (the multi-process path)."""
+    _check(name, count, direct=0)
+    _check(name, count, direct=0, proto="ll")
+
+
+@pytest.mark.parametrize("name,count", [("twostep_a2a_2x4", 4096), ("ring_ag_8", 2048), ("twostep_a2a_1x8", 1000)])
+def test_direct_path_ll(name, count):
+    _check(name, count, proto="ll")
+    _check(name, count, proto="ll", dtype="bfloat16")
