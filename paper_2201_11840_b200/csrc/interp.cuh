@@ -504,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int total = my_tiles * nops;
 
   // one non-blocking poll of op q's preconditions (one flag per lane); true when all hold
+  bool pend_send = false, pend_recv = false;  // the in-flight op will advance sent / rcvd
   auto poll = [&](int q) -> bool {
     const int s = q % nops;
     const int64_t it = q / nops;
@@ -511,8 +512,10 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
     const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
     const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
     bool ok = true;
-    if (wl == 0 && send && !out_d) ok = ld_relaxed(cout.tail, sys) + slots >= sent + 1;
-    if (wl == 1 && recv && !(LL && !in_d)) ok = ld_relaxed(cin.head, sys) >= rcvd + 1;
+    // counters as they will be once the in-flight op is published
+    const uint64_t sent_q = sent + (pend_send ? 1 : 0), rcvd_q = rcvd + (pend_recv ? 1 : 0);
+    if (wl == 0 && send && !out_d) ok = ld_relaxed(cout.tail, sys) + slots >= sent_q + 1;
+    if (wl == 1 && recv && !(LL && !in_d)) ok = ld_relaxed(cin.head, sys) >= rcvd_q + 1;
     for (int d = wl - 2; d >= 0 && d < op.ndeps; d += 30) {
       const DevDep dd = deps[op.dep_begin + d];
       ok = ok && ld_relaxed(sems + dd.sem + lane, false) >= ((epoch << 32) | static_cast<uint64_t>(it * dd.nops + dd.step + 1));
@@ -564,6 +567,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
           if (psend) ++sent;
           if (precv) ++rcvd;
           pending = -1;
+          pend_send = pend_recv = false;
           __syncwarp();
         }
       }
@@ -660,6 +664,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       ++posted;
     }
     pending = q;
+    pend_send = send;
+    pend_recv = recv;
     pending_data = kind != 0;
   }
   // release the data warps
