@@ -127,6 +127,8 @@ typedef struct {
   int64_t wire_bytes; /* max over ranks of bytes sent or received by send/recv-family ops */
   int64_t hbm_bytes;  /* algorithmic local bytes (reads + writes of user/scratch buffers) of the launch */
   char name[64];      /* IR name */
+  int unit_warps;     /* warps interpreting one (thread block, lane) */
+  int group;          /* tiles per op-major group inside a lane */
 } gc3PlanInfo;
 /* collective: 0 allreduce, 1 allgather, 2 reducescatter, 3 alltoall; count as in the NCCL call. */
 ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDataType_t datatype, gc3PlanInfo* info);

@@ -83,7 +83,9 @@ struct LaunchArgs {
   int32_t* abort_flag;  // device word: any block that times out raises it
   uint64_t* err_info;   // host-mapped: {code, rank, tb, step, tile, what, 0, 0}
   uint64_t* trace;      // optional %globaltimer event log: [block][op seq][4] (see interp.cuh)
-  int32_t trace_ops;    // ops recorded per block
+  int32_t trace_ops;    // ops recorded per unit
+  int32_t unit_warps;   // warps interpreting one (thread block, lane); kThreads/32 divisible by it
+  int32_t group;        // tiles per op-major group inside a lane (1 = tile-major)
   int32_t pad_;
   char* bufs[kMaxLocalRanks][3];  // per local rank: input, output, scratch
 };

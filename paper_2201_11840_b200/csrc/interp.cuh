@@ -32,7 +32,7 @@
 #define GC3_UNROLL_COPY 8
 #endif
 #ifndef GC3_MINBLOCKS
-#define GC3_MINBLOCKS 2
+#define GC3_MINBLOCKS 1
 #endif
 
 namespace gc3 {
@@ -209,32 +209,29 @@ struct RedNone {
 };
 
 // ------------------------------------------------------------------ data movers
-// Executed by the data warps only: thread `t` of `n` data threads.
+// Executed by the `n` threads of one unit; `t` is the thread's index in the unit.
 // out0 (and out1 if non-null) = RED ? R(in0, in1) : in0, over nbytes. All pointers 16B aligned
 // takes the 128-bit path; the ragged remainder (and misaligned segments) go element-wise.
-constexpr int kDataThreads = kThreads - 32;
-
 template <class R, bool RED, bool TWO>
-__device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* o0, uint4* o1, int64_t nvec, int t) {
+__device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* o0, uint4* o1, int64_t nvec, int t, int n) {
   constexpr int U = R::kReduce ? GC3_UNROLL : GC3_UNROLL_COPY;  // 128-bit loads in flight per thread
-  constexpr int N = kDataThreads;
   int64_t i = t;
-  for (; i + (U - 1) * N < nvec; i += U * N) {
+  for (; i + (U - 1) * n < nvec; i += U * n) {
     uint4 x[U], y[U];
 #pragma unroll
-    for (int k = 0; k < U; ++k) x[k] = ld_cg(a + i + k * N);
+    for (int k = 0; k < U; ++k) x[k] = ld_cg(a + i + k * n);
     if (RED) {
 #pragma unroll
-      for (int k = 0; k < U; ++k) y[k] = ld_cg(b + i + k * N);
+      for (int k = 0; k < U; ++k) y[k] = ld_cg(b + i + k * n);
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const uint4 v = RED ? R::template vec<uint4>(x[k], y[k]) : x[k];
-      st_vec(o0 + i + k * N, v);
-      if (TWO) st_vec(o1 + i + k * N, v);
+      st_vec(o0 + i + k * n, v);
+      if (TWO) st_vec(o1 + i + k * n, v);
     }
   }
-  for (; i < nvec; i += N) {
+  for (; i < nvec; i += n) {
     const uint4 x = ld_cg(a + i);
     const uint4 v = RED ? R::template vec<uint4>(x, ld_cg(b + i)) : x;
     st_vec(o0 + i, v);
@@ -243,9 +240,9 @@ __device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* 
 }
 
 template <class R>
-__device__ __forceinline__ void move_elems(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, bool red, int t) {
+__device__ __forceinline__ void move_elems(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, bool red, int t, int n) {
   constexpr int E = R::kEsize;
-  for (int64_t i = t * static_cast<int64_t>(E); i < nbytes; i += static_cast<int64_t>(kDataThreads) * E) {
+  for (int64_t i = t * static_cast<int64_t>(E); i < nbytes; i += static_cast<int64_t>(n) * E) {
     char tmp[E];
     if (red) R::elem(a + i, b + i, tmp);
     else
@@ -257,7 +254,7 @@ __device__ __forceinline__ void move_elems(const char* a, const char* b, char* o
 }
 
 template <class R>
-__device__ void move(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, int t) {
+__device__ void move(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, int t, int n) {
   if (nbytes <= 0) return;
   if (!o0) {
     o0 = o1;
@@ -274,16 +271,16 @@ __device__ void move(const char* a, const char* b, char* o0, char* o1, int64_t n
     uint4* v0 = reinterpret_cast<uint4*>(o0);
     uint4* v1 = reinterpret_cast<uint4*>(o1);
     if (red) {
-      if (o1) move_vec<R, true, true>(va, vb, v0, v1, nvec, t);
-      else move_vec<R, true, false>(va, vb, v0, v1, nvec, t);
+      if (o1) move_vec<R, true, true>(va, vb, v0, v1, nvec, t, n);
+      else move_vec<R, true, false>(va, vb, v0, v1, nvec, t, n);
     } else {
-      if (o1) move_vec<R, false, true>(va, vb, v0, v1, nvec, t);
-      else move_vec<R, false, false>(va, vb, v0, v1, nvec, t);
+      if (o1) move_vec<R, false, true>(va, vb, v0, v1, nvec, t, n);
+      else move_vec<R, false, false>(va, vb, v0, v1, nvec, t, n);
     }
     done = nvec << 4;
   }
   if (done < nbytes)
-    move_elems<R>(a + done, b ? b + done : nullptr, o0 + done, o1 ? o1 + done : nullptr, nbytes - done, red, t);
+    move_elems<R>(a + done, b ? b + done : nullptr, o0 + done, o1 ? o1 + done : nullptr, nbytes - done, red, t, n);
 }
 
 // ------------------------------------------------------------------ watchdog
@@ -310,22 +307,45 @@ static __device__ __noinline__ void raise_timeout(const Ctx c, int what) {
   }
 }
 
+// Spins until *p >= target; false if the launch was aborted. Polls with relaxed loads (an acquire
+// load would invalidate L1 on every iteration) and acquires once with a fence when satisfied.
+__device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys, const Ctx& c, int what) {
+  if (ld_relaxed(p, sys) >= target) {
+    fence_acq_rel(sys);
+    return true;
+  }
+  const uint64_t start = globaltimer();
+  for (int n = 0;; ++n) {
+    if (ld_relaxed(p, sys) >= target) {
+      fence_acq_rel(sys);
+      return true;
+    }
+    if ((n & 255) == 255) {
+      if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
+      if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
+        raise_timeout(c, what);
+        return false;
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ bool is_recv(int op) {
   return op == kOpRecv || op == kOpRrc || op == kOpRcs || op == kOpRrcs || op == kOpRrs;
 }
 __device__ __forceinline__ bool is_send(int op) { return op == kOpSend || op == kOpRcs || op == kOpRrcs || op == kOpRrs; }
 
-// ------------------------------------------------------------------ LL op body (data warps)
-// Lines of the incoming/outgoing message are distributed over the data threads; every thread
+// ------------------------------------------------------------------ LL op body
+// Lines of the incoming/outgoing message are distributed over the unit's threads; every thread
 // polls the flags of its own lines only. inl == nullptr: the incoming message is in place (direct)
 // or absent; outl == nullptr: the outgoing message goes to outd (direct, plain stores) or is absent.
 template <class R>
-__device__ void ll_op(int opcode, int count, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl,
-                      uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, const Ctx& c, int t) {
+__device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl,
+                      uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, const Ctx& c, int t, int n) {
   const int64_t lines_per_seg = tbytes >> 3;
   const int64_t nlines = lines_per_seg * count;
   const bool send = is_send(opcode);
-  for (int64_t k = t; k < nlines; k += kDataThreads) {
+  for (int64_t k = t; k < nlines; k += n) {
     const int j = static_cast<int>(k / lines_per_seg);
     const int64_t off = ((k - j * lines_per_seg) << 3) + j * chunk_bytes;
     char* src = src0 + off;
@@ -335,14 +355,14 @@ __device__ void ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
       uint4 l = ld_volatile_line(inl + k);
       if (l.y != in_flag || l.w != in_flag) {
         const uint64_t start = globaltimer();
-        for (int n = 0;; ++n) {
+        for (int it = 0;; ++it) {
           l = ld_volatile_line(inl + k);
           if (l.y == in_flag && l.w == in_flag) break;
-          if ((n & 255) == 255) {
-            if (*reinterpret_cast<volatile int*>(c.abort_flag)) return;  // the control warp exits the launch
+          if ((it & 255) == 255) {
+            if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
             if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
               raise_timeout(c, 4);
-              return;
+              return false;
             }
           }
         }
@@ -373,93 +393,45 @@ __device__ void ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
       else st_vec8(outd + off, v);
     }
   }
+  return true;
 }
 
 // ------------------------------------------------------------------ the interpreter
-// Warp-specialised execution of one (IR thread block, lane) per CUDA block:
-//   * warp 0 (control) walks the (tile, op) sequence: it waits for each op's preconditions
-//     (deps, FIFO credit, posted message), describes the op's data movement in a shared-memory
-//     descriptor, and publishes the op (FIFO head / tail, semaphore) once the data warps are done;
-//   * warps 1.. (data) execute descriptors: vectorised moves with the reduction fused in, or LL
-//     line traffic.
-// Descriptors are double-buffered. While the data warps move op k, the control warp already polls
-// op k+1's preconditions, but it publishes op k as soon as op k's data is done (never after
-// blocking on op k+1, which could depend on op k's publication). A named barrier hands a
-// descriptor to the data warps; a shared counter reports completion. Ops are separated: the data
-// warps start a descriptor only after the previous one completed block-wide.
-struct Desc {
-  const char* a;
-  const char* b;
-  char* o0;
-  char* o1;
-  int64_t sa, sb, s0, s1;  // per-segment strides
-  int64_t nbytes;          // per segment
-  // LL
-  char* src;
-  char* dst;
-  const uint4* inl;
-  uint4* outl;
-  char* outd;
-  int64_t chunk_bytes;
-  uint32_t in_flag, out_flag;
-  int32_t count;
-  int32_t opcode;
-  int32_t kind;  // 1 vector move, 2 LL, 3 exit
-  int32_t step;
-  int64_t tile;
-};
-
-__device__ __forceinline__ void bar_sync(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(kThreads) : "memory"); }
-__device__ __forceinline__ void bar_arrive(int id) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(kThreads) : "memory"); }
+// A "unit" of `unit_warps` warps interprets one (IR thread block, lane): for each tile of the lane,
+// for each op in order:
+//   (1) wait: deps on other thread blocks' semaphores, a free outgoing FIFO slot,
+//       a posted incoming message -- polled in parallel by different threads of the unit;
+//   (2) move: the unit's threads move the op's bytes, the reduction fused into the transfer;
+//   (3) publish: after a unit barrier, thread 0 fences and posts the slot counter, frees the
+//       incoming slot and sets the semaphore.
+// A CUDA block holds kThreads/32/unit_warps units, so small units give many independent pipelines
+// (a thread block's tiles are serial inside one lane; concurrency comes from lanes).
+// Units sync with __syncwarp (1 warp) or a per-unit named barrier (bar.sync id, n).
+__device__ __forceinline__ bool unit_and(bool p, int uw, int bar_id, int n) {
+  if (uw == 1) return __all_sync(0xffffffffu, p);
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbar.red.and.pred q, %2, %3, p;\n\tselp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r) : "r"(static_cast<int>(p)), "r"(bar_id), "r"(n) : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ void unit_sync(int uw, int bar_id, int n) {
+  if (uw == 1) __syncwarp();
+  else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(n) : "memory");
+}
 
 template <class R, bool LL>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
-  __shared__ Desc s_desc[2];
-  __shared__ unsigned s_done[2];
+  const int uw = a.unit_warps;
+  const int n = uw * 32;                         // threads per unit
+  const int uib = threadIdx.x / n;               // unit in this block
+  const int t = threadIdx.x - uib * n;           // thread in unit
+  const int unit = blockIdx.x * (kThreads / n) + uib;
   const int lanes = a.lanes;
-  const int lane = blockIdx.x % lanes;
-  const int tbi = blockIdx.x / lanes;
-  if (threadIdx.x < 2) s_done[threadIdx.x] = 0;
-  __syncthreads();
-
-  if (threadIdx.x >= 32) {  // ---------------- data warps
-    const int t = threadIdx.x - 32;
-    const Ctx c{a.abort_flag, a.err_info, a.timeout_ns, 0, tbi, 0, 0};
-    for (int n = 0;; ++n) {
-      bar_sync(1 + (n & 1));
-      const Desc& d = s_desc[n & 1];
-      const int kind = d.kind;
-      if (kind == 3) return;
-      if (kind == 2) {
-        Ctx cc = c;
-        cc.step = d.step;
-        cc.tile = d.tile;
-        ll_op<R>(d.opcode, d.count, d.src, d.dst, d.chunk_bytes, d.nbytes, d.inl, d.outl, d.outd, d.in_flag, d.out_flag, cc, t);
-      } else {
-        const char* pa = d.a;
-        const char* pb = d.b;
-        char* p0 = d.o0;
-        char* p1 = d.o1;
-        for (int j = 0; j < d.count; ++j) {
-          move<R>(pa, pb, p0, p1, d.nbytes, t);
-          pa += d.sa;
-          if (pb) pb += d.sb;
-          if (p0) p0 += d.s0;
-          if (p1) p1 += d.s1;
-        }
-      }
-      // release this warp's stores at CTA scope; the control warp's scoped fence is cumulative
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) {
-        unsigned prev;
-        asm volatile("atom.release.cta.shared::cta.add.u32 %0, [%1], 1;"
-                     : "=r"(prev) : "r"(static_cast<unsigned>(__cvta_generic_to_shared(&s_done[n & 1]))) : "memory");
-      }
-    }
-  }
-
-  // ---------------- control warp
-  const int wl = threadIdx.x;
+  if (unit >= a.ntbs * lanes) return;  // a whole unit leaves together
+  const int bar_id = 1 + uib;
+  const int lane = unit % lanes;
+  const int tbi = unit / lanes;
   const DevTb tb = a.tbs[tbi];
   const bool sys = a.sys_scope != 0;
   const bool has_in = tb.chan_in >= 0, has_out = tb.chan_out >= 0;
@@ -469,209 +441,126 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const uint64_t epoch = a.epoch;
   // this rank's buffers and the send peer's (direct writes), selected with constant indices (a
   // dynamically indexed kernel parameter would be copied to local memory)
-  char* buf[3] = {nullptr, nullptr, nullptr};
-  char* peer[3] = {nullptr, nullptr, nullptr};
+  char *b0 = nullptr, *b1 = nullptr, *b2 = nullptr, *q0 = nullptr, *q1 = nullptr, *q2 = nullptr;
 #pragma unroll
   for (int i = 0; i < kMaxLocalRanks; ++i) {
     if (i == tb.rank_slot) {
-      buf[0] = a.bufs[i][0];
-      buf[1] = a.bufs[i][1];
-      buf[2] = a.bufs[i][2];
+      b0 = a.bufs[i][0];
+      b1 = a.bufs[i][1];
+      b2 = a.bufs[i][2];
     }
     if (i == tb.peer_slot) {
-      peer[0] = a.bufs[i][0];
-      peer[1] = a.bufs[i][1];
-      peer[2] = a.bufs[i][2];
+      q0 = a.bufs[i][0];
+      q1 = a.bufs[i][1];
+      q2 = a.bufs[i][2];
     }
   }
-  DevChan cin{}, cout{};
-  if (has_in) cin = a.chans[tb.chan_in + lane];
-  if (has_out) cout = a.chans[tb.chan_out + lane];
-  uint64_t rcvd = has_in ? *cin.mine : 0;
-  uint64_t sent = has_out ? *cout.mine : 0;
+  const DevChan* const cin = has_in ? a.chans + tb.chan_in + lane : nullptr;
+  const DevChan* const cout = has_out ? a.chans + tb.chan_out + lane : nullptr;
+  uint64_t rcvd = has_in ? *cin->mine : 0;
+  uint64_t sent = has_out ? *cout->mine : 0;
   uint64_t* const sems = a.sems;
-  uint64_t* const my_sem = sems + tb.sem + lane;
   const DevOp* const ops = a.ops + tb.op_begin;
-  const DevDep* const deps = a.deps;
   Ctx c{a.abort_flag, a.err_info, a.timeout_ns, tb.rank_slot, tbi, 0, 0};
   uint64_t* const trace = a.trace;
   const int trace_ops = a.trace_ops;
   auto stamp = [&](int qq, int k) {
-    if (trace && qq < trace_ops && wl == 0) trace[(static_cast<int64_t>(blockIdx.x) * trace_ops + qq) * 4 + k] = globaltimer();
+    if (trace && qq < trace_ops) trace[(static_cast<int64_t>(unit) * trace_ops + qq) * 4 + k] = globaltimer();
   };
+
+  // Execution order inside the lane: groups of G tiles, op-major within a group (op s of every tile
+  // of the group, then op s+1). Tiles are position-independent instances of the program, and every
+  // thread block uses the same order, so the k-th send still meets the k-th receive on each
+  // connection; a group lets the lane's tiles pipeline through multi-hop chains (the planner checks
+  // the order is deadlock-free at this FIFO depth). G = 1 is the paper's tile-major loop.
   const int nops = tb.nops;
-  const int my_tiles = ntiles > lane ? static_cast<int>((ntiles - 1 - lane) / lanes + 1) : 0;
-  const int total = my_tiles * nops;
-
-  // one non-blocking poll of op q's preconditions (one flag per lane); true when all hold
-  bool pend_send = false, pend_recv = false;  // the in-flight op will advance sent / rcvd
-  auto poll = [&](int q) -> bool {
-    const int s = q % nops;
-    const int64_t it = q / nops;
-    const DevOp op = ops[s];
-    const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
-    const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
-    bool ok = true;
-    // counters as they will be once the in-flight op is published
-    const uint64_t sent_q = sent + (pend_send ? 1 : 0), rcvd_q = rcvd + (pend_recv ? 1 : 0);
-    if (wl == 0 && send && !out_d) ok = ld_relaxed(cout.tail, sys) + slots >= sent_q + 1;
-    if (wl == 1 && recv && !(LL && !in_d)) ok = ld_relaxed(cin.head, sys) >= rcvd_q + 1;
-    for (int d = wl - 2; d >= 0 && d < op.ndeps; d += 30) {
-      const DevDep dd = deps[op.dep_begin + d];
-      ok = ok && ld_relaxed(sems + dd.sem + lane, false) >= ((epoch << 32) | static_cast<uint64_t>(it * dd.nops + dd.step + 1));
-    }
-    return __all_sync(0xffffffffu, ok);
-  };
-  auto aborted = [&]() { return *reinterpret_cast<volatile int*>(a.abort_flag) != 0; };
-
-  int posted = 0;            // descriptors handed to the data warps
-  int pending = -1;          // op whose data is in flight (published when done), -1 if none
-  bool pending_data = false;
-  uint64_t wait_start = 0;
-  bool pre_ok = false;
-  for (int q = 0; q <= total; ++q) {
-    // wait for op q's preconditions while completing op `pending`
-    pre_ok = q == total;
-    if (!pre_ok) {
-      c.step = q % nops;
-      c.tile = lane + static_cast<int64_t>(q / nops) * lanes;
-      stamp(q, 0);
-    }
-    wait_start = 0;
-    for (int n = 0;; ++n) {
-      if (!pre_ok) pre_ok = poll(q);
-      if (pending >= 0) {
-        const bool done = !pending_data || *reinterpret_cast<volatile unsigned*>(&s_done[(posted - 1) & 1]) == kThreads / 32 - 1;
-        if (done) {
-          // publish op `pending`: slot posted / slot freed / semaphore
-          const int ps = pending % nops;
-          const DevOp pop = ops[ps];
-          const bool precv = is_recv(pop.opcode), psend = is_send(pop.opcode);
-          const bool pin_d = (pop.direct & kInDirect) != 0, pout_d = (pop.direct & kOutDirect) != 0;
-          const bool pll_out = LL && psend && !pout_d;
-          stamp(pending, 2);
-          if (wl == 0) {
-            if (pending_data) s_done[(posted - 1) & 1] = 0;
-            fence_acq_rel(sys);
-            if (psend && !pll_out) st_release(cout.head, sent + 1, sys);
-            if (precv) st_release(cin.tail, rcvd + 1, sys);
-            if (pop.has_dep)
-              st_release(my_sem, (epoch << 32) | static_cast<uint64_t>((pending / nops) * nops + ps + 1), false);
-            if (pending + 1 == total) {  // persistent FIFO counters for the next launch
-              if (has_in) *cin.mine = rcvd + (precv ? 1 : 0);
-              if (has_out) *cout.mine = sent + (psend ? 1 : 0);
-            }
-          }
-          (void)pin_d;
-          stamp(pending, 3);
-          if (psend) ++sent;
-          if (precv) ++rcvd;
-          pending = -1;
-          pend_send = pend_recv = false;
-          __syncwarp();
-        }
+  const int64_t my_tiles = ntiles > lane ? (ntiles - 1 - lane) / lanes + 1 : 0;
+  const int G = a.group > 0 ? a.group : 1;
+  int q = 0;  // position in the lane's (tile, op) order; semaphores publish q + 1
+  for (int64_t g0 = 0; g0 < my_tiles; g0 += G) {
+    const int gsize = static_cast<int>(min(static_cast<int64_t>(G), my_tiles - g0));
+    for (int s = 0; s < nops; ++s)
+    for (int jj = 0; jj < gsize; ++jj, ++q) {
+      const int64_t i_tile = g0 + jj;
+      const int64_t tile = lane + i_tile * lanes;
+      const int64_t t0 = tile * tile_elems;
+      const int64_t tbytes = min(tile_elems, chunk_elems - t0) * R::kEsize;
+      const int64_t t0_bytes = t0 * R::kEsize;
+      c.tile = tile;
+      const DevOp op = ops[s];
+      const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
+      const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
+      const bool ll_in = LL && recv && !in_d, ll_out = LL && send && !out_d;
+      c.step = s;
+      if (t == 0) stamp(q, 0);
+      // (1) preconditions, polled in parallel
+      bool ok = true;
+      if (t == 0 && send && !out_d) ok = wait_geq(cout->tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
+      if (t == 1 && recv && !ll_in) ok = wait_geq(cin->head, rcvd + 1, sys, c, 3);
+      for (int d = t - 2; d >= 0 && d < op.ndeps; d += n - 2) {
+        const DevDep dd = a.deps[op.dep_begin + d];
+        const uint64_t target = (epoch << 32) | static_cast<uint64_t>(g0 * dd.nops + static_cast<int64_t>(dd.step) * gsize + jj + 1);
+        ok = ok && wait_geq(sems + dd.sem + lane, target, false, c, 1);
       }
-      if (pre_ok && pending < 0) break;
-      if ((n & 63) == 63) {
-        if (aborted()) break;
-        if (a.timeout_ns) {
-          const uint64_t now = globaltimer();
-          if (!wait_start) wait_start = now;
-          else if (now - wait_start > a.timeout_ns) {
-            if (wl == 0) raise_timeout(c, pending >= 0 ? 5 : 1);
-            break;
+      if (!unit_and(ok, uw, bar_id, n)) return;
+      if (t == 0) stamp(q, 1);
+
+      // (2) the transfer, with the reduction fused in
+      auto sel = [&](int b) { return b == 0 ? b0 : (b == 1 ? b1 : b2); };
+      auto selp = [&](int b) { return b == 0 ? q0 : (b == 1 ? q1 : q2); };
+      char* src = sel(op.src_buf) + op.src_off * chunk_bytes + t0_bytes;
+      char* dst = sel(op.dst_buf) + op.dst_off * chunk_bytes + t0_bytes;
+      char* peer_dst = out_d ? selp(op.dst_buf) + op.dst_off * chunk_bytes + t0_bytes : nullptr;
+      const char* in = recv && !in_d ? cin->fifo + static_cast<int64_t>(rcvd % slots) * cin->slot_bytes : nullptr;
+      char* out = send && !out_d ? cout->fifo + static_cast<int64_t>(sent % slots) * cout->slot_bytes : nullptr;
+      if (ll_in || ll_out) {
+        ok = ll_op<R>(op.opcode, op.count, src, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
+                      ll_out ? reinterpret_cast<uint4*>(out) : nullptr, peer_dst, static_cast<uint32_t>(rcvd + 1),
+                      static_cast<uint32_t>(sent + 1), c, t, n);
+      } else {
+        for (int j = 0; j < op.count; ++j) {
+          char* sj = src + j * chunk_bytes;
+          char* dj = dst + j * chunk_bytes;
+          const char* mi = in ? in + j * tbytes : nullptr;
+          char* mo = out_d ? peer_dst + j * chunk_bytes : (out ? out + j * tbytes : nullptr);
+          switch (op.opcode) {
+            case kOpSend: move<R>(sj, nullptr, mo, nullptr, tbytes, t, n); break;
+            case kOpRecv:
+              if (!in_d) move<R>(mi, nullptr, dj, nullptr, tbytes, t, n);
+              break;
+            case kOpCopy: move<R>(sj, nullptr, dj, nullptr, tbytes, t, n); break;
+            case kOpReduce: move<R>(dj, sj, dj, nullptr, tbytes, t, n); break;
+            case kOpRrc: move<R>(sj, mi, dj, nullptr, tbytes, t, n); break;
+            case kOpRcs:
+              if (in_d) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
+              else move<R>(mi, nullptr, sj, mo, tbytes, t, n);
+              break;
+            case kOpRrcs: move<R>(sj, mi, sj, mo, tbytes, t, n); break;
+            case kOpRrs: move<R>(sj, mi, nullptr, mo, tbytes, t, n); break;
+            default: break;
           }
         }
       }
-    }
-    if (!(pre_ok && pending < 0) || q == total) break;
-    fence_acq_rel(sys);  // acquire what the polled flags published
-    stamp(q, 1);
+      if (t == 0) stamp(q, 2);
+      if (!unit_and(ok, uw, bar_id, n)) return;
 
-    // describe op q's data movement
-    const int s = q % nops;
-    const int64_t tile = lane + static_cast<int64_t>(q / nops) * lanes;
-    const int64_t t0 = tile * tile_elems;
-    const int64_t tlen = min(tile_elems, chunk_elems - t0);
-    const int64_t tbytes = tlen * R::kEsize;
-    const int64_t t0_bytes = t0 * R::kEsize;
-    const DevOp op = ops[s];
-    const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
-    const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
-    const bool ll_in = LL && recv && !in_d, ll_out = LL && send && !out_d;
-    auto sel = [](int b, char* const* v) { return b == 0 ? v[0] : (b == 1 ? v[1] : v[2]); };
-    char* src = sel(op.src_buf, buf) + op.src_off * chunk_bytes + t0_bytes;
-    char* dst = sel(op.dst_buf, buf) + op.dst_off * chunk_bytes + t0_bytes;
-    char* peer_dst = out_d ? sel(op.dst_buf, peer) + op.dst_off * chunk_bytes + t0_bytes : nullptr;
-    const char* in = recv && !in_d ? cin.fifo + static_cast<int64_t>(rcvd % slots) * cin.slot_bytes : nullptr;
-    char* out = send && !out_d ? cout.fifo + static_cast<int64_t>(sent % slots) * cout.slot_bytes : nullptr;
-    int kind = 1;
-    const char *pa = nullptr, *pb = nullptr;
-    char *p0 = nullptr, *p1 = nullptr;
-    int64_t sa = chunk_bytes, sb = tbytes, s0 = chunk_bytes, s1 = tbytes;
-    char* mo = out_d ? peer_dst : out;
-    const int64_t smo = out_d ? chunk_bytes : tbytes;
-    if (ll_in || ll_out) {
-      kind = 2;
-    } else {
-      switch (op.opcode) {
-        case kOpSend: pa = src; p0 = mo; s0 = smo; break;
-        case kOpRecv:
-          if (in_d) kind = 0;
-          else { pa = in; sa = tbytes; p0 = dst; }
-          break;
-        case kOpCopy: pa = src; p0 = dst; break;
-        case kOpReduce: pa = dst; pb = src; sb = chunk_bytes; p0 = dst; break;
-        case kOpRrc: pa = src; pb = in; p0 = dst; break;
-        case kOpRcs:
-          if (in_d) { pa = src; p0 = mo; s0 = smo; }
-          else { pa = in; sa = tbytes; p0 = src; p1 = mo; s1 = smo; }
-          break;
-        case kOpRrcs: pa = src; pb = in; p0 = src; p1 = mo; s1 = smo; break;
-        case kOpRrs: pa = src; pb = in; p0 = mo; s0 = smo; break;
-        default: kind = 0; break;
+      // (3) publish: slot posted / slot freed / semaphore
+      if (t == 0) {
+        const bool publishes = (send && !ll_out) || recv || op.has_dep;
+        if (publishes) fence_acq_rel(sys);
+        if (send && !ll_out) st_release(cout->head, sent + 1, sys);
+        if (recv) st_release(cin->tail, rcvd + 1, sys);
+        if (op.has_dep) st_release(sems + tb.sem + lane, (epoch << 32) | static_cast<uint64_t>(q + 1), false);
+        stamp(q, 3);
       }
-      if (tbytes <= 0) kind = 0;
+      if (send) ++sent;
+      if (recv) ++rcvd;
     }
-    if (kind != 0) {
-      if (wl == 0) {
-        Desc& d = s_desc[posted & 1];
-        d.a = pa;
-        d.b = pb;
-        d.o0 = p0;
-        d.o1 = p1;
-        d.sa = sa;
-        d.sb = sb;
-        d.s0 = s0;
-        d.s1 = s1;
-        d.nbytes = tbytes;
-        d.src = src;
-        d.dst = dst;
-        d.inl = ll_in ? reinterpret_cast<const uint4*>(in) : nullptr;
-        d.outl = ll_out ? reinterpret_cast<uint4*>(out) : nullptr;
-        d.outd = peer_dst;
-        d.chunk_bytes = chunk_bytes;
-        d.in_flag = static_cast<uint32_t>(rcvd + 1);
-        d.out_flag = static_cast<uint32_t>(sent + 1);
-        d.count = op.count;
-        d.opcode = op.opcode;
-        d.kind = kind;
-        d.step = s;
-        d.tile = tile;
-      }
-      __syncwarp();
-      bar_arrive(1 + (posted & 1));
-      ++posted;
-    }
-    pending = q;
-    pend_send = send;
-    pend_recv = recv;
-    pending_data = kind != 0;
   }
-  // release the data warps
-  if (wl == 0) s_desc[posted & 1].kind = 3;
-  __syncwarp();
-  bar_arrive(1 + (posted & 1));
+  if (t == 0) {  // persistent FIFO counters for the next launch
+    if (has_in) *cin->mine = rcvd;
+    if (has_out) *cout->mine = sent;
+  }
 }
 
 }  // namespace dev

@@ -91,6 +91,8 @@ struct Config {
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
   int trace = 0;                     // record the in-kernel %globaltimer event log
   int direct = 1;                    // write dead receive spans directly (see direct_messages)
+  int unit_warps = 4;                // warps per (thread block, lane) unit
+  int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
 
 Config config_from_env() {
@@ -103,6 +105,8 @@ Config config_from_env() {
   c.timeout_ms = env_int("GC3_TIMEOUT_MS", c.timeout_ms);
   c.trace = static_cast<int>(env_int("GC3_TRACE", 0));
   c.direct = static_cast<int>(env_int("GC3_DIRECT", 1));
+  c.unit_warps = static_cast<int>(env_int("GC3_UNIT_WARPS", c.unit_warps));
+  c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
   return c;
 }
 
@@ -217,6 +221,8 @@ struct RankIR {
   bool has_reduce = false;
   int max_count = 1;
   ArenaLayout lay;
+  std::vector<std::vector<std::vector<uint8_t>>> eff_direct;     // direct flags of this device's launch
+  std::map<std::tuple<int64_t, int, int>, bool> order_ok;         // (tiles, group, slots) -> deadlock-free
   char* arena = nullptr;
   cudaIpcMemHandle_t handle{};
 };
@@ -554,6 +560,23 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       if (plan.ranks[i] == rank) return static_cast<int>(i);
     return -1;
   };
+  {  // the direct flags this launch applies (both ends in it), for the planner's deadlock check
+    std::vector<std::vector<std::vector<uint8_t>>> eff(p.ranks());
+    for (int r = 0; r < p.ranks(); ++r) {
+      eff[r].resize(p.gpus[r].tbs.size());
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+        const ThreadBlock& tb = p.gpus[r].tbs[t];
+        eff[r][t].assign(tb.ops.size(), 0);
+        if (direct.empty() || slot_of(r) < 0) continue;
+        for (size_t s = 0; s < tb.ops.size(); ++s) {
+          const uint8_t f = direct[r][t][s];
+          if ((f & kInDirect) && tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0) eff[r][t][s] |= kInDirect;
+          if ((f & kOutDirect) && tb.send_peer >= 0 && slot_of(tb.send_peer) >= 0) eff[r][t][s] |= kOutDirect;
+        }
+      }
+    }
+    for (int r : plan.ranks) cl->local[r]->irs[id]->eff_direct = eff;
+  }
   std::vector<int> sem_base_of_rank;
   int sem_next = 0;
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
@@ -738,11 +761,84 @@ int select_ir(Comm* c, int coll, size_t count, int dtype) {
   return -1;
 }
 
+// Deadlock check of the kernel's execution order: every thread block walks its lane's tiles in
+// groups of G, op-major inside a group; a non-direct send needs a free slot (FIFO depth `slots`),
+// a receive needs a posted message, a dep needs its (thread block, step, tile) done. Enabling is
+// monotone (only the owner of a connection end consumes it), so one greedy maximal run decides
+// whether the order can deadlock: it completes iff every fair execution does.
+bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std::vector<uint8_t>>>& direct, int64_t tiles,
+                            int G, int slots) {
+  if (tiles <= 0) return true;
+  struct TbRun {
+    int rank, t;
+    int64_t pos = 0;  // ops completed in the thread block's order
+  };
+  std::vector<TbRun> run;
+  std::map<std::tuple<int, int, int>, std::pair<int64_t, int64_t>> conn;  // (src, dst, ch) -> (sent, consumed)
+  std::vector<std::vector<int>> run_of(p.ranks());
+  for (int r = 0; r < p.ranks(); ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      run_of[r].push_back(static_cast<int>(run.size()));
+      run.push_back({r, static_cast<int>(t)});
+    }
+  auto decode = [&](int64_t pos, int nops, int64_t& tile, int& step, int64_t& g0, int& gsize) {
+    const int64_t per_group = static_cast<int64_t>(G) * nops;
+    g0 = pos / per_group * G;
+    gsize = static_cast<int>(std::min<int64_t>(G, tiles - g0));
+    const int64_t in_group = pos - g0 * nops;
+    step = static_cast<int>(in_group / gsize);
+    tile = g0 + in_group % gsize;
+  };
+  auto position = [&](int64_t tile, int step, int nops) {
+    const int64_t g0 = tile / G * G;
+    const int gsize = static_cast<int>(std::min<int64_t>(G, tiles - g0));
+    return g0 * nops + static_cast<int64_t>(step) * gsize + (tile - g0);
+  };
+  for (bool progress = true; progress;) {
+    progress = false;
+    for (TbRun& tr : run) {
+      const ThreadBlock& tb = p.gpus[tr.rank].tbs[tr.t];
+      const int nops = static_cast<int>(tb.ops.size());
+      while (nops > 0 && tr.pos < tiles * nops) {
+        int64_t tile, g0;
+        int step, gsize;
+        decode(tr.pos, nops, tile, step, g0, gsize);
+        const Op& op = tb.ops[step];
+        bool ok = true;
+        for (const Dep& d : op.deps) {
+          const int ti = tb_index(p, tr.rank, d.tb);
+          const int dn = static_cast<int>(p.gpus[tr.rank].tbs[ti].ops.size());
+          if (run[run_of[tr.rank][ti]].pos < position(tile, d.step, dn) + 1) ok = false;
+        }
+        const bool direct_out = !direct.empty() && (direct[tr.rank][tr.t][step] & kOutDirect);
+        if (ok && op_receives(op.op)) {
+          const auto& c = conn[{tb.recv_peer, tr.rank, tb.channel}];
+          if (c.first <= c.second) ok = false;
+        }
+        if (ok && op_sends(op.op) && !direct_out) {
+          const auto& c = conn[{tr.rank, tb.send_peer, tb.channel}];
+          if (c.first - c.second >= slots) ok = false;
+        }
+        if (!ok) break;
+        if (op_receives(op.op)) conn[{tb.recv_peer, tr.rank, tb.channel}].second++;
+        if (op_sends(op.op)) conn[{tr.rank, tb.send_peer, tb.channel}].first++;
+        tr.pos++;
+        progress = true;
+      }
+    }
+  }
+  for (const TbRun& tr : run)
+    if (tr.pos < tiles * static_cast<int64_t>(p.gpus[tr.rank].tbs[tr.t].ops.size())) return false;
+  return true;
+}
+
 struct CallPlan {
   int id = -1;
   bool ll = false;
   int lanes = 1;
   int grid = 0;
+  int unit_warps = 4;
+  int group = 1;
   int64_t chunk_elems = 0, tile_elems = 0, ntiles = 0;  // in kernel element units
   int kesize = 1;                                          // kernel element size
   KernelFn fn = nullptr;
@@ -773,18 +869,26 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (!cp.fn) return set_error(ncclInvalidArgument, "no kernel for dtype %d op %d", dtype, redop);
   auto it = ds.occupancy.find(cp.fn);
   if (it == ds.occupancy.end()) it = ds.occupancy.emplace(cp.fn, interp_blocks_per_sm(cp.fn)).first;
-  const int capacity = it->second * ds.num_sms;
+  // units: `unit_warps` warps interpret one (thread block, lane); all units must be co-resident
+  int uw = c->cfg.unit_warps;
+  if (uw < 1 || uw > kThreads / 32 || (kThreads / 32) % uw) uw = kThreads / 32;
+  const int units_per_block = kThreads / 32 / uw;
+  const int capacity = it->second * ds.num_sms * units_per_block;
   if (capacity < nlocal_tbs)
-    return set_error(ncclInvalidUsage, "%d thread blocks cannot be co-resident (capacity %d)", nlocal_tbs, capacity);
-  int lanes = c->cfg.lanes > 0 ? c->cfg.lanes : std::max(1, (2 * ds.num_sms) / std::max(1, nlocal_tbs));
+    return set_error(ncclInvalidUsage, "%d thread blocks cannot be co-resident (capacity %d units)", nlocal_tbs, capacity);
+  // aim for every resident warp busy: one unit per unit_warps resident warps
+  const int target_units = it->second * ds.num_sms * (kThreads / 32) / uw;
+  int lanes = c->cfg.lanes > 0 ? c->cfg.lanes : std::max(1, target_units / std::max(1, nlocal_tbs));
   lanes = std::min({lanes, ir.lanes, capacity / nlocal_tbs});
   lanes = std::max(lanes, 1);
   int64_t tile_bytes;
   if (c->cfg.tile_bytes > 0) {
     tile_bytes = std::min<int64_t>(c->cfg.tile_bytes / 16 * 16, tile_bytes_cap);
-  } else {
+  } else {  // a few tiles per lane (they pipeline through multi-hop chains), none below 8 KiB per warp
     const int64_t per_lane = (chunk_bytes + lanes - 1) / lanes;
-    tile_bytes = std::min<int64_t>(align_up(static_cast<size_t>(std::max<int64_t>(per_lane, 16)), 16), tile_bytes_cap);
+    const int64_t floor_bytes = static_cast<int64_t>(8 << 10) * uw;
+    tile_bytes = std::min<int64_t>(std::max<int64_t>(per_lane / 4, floor_bytes), tile_bytes_cap);
+    tile_bytes = align_up(static_cast<size_t>(std::max<int64_t>(tile_bytes, 16)), 16);
   }
   tile_bytes = std::max<int64_t>(tile_bytes, 16);
   if (chunk_bytes <= tile_bytes) tile_bytes = chunk_bytes;
@@ -793,7 +897,24 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.ntiles = cp.tile_elems > 0 ? (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems : 0;
   if (cp.ntiles < lanes) lanes = static_cast<int>(std::max<int64_t>(cp.ntiles, 1));
   cp.lanes = lanes;
-  cp.grid = nlocal_tbs * lanes;
+  cp.unit_warps = uw;
+  cp.grid = (nlocal_tbs * lanes + units_per_block - 1) / units_per_block;
+  // op-major tile groups: the largest G (<= tiles of a lane) whose order is deadlock-free here
+  const int64_t max_tiles = cp.ntiles > 0 ? (cp.ntiles + lanes - 1) / lanes : 0;
+  const int64_t min_tiles = cp.ntiles / lanes;
+  int G = c->cfg.group > 0 ? c->cfg.group : static_cast<int>(std::min<int64_t>(std::max<int64_t>(max_tiles, 1), 64));
+  RankIR& mir = *c->irs[id];
+  for (; G > 1; G /= 2) {
+    const auto key = std::make_tuple(max_tiles, G, ir.slots);
+    auto f = mir.order_ok.find(key);
+    if (f == mir.order_ok.end()) {
+      const bool okay = order_is_deadlock_free(p, mir.eff_direct, max_tiles, G, ir.slots) &&
+                        (min_tiles == max_tiles || order_is_deadlock_free(p, mir.eff_direct, min_tiles, G, ir.slots));
+      f = mir.order_ok.emplace(key, okay).first;
+    }
+    if (f->second) break;
+  }
+  cp.group = std::max(G, 1);
   return ncclSuccess;
 }
 
@@ -843,6 +964,8 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.sems = plan.d_sems;
   a.ntbs = plan.ntbs;
   a.lanes = cp.lanes;
+  a.unit_warps = cp.unit_warps;
+  a.group = cp.group;
   a.slots = ir0.slots;
   a.sys_scope = plan.sys_scope ? 1 : 0;
   a.chunk_elems = cp.chunk_elems;
@@ -857,7 +980,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     for (int r : plan.ranks)
       for (const auto& tb : c0->irs[id]->prog.gpus[r].tbs) max_nops = std::max(max_nops, static_cast<int>(tb.ops.size()));
     const int ops_per_block = static_cast<int>(std::min<int64_t>((cp.ntiles + cp.lanes - 1) / cp.lanes * max_nops, 1 << 20));
-    const size_t need = static_cast<size_t>(cp.grid) * ops_per_block * 4 * sizeof(uint64_t);
+    const size_t need = static_cast<size_t>(plan.ntbs) * cp.lanes * ops_per_block * 4 * sizeof(uint64_t);
     DeviceGuard gt(dev);
     if (need > ds->trace_bytes) {
       if (ds->d_trace) cudaFree(ds->d_trace);
@@ -869,7 +992,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     CUDA_TRY(cudaMemsetAsync(ds->d_trace, 0, need, p0.stream));
     a.trace = ds->d_trace;
     a.trace_ops = ops_per_block;
-    ds->trace_grid = cp.grid;
+    ds->trace_grid = plan.ntbs * cp.lanes;
     ds->trace_ops = ops_per_block;
     ds->trace_lanes = cp.lanes;
   }
@@ -1300,6 +1423,8 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "timeout_ms") c.timeout_ms = value;
   else if (k == "trace") c.trace = static_cast<int>(value);
   else if (k == "direct") c.direct = static_cast<int>(value);
+  else if (k == "unit_warps") c.unit_warps = static_cast<int>(value);
+  else if (k == "group") c.group = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
@@ -1341,6 +1466,8 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
   NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1, ntbs, cp));
   info->protocol = cp.ll ? 1 : 0;
   info->lanes = cp.lanes;
+  info->unit_warps = cp.unit_warps;
+  info->group = cp.group;
   info->grid = cp.grid;
   info->local_ranks = nlocal;
   info->slots = ir.slots;
