@@ -267,7 +267,8 @@ def run_gc3(args, cfg):
     if args.quick and rank == 0:
         print(json.dumps({"config": args.config, "bytes": S, "ms": round(ms, 4), "agg_busbw": result["value"],
                           "hbm_frac": result["roofline"]["frac"], "lanes": plan["lanes"], "grid": plan["grid"],
-                          "tile": result["config"]["tile_bytes"], "proto": result["config"]["protocol"]}), flush=True)
+                          "tile": result["config"]["tile_bytes"], "proto": result["config"]["protocol"],
+                          "uw": plan["unit_warps"], "group": plan["group"], "ntiles": plan["ntiles"]}), flush=True)
         for c in comms:
             c.destroy()
         return
