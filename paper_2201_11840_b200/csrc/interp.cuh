@@ -26,7 +26,7 @@
 #include "devplan.hpp"
 
 #ifndef GC3_UNROLL
-#define GC3_UNROLL 4
+#define GC3_UNROLL 8
 #endif
 #ifndef GC3_UNROLL_COPY
 #define GC3_UNROLL_COPY 8

@@ -884,10 +884,10 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   int64_t tile_bytes;
   if (c->cfg.tile_bytes > 0) {
     tile_bytes = std::min<int64_t>(c->cfg.tile_bytes / 16 * 16, tile_bytes_cap);
-  } else {  // a few tiles per lane (they pipeline through multi-hop chains), none below 8 KiB per warp
+  } else {  // one tile per lane when it fits a slot; larger chunks give each lane several tiles,
+            // which pipeline through multi-hop chains in op-major groups
     const int64_t per_lane = (chunk_bytes + lanes - 1) / lanes;
-    const int64_t floor_bytes = static_cast<int64_t>(8 << 10) * uw;
-    tile_bytes = std::min<int64_t>(std::max<int64_t>(per_lane / 4, floor_bytes), tile_bytes_cap);
+    tile_bytes = std::min<int64_t>(std::max<int64_t>(per_lane, 4 << 10), tile_bytes_cap);
     tile_bytes = align_up(static_cast<size_t>(std::max<int64_t>(tile_bytes, 16)), 16);
   }
   tile_bytes = std::max<int64_t>(tile_bytes, 16);
