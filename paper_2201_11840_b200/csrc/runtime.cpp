@@ -575,7 +575,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         }
       }
     }
-    for (int r : plan.ranks) cl->local[r]->irs[id]->eff_direct = eff;
+    for (int r : plan.ranks) {
+      cl->local[r]->irs[id]->eff_direct = eff;
+      cl->local[r]->irs[id]->order_ok.clear();  // verdicts computed without the direct flags
+    }
   }
   std::vector<int> sem_base_of_rank;
   int sem_next = 0;
