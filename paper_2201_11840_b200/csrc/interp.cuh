@@ -55,6 +55,10 @@ __device__ __forceinline__ void fence_acq_rel(bool sys) {
   if (sys) asm volatile("fence.acq_rel.sys;" ::: "memory");
   else asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+__device__ __forceinline__ void st_relaxed(uint64_t* p, uint64_t v, bool sys) {
+  if (sys) asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+  else asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ void st_release(uint64_t* p, uint64_t v, bool sys) {
   if (sys) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
   else asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -547,10 +551,12 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       // (3) publish: slot posted / slot freed / semaphore
       if (t == 0) {
         const bool publishes = (send && !ll_out) || recv || op.has_dep;
+        // one scoped fence orders the unit's data (gathered by the barrier above) before all
+        // three flag stores: a release pattern per flag without a fence per store
         if (publishes) fence_acq_rel(sys);
-        if (send && !ll_out) st_release(cout->head, sent + 1, sys);
-        if (recv) st_release(cin->tail, rcvd + 1, sys);
-        if (op.has_dep) st_release(sems + tb.sem + lane, (epoch << 32) | static_cast<uint64_t>(q + 1), false);
+        if (send && !ll_out) st_relaxed(cout->head, sent + 1, sys);
+        if (recv) st_relaxed(cin->tail, rcvd + 1, sys);
+        if (op.has_dep) st_relaxed(sems + tb.sem + lane, (epoch << 32) | static_cast<uint64_t>(q + 1), false);
         stamp(q, 3);
       }
       if (send) ++sent;

@@ -91,7 +91,7 @@ struct Config {
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
   int trace = 0;                     // record the in-kernel %globaltimer event log
   int direct = 1;                    // write dead receive spans directly (see direct_messages)
-  int unit_warps = 4;                // warps per (thread block, lane) unit
+  int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
 
@@ -874,6 +874,10 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (it == ds.occupancy.end()) it = ds.occupancy.emplace(cp.fn, interp_blocks_per_sm(cp.fn)).first;
   // units: `unit_warps` warps interpret one (thread block, lane); all units must be co-resident
   int uw = c->cfg.unit_warps;
+  if (uw <= 0) {  // automatic: reductions move two operands per element, give them wider units
+    uw = ir.has_reduce ? 8 : 4;
+    while (uw > 1 && it->second * ds.num_sms * (kThreads / 32 / uw) < nlocal_tbs) uw /= 2;
+  }
   if (uw < 1 || uw > kThreads / 32 || (kThreads / 32) % uw) uw = kThreads / 32;
   const int units_per_block = kThreads / 32 / uw;
   const int capacity = it->second * ds.num_sms * units_per_block;
