@@ -159,6 +159,20 @@ ncclResult_t gc3IrValidate(gc3Ir_t ir, int nodes, int gpus_per_node, int max_thr
 ncclResult_t gc3IrCheckSlots(gc3Ir_t ir, int slots, char** violations);
 /* program.hpp:366-419 parallelize(k) as an IR rewrite; returns a new handle */
 ncclResult_t gc3IrReplicate(gc3Ir_t ir, int instances, gc3Ir_t* out);
+/* Host-side plan introspection (used by tests; no CUDA needed):
+ * arena layout of `rank` (FIFO offsets, counter offsets) as JSON — every process computes every
+ * peer's layout from the program text, so this must agree across processes; */
+ncclResult_t gc3IrArenaLayout(gc3Ir_t ir, int rank, int lanes, int slots, int64_t slot_unit, char** json);
+/* [rank][tb][step] flags of the happens-before analysis (1: receive written in place by its sender,
+ * 2: send written into the receiver's span); */
+ncclResult_t gc3IrDirectMessages(gc3Ir_t ir, char** json);
+/* whether the lane order "groups of `group` tiles, op-major" is deadlock-free at FIFO depth `slots`. */
+ncclResult_t gc3IrOrderCheck(gc3Ir_t ir, int64_t tiles, int group, int slots, int* deadlock_free);
+/* Single-node bootstrap all-gather of fixed-size records through /dev/shm keyed by the unique id
+ * (what ncclCommInitRank / gc3RegisterIR use to exchange device info and CUDA IPC handles):
+ * out receives nranks * bytes, rank-major. */
+ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, const void* payload, size_t bytes, void* out,
+                                  int timeout_ms);
 ncclResult_t gc3IrFree(gc3Ir_t ir);
 void gc3Free(void* p);
 

@@ -1556,6 +1556,63 @@ ncclResult_t gc3IrReplicate(gc3Ir_t ir, int instances, gc3Ir_t* out) {
   return ncclSuccess;
 }
 
+ncclResult_t gc3IrArenaLayout(gc3Ir_t ir, int rank, int lanes, int slots, int64_t slot_unit, char** json) {
+  if (!ir || !json || rank < 0 || rank >= ir->p.ranks() || lanes < 1 || slots < 1 || slot_unit < 1) return ncclInvalidArgument;
+  const ArenaLayout a = make_layout(ir->p, rank, lanes, slots, slot_unit);
+  std::ostringstream os;
+  os << "{\"n_in\": " << a.n_in << ", \"n_out\": " << a.n_out << ", \"bytes\": " << a.bytes << ", \"off_head\": " << a.off_head
+     << ", \"off_tail\": " << a.off_tail << ", \"off_mine_in\": " << a.off_mine_in << ", \"off_mine_out\": " << a.off_mine_out
+     << ", \"fifo_off\": [";
+  for (size_t i = 0; i < a.fifo_off.size(); ++i) os << (i ? ", " : "") << a.fifo_off[i];
+  os << "], \"slot_stride\": [";
+  for (size_t i = 0; i < a.slot_stride.size(); ++i) os << (i ? ", " : "") << a.slot_stride[i];
+  os << "]}";
+  *json = dup_cstr(os.str());
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrDirectMessages(gc3Ir_t ir, char** json) {
+  if (!ir || !json) return ncclInvalidArgument;
+  const auto f = direct_messages(ir->p);
+  std::ostringstream os;
+  os << "[";
+  for (size_t r = 0; r < f.size(); ++r) {
+    os << (r ? ", " : "") << "[";
+    for (size_t t = 0; t < f[r].size(); ++t) {
+      os << (t ? ", " : "") << "[";
+      for (size_t s = 0; s < f[r][t].size(); ++s) os << (s ? ", " : "") << static_cast<int>(f[r][t][s]);
+      os << "]";
+    }
+    os << "]";
+  }
+  os << "]";
+  *json = dup_cstr(os.str());
+  return ncclSuccess;
+}
+
+ncclResult_t gc3IrOrderCheck(gc3Ir_t ir, int64_t tiles, int group, int slots, int* deadlock_free) {
+  if (!ir || !deadlock_free || tiles < 0 || group < 1 || slots < 1) return ncclInvalidArgument;
+  *deadlock_free = order_is_deadlock_free(ir->p, {}, tiles, group, slots) ? 1 : 0;
+  return ncclSuccess;
+}
+
+ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, const void* payload, size_t bytes, void* out,
+                                  int timeout_ms) {
+  if (!id || rank < 0 || rank >= nranks || (bytes && (!payload || !out))) return ncclInvalidArgument;
+  if (std::memcmp(id->internal, "GC3", 4) != 0) return set_error(ncclInvalidArgument, "unique id not created by ncclGetUniqueId");
+  const std::string dir = shm_dir(uid_key(*id));
+  const std::string mine(static_cast<const char*>(payload), bytes);
+  if (!post_record(dir, "x.rank" + std::to_string(rank), mine)) return set_error(ncclSystemError, "cannot post bootstrap record");
+  for (int r = 0; r < nranks; ++r) {
+    std::string rec;
+    if (!read_record(dir, "x.rank" + std::to_string(r), rec, timeout_ms))
+      return set_error(ncclSystemError, "timed out waiting for rank %d's bootstrap record", r);
+    if (rec.size() != bytes) return set_error(ncclInvalidUsage, "rank %d posted %zu bytes, expected %zu", r, rec.size(), bytes);
+    std::memcpy(static_cast<char*>(out) + static_cast<size_t>(r) * bytes, rec.data(), bytes);
+  }
+  return ncclSuccess;
+}
+
 ncclResult_t gc3IrFree(gc3Ir_t ir) {
   delete ir;
   return ncclSuccess;

@@ -90,6 +90,10 @@ def lib():
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
         "gc3IrFree": [vp],
+        "gc3IrArenaLayout": [vp, i, i, i, ctypes.c_int64, ctypes.POINTER(vp)],
+        "gc3IrDirectMessages": [vp, ctypes.POINTER(vp)],
+        "gc3IrOrderCheck": [vp, ctypes.c_int64, i, i, ctypes.POINTER(i)],
+        "gc3BootstrapExchange": [ctypes.POINTER(UniqueId), i, i, vp, sz, vp, i],
     }
     for name, args in sigs.items():
         f = getattr(L, name)
@@ -158,6 +162,23 @@ class IR:
         out = ctypes.c_void_p()
         check(lib().gc3IrReplicate(self._h, instances, ctypes.byref(out)))
         return IR._wrap(out)
+
+    def arena_layout(self, rank, lanes, slots, slot_unit):
+        import json
+        out = ctypes.c_void_p()
+        check(lib().gc3IrArenaLayout(self._h, rank, lanes, slots, slot_unit, ctypes.byref(out)))
+        return json.loads(_take(out.value))
+
+    def direct_messages(self):
+        import json
+        out = ctypes.c_void_p()
+        check(lib().gc3IrDirectMessages(self._h, ctypes.byref(out)))
+        return json.loads(_take(out.value))
+
+    def order_deadlock_free(self, tiles, group, slots):
+        ok = ctypes.c_int()
+        check(lib().gc3IrOrderCheck(self._h, tiles, group, slots, ctypes.byref(ok)))
+        return bool(ok.value)
 
     def __del__(self):
         if getattr(self, "_h", None) and _lib is not None:
@@ -264,12 +285,21 @@ def init_all(devices):
 def get_unique_id():
     uid = UniqueId()
     check(lib().ncclGetUniqueId(ctypes.byref(uid)))
-    return bytes(uid.internal)
+    return ctypes.string_at(ctypes.addressof(uid), 128)  # .internal would stop at the first NUL
+
+
+def bootstrap_exchange(uid_bytes, rank, nranks, payload, timeout_ms=60000):
+    """All-gather of equal-size byte records between the ranks of one node (gc3BootstrapExchange)."""
+    uid = UniqueId()
+    ctypes.memmove(ctypes.addressof(uid), uid_bytes, 128)  # attribute assignment stops at a NUL
+    out = ctypes.create_string_buffer(len(payload) * nranks)
+    check(lib().gc3BootstrapExchange(ctypes.byref(uid), rank, nranks, payload, len(payload), out, timeout_ms))
+    return [out.raw[r * len(payload):(r + 1) * len(payload)] for r in range(nranks)]
 
 
 def init_rank(nranks, uid_bytes, rank):
     uid = UniqueId()
-    uid.internal = uid_bytes
+    ctypes.memmove(ctypes.addressof(uid), uid_bytes, 128)  # attribute assignment stops at a NUL
     h = ctypes.c_void_p()
     check(lib().ncclCommInitRank(ctypes.byref(h), nranks, uid, rank))
     return Comm(h.value)
