@@ -86,7 +86,7 @@ struct LaunchArgs {
   int32_t trace_ops;    // ops recorded per unit
   int32_t unit_warps;   // warps interpreting one (thread block, lane); kThreads/32 divisible by it
   int32_t group;        // tiles per op-major group inside a lane (1 = tile-major)
-  int32_t pad_;
+  int32_t tma_stages;   // shared-memory stages per unit for bulk copies (0: register path only)
   char* bufs[kMaxLocalRanks][3];  // per local rank: input, output, scratch
 };
 

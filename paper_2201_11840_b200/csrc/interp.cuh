@@ -287,6 +287,109 @@ __device__ void move(const char* a, const char* b, char* o0, char* o1, int64_t n
     move_elems<R>(a + done, b ? b + done : nullptr, o0 + done, o1 ? o1 + done : nullptr, nbytes - done, red, t, n);
 }
 
+// ------------------------------------------------------------------ TMA bulk copies
+// Pure-copy ops (send, recv, copy, rcs) on the Simple protocol move through shared memory with the
+// Tensor Memory Accelerator's 1-D bulk engine: one thread keeps `stages` x kStageBytes in flight
+// (cp.async.bulk global->shared, completion on an mbarrier; cp.async.bulk shared->global as bulk
+// groups), so the unit's bandwidth no longer depends on registers or resident warps.
+constexpr int kStageBytes = 16 << 10;
+constexpr int kMaxStages = 8;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra WAIT_%=;\n\t}" ::"r"(
+          smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Ops whose data movement is a plain copy (no reduction); recv with the message already in place
+// moves nothing.
+__device__ __forceinline__ bool is_tma_copy(int op, bool in_direct) {
+  return op == kOpSend || op == kOpCopy || op == kOpRcs || (op == kOpRecv && !in_direct);
+}
+
+// Per-unit bulk-copy pipeline state (lives in thread 0 of the unit).
+struct Tma {
+  char* stage;    // stages x kStageBytes of shared memory
+  uint64_t* bar;  // one mbarrier per stage
+  int stages;
+  uint32_t seq;   // pieces issued so far (stage = seq % stages, parity = (seq / stages) & 1)
+};
+
+// Copies `count` segments of `nbytes` (segment j: a + j*sa -> o0 + j*s0 [, o1 + j*s1]).
+// Called by thread 0 of the unit; returns after every store has completed (async-proxy writes
+// ordered for the generic proxy by the caller's fence.proxy.async).
+static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int64_t s0, char* o1, int64_t s1, int64_t nbytes,
+                         int count) {
+  const int64_t per_seg = (nbytes + kStageBytes - 1) / kStageBytes;
+  const int64_t total = per_seg * count;
+  auto piece = [&](int64_t p, const char*& src, char*& d0, char*& d1, uint32_t& bytes) {
+    const int64_t j = p / per_seg, k = p - j * per_seg;
+    const int64_t off = k * kStageBytes;
+    bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kStageBytes), nbytes - off));
+    src = a + j * sa + off;
+    d0 = o0 + j * s0 + off;
+    d1 = o1 ? o1 + j * s1 + off : nullptr;
+  };
+  const uint32_t base = m.seq;
+  const int64_t prime = min(static_cast<int64_t>(m.stages), total);
+  for (int64_t p = 0; p < prime; ++p) {
+    const char* src;
+    char *d0, *d1;
+    uint32_t bytes;
+    piece(p, src, d0, d1, bytes);
+    const uint32_t g = base + static_cast<uint32_t>(p);
+    uint64_t* bar = m.bar + g % m.stages;
+    mbar_expect_tx(bar, bytes);
+    bulk_load(m.stage + static_cast<size_t>(g % m.stages) * kStageBytes, src, bytes, bar);
+  }
+  for (int64_t p = 0; p < total; ++p) {
+    const char* src;
+    char *d0, *d1;
+    uint32_t bytes;
+    piece(p, src, d0, d1, bytes);
+    const uint32_t g = base + static_cast<uint32_t>(p);
+    char* sm = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
+    mbar_wait(m.bar + g % m.stages, (g / m.stages) & 1);
+    bulk_store(d0, sm, bytes);
+    if (d1) bulk_store(d1, sm, bytes);
+    bulk_commit();
+    const int64_t np = p + m.stages;
+    if (np < total) {  // refill this stage once the store has read it
+      bulk_wait_read_all();
+      const char* nsrc;
+      char *n0, *n1;
+      uint32_t nbytes_p;
+      piece(np, nsrc, n0, n1, nbytes_p);
+      uint64_t* bar = m.bar + g % m.stages;
+      mbar_expect_tx(bar, nbytes_p);
+      bulk_load(sm, nsrc, nbytes_p, bar);
+    }
+  }
+  bulk_wait_all();
+  m.seq = base + static_cast<uint32_t>(total);
+}
+
 // ------------------------------------------------------------------ watchdog
 // Everything here is passed by value: taking the address of a kernel parameter would force the
 // whole LaunchArgs into local memory.
@@ -434,6 +537,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int lanes = a.lanes;
   if (unit >= a.ntbs * lanes) return;  // a whole unit leaves together
   const int bar_id = 1 + uib;
+  // TMA staging: a.tma_stages x kStageBytes of dynamic shared memory per unit, one mbarrier each
+  extern __shared__ __align__(128) char s_stage[];
+  __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * kStageBytes, s_bar[uib], a.tma_stages, 0};
+  if (t == 0 && a.tma_stages > 0) {
+    for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   const int lane = unit % lanes;
   const int tbi = unit / lanes;
   const DevTb tb = a.tbs[tbi];
@@ -521,6 +632,26 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         ok = ll_op<R>(op.opcode, op.count, src, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
                       ll_out ? reinterpret_cast<uint4*>(out) : nullptr, peer_dst, static_cast<uint32_t>(rcvd + 1),
                       static_cast<uint32_t>(sent + 1), c, t, n);
+      } else if (tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
+                 ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
+                   reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(peer_dst) | static_cast<uintptr_t>(tbytes) |
+                   static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
+        if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier
+          char* mo = out_d ? peer_dst : out;
+          const int64_t smo = out_d ? chunk_bytes : tbytes;
+          fence_proxy_async_global();  // generic-proxy acquires above -> async-proxy reads
+          switch (op.opcode) {
+            case kOpSend: tma_copy(tma, src, chunk_bytes, mo, smo, nullptr, 0, tbytes, op.count); break;
+            case kOpRecv: tma_copy(tma, in, tbytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
+            case kOpCopy: tma_copy(tma, src, chunk_bytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
+            case kOpRcs:
+              if (in_d) tma_copy(tma, src, chunk_bytes, mo, smo, nullptr, 0, tbytes, op.count);
+              else tma_copy(tma, in, tbytes, src, chunk_bytes, mo, smo, tbytes, op.count);
+              break;
+            default: break;
+          }
+          fence_proxy_async_global();  // async-proxy writes -> the generic release below
+        }
       } else {
         for (int j = 0; j < op.count; ++j) {
           char* sj = src + j * chunk_bytes;

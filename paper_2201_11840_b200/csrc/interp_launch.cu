@@ -3,6 +3,9 @@
 // parallel); the kernel itself is in interp.cuh.
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+
 #include "devplan.hpp"
 
 namespace gc3 {
@@ -13,6 +16,8 @@ KernelFn interp_kernel_sum(int dtype, bool ll);
 KernelFn interp_kernel_prod(int dtype, bool ll);
 KernelFn interp_kernel_max(int dtype, bool ll);
 KernelFn interp_kernel_min(int dtype, bool ll);
+
+constexpr int kMaxDynamicSmem = 200 << 10;  // TMA staging budget per block
 
 // dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs.
 KernelFn interp_kernel(int dtype, int redop, bool ll) {
@@ -26,14 +31,29 @@ KernelFn interp_kernel(int dtype, int redop, bool ll) {
   }
 }
 
-cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, cudaStream_t stream) {
-  void* params[] = {const_cast<LaunchArgs*>(&args)};
-  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kThreads), params, 0, stream);
+static cudaError_t allow_smem(KernelFn fn) {
+  static std::mutex mu;
+  static std::set<std::pair<int, KernelFn>> done;  // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({dev, fn})) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(reinterpret_cast<const void*>(fn), cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynamicSmem);
+  if (e == cudaSuccess) done.insert({dev, fn});
+  return e;
 }
 
-int interp_blocks_per_sm(KernelFn fn) {
+cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, size_t smem, cudaStream_t stream) {
+  const cudaError_t e = allow_smem(fn);
+  if (e != cudaSuccess) return e;
+  void* params[] = {const_cast<LaunchArgs*>(&args)};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(fn), dim3(grid), dim3(kThreads), params, smem, stream);
+}
+
+int interp_blocks_per_sm(KernelFn fn, size_t smem) {
+  if (allow_smem(fn) != cudaSuccess) return 0;
   int n = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), kThreads, 0) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, reinterpret_cast<const void*>(fn), kThreads, smem) != cudaSuccess) return 0;
   return n;
 }
 

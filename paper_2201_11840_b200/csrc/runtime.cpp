@@ -42,8 +42,11 @@ namespace gc3 {
 
 using KernelFn = void (*)(LaunchArgs);
 KernelFn interp_kernel(int dtype, int redop, bool ll);
-cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, cudaStream_t stream);
-int interp_blocks_per_sm(KernelFn fn);
+cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, size_t smem, cudaStream_t stream);
+int interp_blocks_per_sm(KernelFn fn, size_t smem);
+constexpr int kStageBytesHost = 16 << 10;  // interp.cuh kStageBytes
+constexpr int kMaxStagesHost = 8;          // interp.cuh kMaxStages
+constexpr int kSmemBudget = 192 << 10;
 
 namespace {
 
@@ -92,6 +95,7 @@ struct Config {
   int trace = 0;                     // record the in-kernel %globaltimer event log
   int direct = 1;                    // write dead receive spans directly (see direct_messages)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
+  int tma = 1;                       // bulk (TMA) copies for pure-copy ops on same-device peers
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
 
@@ -107,6 +111,7 @@ Config config_from_env() {
   c.direct = static_cast<int>(env_int("GC3_DIRECT", 1));
   c.unit_warps = static_cast<int>(env_int("GC3_UNIT_WARPS", c.unit_warps));
   c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
+  c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
   return c;
 }
 
@@ -248,7 +253,7 @@ struct DeviceState {
   uint64_t* d_err = nullptr;
   std::vector<DevicePlan> plans;  // by ir id
   int num_sms = 0;
-  std::map<KernelFn, int> occupancy;
+  std::map<std::pair<KernelFn, size_t>, int> occupancy;  // (kernel, dynamic smem) -> blocks per SM
   uint64_t* d_trace = nullptr;  // event log of the last traced launch
   size_t trace_bytes = 0;
   int trace_grid = 0, trace_ops = 0, trace_lanes = 0;
@@ -842,13 +847,16 @@ struct CallPlan {
   int grid = 0;
   int unit_warps = 4;
   int group = 1;
+  int tma_stages = 0;
+  size_t smem = 0;
   int64_t chunk_elems = 0, tile_elems = 0, ntiles = 0;  // in kernel element units
   int kesize = 1;                                          // kernel element size
   KernelFn fn = nullptr;
   int redop = -1;
 };
 
-ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count, int dtype, int redop, int nlocal_tbs, CallPlan& cp) {
+ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count, int dtype, int redop, int nlocal_tbs, bool sys_scope,
+                       CallPlan& cp) {
   const RankIR& ir = *c->irs[id];
   const Program& p = ir.prog;
   const size_t esize = dtype_size(dtype);
@@ -870,21 +878,35 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot unit too small");
   cp.fn = interp_kernel(cp.redop < 0 ? 0 : dtype, cp.redop, cp.ll);
   if (!cp.fn) return set_error(ncclInvalidArgument, "no kernel for dtype %d op %d", dtype, redop);
-  auto it = ds.occupancy.find(cp.fn);
-  if (it == ds.occupancy.end()) it = ds.occupancy.emplace(cp.fn, interp_blocks_per_sm(cp.fn)).first;
+  auto occupancy = [&](size_t smem) {
+    auto f = ds.occupancy.find({cp.fn, smem});
+    if (f == ds.occupancy.end()) f = ds.occupancy.emplace(std::make_pair(cp.fn, smem), interp_blocks_per_sm(cp.fn, smem)).first;
+    return f->second;
+  };
+  const int bps_plain = occupancy(0);
   // units: `unit_warps` warps interpret one (thread block, lane); all units must be co-resident
   int uw = c->cfg.unit_warps;
   if (uw <= 0) {  // automatic: reductions move two operands per element, give them wider units
     uw = ir.has_reduce ? 8 : 4;
-    while (uw > 1 && it->second * ds.num_sms * (kThreads / 32 / uw) < nlocal_tbs) uw /= 2;
+    while (uw > 1 && bps_plain * ds.num_sms * (kThreads / 32 / uw) < nlocal_tbs) uw /= 2;
   }
   if (uw < 1 || uw > kThreads / 32 || (kThreads / 32) % uw) uw = kThreads / 32;
   const int units_per_block = kThreads / 32 / uw;
-  const int capacity = it->second * ds.num_sms * units_per_block;
+  // TMA staging for pure-copy ops (same-device peers; shared-memory stages per unit)
+  cp.tma_stages = 0;
+  if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, kSmemBudget / (units_per_block * kStageBytesHost));
+  cp.smem = static_cast<size_t>(units_per_block) * cp.tma_stages * kStageBytesHost;
+  int bps = occupancy(cp.smem);
+  if (bps * ds.num_sms * units_per_block < nlocal_tbs && cp.smem) {  // staging would break co-residency
+    cp.tma_stages = 0;
+    cp.smem = 0;
+    bps = bps_plain;
+  }
+  const int capacity = bps * ds.num_sms * units_per_block;
   if (capacity < nlocal_tbs)
     return set_error(ncclInvalidUsage, "%d thread blocks cannot be co-resident (capacity %d units)", nlocal_tbs, capacity);
   // aim for every resident warp busy: one unit per unit_warps resident warps
-  const int target_units = it->second * ds.num_sms * (kThreads / 32) / uw;
+  const int target_units = bps * ds.num_sms * (kThreads / 32) / uw;
   int lanes = c->cfg.lanes > 0 ? c->cfg.lanes : std::max(1, target_units / std::max(1, nlocal_tbs));
   lanes = std::min({lanes, ir.lanes, capacity / nlocal_tbs});
   lanes = std::max(lanes, 1);
@@ -958,7 +980,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     return set_error(ncclInvalidUsage, "all %zu ranks hosted on device %d must issue the collective in one group (got %zu)",
                      plan.ranks.size(), dev, ops.size());
   CallPlan cp;
-  NCCL_TRY(plan_call(c0, *ds, id, p0.coll, p0.count, p0.dtype, p0.redop, plan.ntbs, cp));
+  NCCL_TRY(plan_call(c0, *ds, id, p0.coll, p0.count, p0.dtype, p0.redop, plan.ntbs, plan.sys_scope, cp));
   const RankIR& ir0 = *c0->irs[id];
   const size_t esize = dtype_size(p0.dtype);
   const int64_t chunk_bytes = cp.chunk_elems * cp.kesize;
@@ -973,6 +995,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.lanes = cp.lanes;
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
+  a.tma_stages = cp.tma_stages;
   a.slots = ir0.slots;
   a.sys_scope = plan.sys_scope ? 1 : 0;
   a.chunk_elems = cp.chunk_elems;
@@ -1057,7 +1080,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][1] = out;
     a.bufs[slot][2] = c->scratch;
   }
-  CUDA_TRY(interp_launch(cp.fn, a, cp.grid, stream));
+  CUDA_TRY(interp_launch(cp.fn, a, cp.grid, cp.smem, stream));
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
     if (p0.coll != kReduceScatter) continue;
     Pending* q = nullptr;
@@ -1432,6 +1455,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "direct") c.direct = static_cast<int>(value);
   else if (k == "unit_warps") c.unit_warps = static_cast<int>(value);
   else if (k == "group") c.group = static_cast<int>(value);
+  else if (k == "tma") c.tma = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
@@ -1470,7 +1494,7 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
       ++nlocal;
     }
   CallPlan cp;
-  NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1, ntbs, cp));
+  NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1, ntbs, false, cp));
   info->protocol = cp.ll ? 1 : 0;
   info->lanes = cp.lanes;
   info->unit_warps = cp.unit_warps;
