@@ -41,7 +41,7 @@ struct DevDep {
   int32_t sem;   // semaphore base index of the depended-on thread block (lane is added)
   int32_t step;  // depended-on step
   int32_t nops;  // op count of the depended-on thread block (progress encoding)
-  int32_t pad;
+  int32_t mult;  // lane multiplier of the depended-on thread block (it has lanes x mult lanes)
 };
 
 struct DevTb {
@@ -52,6 +52,8 @@ struct DevTb {
   int32_t chan_in;    // receive-side channel base index (x lanes), -1 if none
   int32_t chan_out;   // send-side channel base index (x lanes), -1 if none
   int32_t peer_slot;  // rank slot of the send peer when it runs in the same launch, else -1
+  int32_t mult;       // lane multiplier: this thread block runs lanes x mult lanes (work balance)
+  int32_t unit_base;  // sum of the multipliers of the launch's earlier thread blocks
   int32_t pad;
 };
 
@@ -72,6 +74,7 @@ struct LaunchArgs {
   const DevChan* chans;
   uint64_t* sems;
   int32_t ntbs;
+  int32_t weight;       // sum of the thread blocks' lane multipliers: units = lanes x weight
   int32_t lanes;
   int32_t slots;
   int32_t sys_scope;    // 1: peers on other GPUs (NVLink, .sys fences); 0: same-device loopback

@@ -534,8 +534,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int uib = threadIdx.x / n;               // unit in this block
   const int t = threadIdx.x - uib * n;           // thread in unit
   const int unit = blockIdx.x * (kThreads / n) + uib;
-  const int lanes = a.lanes;
-  if (unit >= a.ntbs * lanes) return;  // a whole unit leaves together
+  const int L0 = a.lanes;  // base lanes; thread block i runs L0 x mult_i lanes
+  if (unit >= a.weight * L0) return;  // a whole unit leaves together
   const int bar_id = 1 + uib;
   // TMA staging: a.tma_stages x kStageBytes of dynamic shared memory per unit, one mbarrier each
   extern __shared__ __align__(128) char s_stage[];
@@ -545,9 +545,17 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
     for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  const int lane = unit % lanes;
-  const int tbi = unit / lanes;
+  // unit -> thread block: thread block i owns units [L0 * unit_base_i, L0 * (unit_base_i + mult_i))
+  int tbi = 0;
+  for (int lo = 0, hi = a.ntbs - 1; lo < hi;) {
+    const int mid = (lo + hi + 1) / 2;
+    if (a.tbs[mid].unit_base * L0 <= unit) lo = mid;
+    else hi = mid - 1;
+    tbi = lo;
+  }
   const DevTb tb = a.tbs[tbi];
+  const int lanes = L0 * tb.mult;
+  const int lane = unit - tb.unit_base * L0;
   const bool sys = a.sys_scope != 0;
   const bool has_in = tb.chan_in >= 0, has_out = tb.chan_out >= 0;
   const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
@@ -614,8 +622,16 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       if (t == 1 && recv && !ll_in) ok = wait_geq(cin->head, rcvd + 1, sys, c, 3);
       for (int d = t - 2; d >= 0 && d < op.ndeps; d += n - 2) {
         const DevDep dd = a.deps[op.dep_begin + d];
-        const uint64_t target = (epoch << 32) | static_cast<uint64_t>(g0 * dd.nops + static_cast<int64_t>(dd.step) * gsize + jj + 1);
-        ok = ok && wait_geq(sems + dd.sem + lane, target, false, c, 1);
+        // the depended-on thread block may run a different lane count: find the lane that owns this
+        // tile there and the tile's position in that lane's order
+        const int ld_lanes = L0 * dd.mult;
+        const int dl = static_cast<int>(tile % ld_lanes);
+        const int64_t di = tile / ld_lanes;
+        const int64_t dn = (ntiles - 1 - dl) / ld_lanes + 1;
+        const int64_t dg0 = di / G * G;
+        const int64_t dgs = min(static_cast<int64_t>(G), dn - dg0);
+        const uint64_t target = (epoch << 32) | static_cast<uint64_t>(dg0 * dd.nops + static_cast<int64_t>(dd.step) * dgs + (di - dg0) + 1);
+        ok = ok && wait_geq(sems + dd.sem + dl, target, false, c, 1);
       }
       if (!unit_and(ok, uw, bar_id, n)) return;
       if (t == 0) stamp(q, 1);

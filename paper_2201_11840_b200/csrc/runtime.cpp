@@ -25,6 +25,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -96,6 +97,7 @@ struct Config {
   int direct = 1;                    // write dead receive spans directly (see direct_messages)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
   int tma = 1;                       // bulk (TMA) copies for pure-copy ops on same-device peers
+  int balance = 1;                   // per-component lane multipliers (lane_multipliers)
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
 
@@ -112,6 +114,7 @@ Config config_from_env() {
   c.unit_warps = static_cast<int>(env_int("GC3_UNIT_WARPS", c.unit_warps));
   c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
   c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
+  c.balance = static_cast<int>(env_int("GC3_BALANCE", c.balance));
   return c;
 }
 
@@ -179,19 +182,25 @@ struct ArenaLayout {
   std::vector<int> in_index, out_index;  // per tb: index among receiving / sending tbs, or -1
   std::vector<size_t> fifo_off;          // per receiving tb: offset of its FIFOs (lanes x slots)
   std::vector<int64_t> slot_stride;      // per receiving tb: bytes of one slot = unit x max count
+  std::vector<int> in_lane_base;         // per receiving tb: index of its first lane's head / counter
+  std::vector<int> out_lane_base;        // per sending tb: index of its first lane's tail / counter
   int n_in = 0, n_out = 0;
   size_t off_head = 0, off_tail = 0, off_mine_in = 0, off_mine_out = 0, bytes = 0;
 };
 
 // FIFO slots are sized per connection: one slot holds a message of `count` tiles, each at most
 // `unit` bytes, so the tile size does not shrink with the aggregation count.
-ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_t unit) {
+// Thread block t of `rank` runs lanes x mult[rank][t] lanes (work balance, see lane_multipliers);
+// `lane_base` gives each receiving / sending thread block's first lane in the counter arrays.
+ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_t unit, const std::vector<std::vector<int>>& mult) {
   ArenaLayout a;
   const Gpu& g = p.gpus[rank];
   a.in_index.assign(g.tbs.size(), -1);
   a.out_index.assign(g.tbs.size(), -1);
   size_t off = 0;
+  int in_lanes = 0, out_lanes = 0;
   for (size_t t = 0; t < g.tbs.size(); ++t) {
+    const int lt = lanes * (mult.empty() ? 1 : mult[rank][t]);
     if (g.tbs[t].recv_peer >= 0) {
       a.in_index[t] = a.n_in++;
       int maxc = 1;
@@ -199,19 +208,25 @@ ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_
         if (op_receives(op.op)) maxc = std::max(maxc, op.count);
       a.fifo_off.push_back(off);
       a.slot_stride.push_back(unit * maxc);
-      off += static_cast<size_t>(lanes) * slots * unit * maxc;
+      a.in_lane_base.push_back(in_lanes);
+      in_lanes += lt;
+      off += static_cast<size_t>(lt) * slots * unit * maxc;
     }
-    if (g.tbs[t].send_peer >= 0) a.out_index[t] = a.n_out++;
+    if (g.tbs[t].send_peer >= 0) {
+      a.out_index[t] = a.n_out++;
+      a.out_lane_base.push_back(out_lanes);
+      out_lanes += lt;
+    }
   }
   off = align_up(off, 256);
   a.off_head = off;
-  off += static_cast<size_t>(a.n_in) * lanes * kCounterStride;
+  off += static_cast<size_t>(in_lanes) * kCounterStride;
   a.off_tail = off;
-  off += static_cast<size_t>(a.n_out) * lanes * kCounterStride;
+  off += static_cast<size_t>(out_lanes) * kCounterStride;
   a.off_mine_in = off;
-  off += static_cast<size_t>(a.n_in) * lanes * 8;
+  off += static_cast<size_t>(in_lanes) * 8;
   a.off_mine_out = off;
-  off += static_cast<size_t>(a.n_out) * lanes * 8;
+  off += static_cast<size_t>(out_lanes) * 8;
   a.bytes = align_up(std::max<size_t>(off, 256), 256);
   return a;
 }
@@ -225,9 +240,10 @@ struct RankIR {
   int lanes = 1;  // lanes provisioned in the arena
   bool has_reduce = false;
   int max_count = 1;
+  std::vector<std::vector<int>> mult;  // lane multiplier per (rank, tb) (lane_multipliers)
   ArenaLayout lay;
   std::vector<std::vector<std::vector<uint8_t>>> eff_direct;     // direct flags of this device's launch
-  std::map<std::tuple<int64_t, int, int>, bool> order_ok;         // (tiles, group, slots) -> deadlock-free
+  std::map<std::tuple<int64_t, int, int, int>, bool> order_ok;    // (tiles, lanes, group, slots) -> deadlock-free
   char* arena = nullptr;
   cudaIpcMemHandle_t handle{};
 };
@@ -237,6 +253,7 @@ struct DevicePlan {  // one registered IR on one device
   bool built = false;
   std::vector<int> ranks;  // local ranks in launch order (rank_slot -> rank)
   int ntbs = 0;
+  int weight = 0;          // sum of lane multipliers: units = lanes x weight
   DevTb* d_tbs = nullptr;
   DevOp* d_ops = nullptr;
   DevDep* d_deps = nullptr;
@@ -535,6 +552,58 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p)
   return flags;
 }
 
+// Work balance. Thread blocks joined by FIFO connections must run the same number of lanes (lane
+// l of a sender talks to lane l of its receiver), but separate components need not: a component
+// whose thread blocks move more bytes per tile (e.g. the coalesced count-G exchange of the two-step
+// AllToAll) gets proportionally more lanes. Weight of a thread block = chunk
+// passes its units make per tile (a direct receive moves nothing; its sender does the writing).
+std::vector<std::vector<int>> lane_multipliers(const Program& p) {
+  const int R = p.ranks();
+  const auto direct = direct_messages(p);
+  std::vector<int> base(R + 1, 0);
+  for (int r = 0; r < R; ++r) base[r + 1] = base[r] + static_cast<int>(p.gpus[r].tbs.size());
+  std::vector<int> parent(base[R]);
+  for (int i = 0; i < base[R]; ++i) parent[i] = i;
+  std::function<int(int)> find = [&](int x) { return parent[x] == x ? x : parent[x] = find(parent[x]); };
+  std::vector<int> weight(base[R], 0);
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      if (tb.send_peer >= 0 && tb.send_peer < R) {
+        const int rt = find_receiver(p, r, tb.send_peer, tb.channel);
+        if (rt >= 0) parent[find(base[r] + static_cast<int>(t))] = find(base[tb.send_peer] + rt);
+      }
+      int w = 0;
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        const Op& op = tb.ops[s];
+        const bool in_d = !direct.empty() && (direct[r][t][s] & kInDirect);
+        int passes = 0;
+        switch (op.op) {
+          case Opcode::send: case Opcode::copy: passes = 2; break;
+          case Opcode::recv: passes = in_d ? 0 : 2; break;
+          case Opcode::reduce: case Opcode::rrc: case Opcode::rrs: passes = 3; break;
+          case Opcode::rcs: passes = in_d ? 2 : 3; break;
+          case Opcode::rrcs: passes = 4; break;
+          default: break;
+        }
+        w += passes * op.count;
+      }
+      weight[base[r] + static_cast<int>(t)] = w;
+    }
+  std::map<int, int> comp_w;
+  for (int i = 0; i < base[R]; ++i) comp_w[find(i)] = std::max(comp_w[find(i)], weight[i]);
+  int wmin = 0;
+  for (const auto& [root, w] : comp_w)
+    if (w > 0 && (wmin == 0 || w < wmin)) wmin = w;
+  std::vector<std::vector<int>> mult(R);
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const int w = comp_w[find(base[r] + static_cast<int>(t))];
+      mult[r].push_back(wmin > 0 ? std::max(1, std::min(4, (w + wmin / 2) / wmin)) : 1);
+    }
+  return mult;
+}
+
 ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   if (ds.plans.size() <= static_cast<size_t>(id)) ds.plans.resize(id + 1);
   DevicePlan& plan = ds.plans[id];
@@ -585,11 +654,16 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       cl->local[r]->irs[id]->order_ok.clear();  // verdicts computed without the direct flags
     }
   }
-  std::vector<int> sem_base_of_rank;
-  int sem_next = 0;
+  // semaphores: lanes x mult per thread block, in launch order
+  const auto& mult = ir0.mult;
+  std::map<std::pair<int, int>, int> sem_base;  // (rank, tb index) -> first semaphore
+  int sem_next = 0, weight = 0;
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
-    sem_base_of_rank.push_back(sem_next);
-    sem_next += static_cast<int>(p.gpus[plan.ranks[slot]].tbs.size()) * L;
+    const int r = plan.ranks[slot];
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      sem_base[{r, static_cast<int>(t)}] = sem_next;
+      sem_next += L * mult[r][t];
+    }
   }
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
     const int r = plan.ranks[slot];
@@ -598,11 +672,15 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
     const Gpu& g = p.gpus[r];
     for (size_t t = 0; t < g.tbs.size(); ++t) {
       const ThreadBlock& tb = g.tbs[t];
+      const int Lt = L * mult[r][t];
       DevTb d{};
       d.rank_slot = static_cast<int>(slot);
       d.op_begin = static_cast<int>(ops.size());
       d.nops = static_cast<int>(tb.ops.size());
-      d.sem = sem_base_of_rank[slot] + static_cast<int>(t) * L;
+      d.sem = sem_base[{r, static_cast<int>(t)}];
+      d.mult = mult[r][t];
+      d.unit_base = weight;
+      weight += mult[r][t];
       d.chan_in = d.chan_out = -1;
       d.peer_slot = tb.send_peer >= 0 ? slot_of(tb.send_peer) : -1;
       const bool in_local = tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0;
@@ -627,9 +705,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
           const int ti = tb_index(p, r, dp.tb);
           if (ti < 0) return set_error(ncclInvalidArgument, "IR dep on unknown tb %d", dp.tb);
           DevDep dd{};
-          dd.sem = sem_base_of_rank[slot] + ti * L;
+          dd.sem = sem_base[{r, ti}];
           dd.step = dp.step;
           dd.nops = static_cast<int>(g.tbs[ti].ops.size());
+          dd.mult = mult[r][ti];
           deps.push_back(dd);
         }
         ops.push_back(o);
@@ -642,16 +721,17 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         NCCL_TRY(peer_arena(c, id, s, sender_arena));
         if (!cl->local[s] || cl->local[s]->device != c->device) plan.sys_scope = true;
         const int k = ir.lay.in_index[t];
-        const ArenaLayout slay = make_layout(p, s, L, ir.slots, ir.slot_bytes);
+        const ArenaLayout slay = make_layout(p, s, L, ir.slots, ir.slot_bytes, mult);
         const int m = slay.out_index[st];
+        const size_t kb = ir.lay.in_lane_base[k], mb = slay.out_lane_base[m];
         d.chan_in = static_cast<int>(chans.size());
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < Lt; ++l) {
           DevChan ch{};
           ch.fifo = ir.arena + ir.lay.fifo_off[k] + static_cast<size_t>(l) * ir.slots * ir.lay.slot_stride[k];
           ch.slot_bytes = ir.lay.slot_stride[k];
-          ch.head = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_head + (static_cast<size_t>(k) * L + l) * kCounterStride);
-          ch.tail = reinterpret_cast<uint64_t*>(sender_arena + slay.off_tail + (static_cast<size_t>(m) * L + l) * kCounterStride);
-          ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_in + (static_cast<size_t>(k) * L + l) * 8);
+          ch.head = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_head + (kb + l) * kCounterStride);
+          ch.tail = reinterpret_cast<uint64_t*>(sender_arena + slay.off_tail + (mb + l) * kCounterStride);
+          ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_in + (kb + l) * 8);
           chans.push_back(ch);
         }
       }
@@ -662,17 +742,18 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         char* recv_arena = nullptr;
         NCCL_TRY(peer_arena(c, id, dst, recv_arena));
         if (!cl->local[dst] || cl->local[dst]->device != c->device) plan.sys_scope = true;
-        const ArenaLayout rlay = make_layout(p, dst, L, ir.slots, ir.slot_bytes);
+        const ArenaLayout rlay = make_layout(p, dst, L, ir.slots, ir.slot_bytes, mult);
         const int k = rlay.in_index[rt];
         const int m = ir.lay.out_index[t];
+        const size_t kb = rlay.in_lane_base[k], mb = ir.lay.out_lane_base[m];
         d.chan_out = static_cast<int>(chans.size());
-        for (int l = 0; l < L; ++l) {
+        for (int l = 0; l < Lt; ++l) {
           DevChan ch{};
           ch.fifo = recv_arena + rlay.fifo_off[k] + static_cast<size_t>(l) * ir.slots * rlay.slot_stride[k];
           ch.slot_bytes = rlay.slot_stride[k];
-          ch.head = reinterpret_cast<uint64_t*>(recv_arena + rlay.off_head + (static_cast<size_t>(k) * L + l) * kCounterStride);
-          ch.tail = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_tail + (static_cast<size_t>(m) * L + l) * kCounterStride);
-          ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_out + (static_cast<size_t>(m) * L + l) * 8);
+          ch.head = reinterpret_cast<uint64_t*>(recv_arena + rlay.off_head + (kb + l) * kCounterStride);
+          ch.tail = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_tail + (mb + l) * kCounterStride);
+          ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_out + (mb + l) * 8);
           chans.push_back(ch);
         }
       }
@@ -697,6 +778,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   CUDA_TRY(cudaMalloc(&plan.d_sems, nsem * sizeof(uint64_t)));
   CUDA_TRY(cudaMemset(plan.d_sems, 0, nsem * sizeof(uint64_t)));
   plan.ntbs = static_cast<int>(tbs.size());
+  plan.weight = weight;
   plan.built = true;
   return ncclSuccess;
 }
@@ -774,69 +856,66 @@ int select_ir(Comm* c, int coll, size_t count, int dtype) {
 // a receive needs a posted message, a dep needs its (thread block, step, tile) done. Enabling is
 // monotone (only the owner of a connection end consumes it), so one greedy maximal run decides
 // whether the order can deadlock: it completes iff every fair execution does.
-bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std::vector<uint8_t>>>& direct, int64_t tiles,
-                            int G, int slots) {
-  if (tiles <= 0) return true;
-  struct TbRun {
-    int rank, t;
-    int64_t pos = 0;  // ops completed in the thread block's order
+bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std::vector<uint8_t>>>& direct, int64_t ntiles,
+                            int lanes, const std::vector<std::vector<int>>& mult, int G, int slots) {
+  if (ntiles <= 0) return true;
+  struct Unit {
+    int r, t, lane, lt;
+    int64_t ntl;      // tiles of this lane
+    int64_t pos = 0;  // ops completed in the lane's order
   };
-  std::vector<TbRun> run;
-  std::map<std::tuple<int, int, int>, std::pair<int64_t, int64_t>> conn;  // (src, dst, ch) -> (sent, consumed)
-  std::vector<std::vector<int>> run_of(p.ranks());
+  std::vector<Unit> units;
+  std::map<std::pair<int, int>, int> first;  // (rank, tb) -> its lane-0 unit
   for (int r = 0; r < p.ranks(); ++r)
     for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
-      run_of[r].push_back(static_cast<int>(run.size()));
-      run.push_back({r, static_cast<int>(t)});
+      const int lt = lanes * (mult.empty() ? 1 : mult[r][t]);
+      first[{r, static_cast<int>(t)}] = static_cast<int>(units.size());
+      for (int l = 0; l < lt; ++l) units.push_back({r, static_cast<int>(t), l, lt, ntiles > l ? (ntiles - 1 - l) / lt + 1 : 0});
     }
-  auto decode = [&](int64_t pos, int nops, int64_t& tile, int& step, int64_t& g0, int& gsize) {
-    const int64_t per_group = static_cast<int64_t>(G) * nops;
-    g0 = pos / per_group * G;
-    gsize = static_cast<int>(std::min<int64_t>(G, tiles - g0));
-    const int64_t in_group = pos - g0 * nops;
-    step = static_cast<int>(in_group / gsize);
-    tile = g0 + in_group % gsize;
+  auto position = [&](int64_t i, int step, int nops, int64_t ntl) {
+    const int64_t g0 = i / G * G;
+    const int64_t gsize = std::min<int64_t>(G, ntl - g0);
+    return g0 * nops + step * gsize + (i - g0);
   };
-  auto position = [&](int64_t tile, int step, int nops) {
-    const int64_t g0 = tile / G * G;
-    const int gsize = static_cast<int>(std::min<int64_t>(G, tiles - g0));
-    return g0 * nops + static_cast<int64_t>(step) * gsize + (tile - g0);
-  };
+  std::map<std::tuple<int, int, int, int>, std::pair<int64_t, int64_t>> conn;  // (src, dst, ch, lane) -> (sent, consumed)
   for (bool progress = true; progress;) {
     progress = false;
-    for (TbRun& tr : run) {
-      const ThreadBlock& tb = p.gpus[tr.rank].tbs[tr.t];
+    for (Unit& u : units) {
+      const ThreadBlock& tb = p.gpus[u.r].tbs[u.t];
       const int nops = static_cast<int>(tb.ops.size());
-      while (nops > 0 && tr.pos < tiles * nops) {
-        int64_t tile, g0;
-        int step, gsize;
-        decode(tr.pos, nops, tile, step, g0, gsize);
+      while (nops > 0 && u.pos < u.ntl * nops) {
+        const int64_t g0 = u.pos / (static_cast<int64_t>(G) * nops) * G;
+        const int64_t gsize = std::min<int64_t>(G, u.ntl - g0);
+        const int64_t in_group = u.pos - g0 * nops;
+        const int step = static_cast<int>(in_group / gsize);
+        const int64_t tile = u.lane + (g0 + in_group % gsize) * u.lt;
         const Op& op = tb.ops[step];
         bool ok = true;
         for (const Dep& d : op.deps) {
-          const int ti = tb_index(p, tr.rank, d.tb);
-          const int dn = static_cast<int>(p.gpus[tr.rank].tbs[ti].ops.size());
-          if (run[run_of[tr.rank][ti]].pos < position(tile, d.step, dn) + 1) ok = false;
+          const int ti = tb_index(p, u.r, d.tb);
+          const Unit& du = units[first[{u.r, ti}] + static_cast<int>(tile % units[first[{u.r, ti}]].lt)];
+          const int dn = static_cast<int>(p.gpus[u.r].tbs[ti].ops.size());
+          if (du.pos < position(tile / du.lt, d.step, dn, du.ntl) + 1) ok = false;
         }
-        const bool direct_out = !direct.empty() && (direct[tr.rank][tr.t][step] & kOutDirect);
+        const bool direct_out = !direct.empty() && (direct[u.r][u.t][step] & kOutDirect);
         if (ok && op_receives(op.op)) {
-          const auto& c = conn[{tb.recv_peer, tr.rank, tb.channel}];
+          const auto& c = conn[{tb.recv_peer, u.r, tb.channel, u.lane}];
           if (c.first <= c.second) ok = false;
         }
         if (ok && op_sends(op.op) && !direct_out) {
-          const auto& c = conn[{tr.rank, tb.send_peer, tb.channel}];
+          const auto& c = conn[{u.r, tb.send_peer, tb.channel, u.lane}];
           if (c.first - c.second >= slots) ok = false;
         }
         if (!ok) break;
-        if (op_receives(op.op)) conn[{tb.recv_peer, tr.rank, tb.channel}].second++;
-        if (op_sends(op.op)) conn[{tr.rank, tb.send_peer, tb.channel}].first++;
-        tr.pos++;
+        if (op_receives(op.op)) conn[{tb.recv_peer, u.r, tb.channel, u.lane}].second++;
+        if (op_sends(op.op)) conn[{u.r, tb.send_peer, tb.channel, u.lane}].first++;
+        u.pos++;
         progress = true;
       }
     }
   }
-  for (const TbRun& tr : run)
-    if (tr.pos < tiles * static_cast<int64_t>(p.gpus[tr.rank].tbs[tr.t].ops.size())) return false;
+  for (const Unit& u : units)
+    if (u.pos < u.ntl * static_cast<int64_t>(p.gpus[u.r].tbs[u.t].ops.size())) return false;
   return true;
 }
 
@@ -855,7 +934,7 @@ struct CallPlan {
   int redop = -1;
 };
 
-ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count, int dtype, int redop, int nlocal_tbs, bool sys_scope,
+ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count, int dtype, int redop, int weight, bool sys_scope,
                        CallPlan& cp) {
   const RankIR& ir = *c->irs[id];
   const Program& p = ir.prog;
@@ -888,7 +967,7 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   int uw = c->cfg.unit_warps;
   if (uw <= 0) {  // automatic: reductions move two operands per element, give them wider units
     uw = ir.has_reduce ? 8 : 4;
-    while (uw > 1 && bps_plain * ds.num_sms * (kThreads / 32 / uw) < nlocal_tbs) uw /= 2;
+    while (uw > 1 && bps_plain * ds.num_sms * (kThreads / 32 / uw) < weight) uw /= 2;
   }
   if (uw < 1 || uw > kThreads / 32 || (kThreads / 32) % uw) uw = kThreads / 32;
   const int units_per_block = kThreads / 32 / uw;
@@ -897,18 +976,18 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, kSmemBudget / (units_per_block * kStageBytesHost));
   cp.smem = static_cast<size_t>(units_per_block) * cp.tma_stages * kStageBytesHost;
   int bps = occupancy(cp.smem);
-  if (bps * ds.num_sms * units_per_block < nlocal_tbs && cp.smem) {  // staging would break co-residency
+  if (bps * ds.num_sms * units_per_block < weight && cp.smem) {  // staging would break co-residency
     cp.tma_stages = 0;
     cp.smem = 0;
     bps = bps_plain;
   }
   const int capacity = bps * ds.num_sms * units_per_block;
-  if (capacity < nlocal_tbs)
-    return set_error(ncclInvalidUsage, "%d thread blocks cannot be co-resident (capacity %d units)", nlocal_tbs, capacity);
+  if (capacity < weight)
+    return set_error(ncclInvalidUsage, "%d thread-block lanes cannot be co-resident (capacity %d units)", weight, capacity);
   // aim for every resident warp busy: one unit per unit_warps resident warps
   const int target_units = bps * ds.num_sms * (kThreads / 32) / uw;
-  int lanes = c->cfg.lanes > 0 ? c->cfg.lanes : std::max(1, target_units / std::max(1, nlocal_tbs));
-  lanes = std::min({lanes, ir.lanes, capacity / nlocal_tbs});
+  int lanes = c->cfg.lanes > 0 ? c->cfg.lanes : std::max(1, target_units / std::max(1, weight));
+  lanes = std::min({lanes, ir.lanes, capacity / weight});
   lanes = std::max(lanes, 1);
   int64_t tile_bytes;
   if (c->cfg.tile_bytes > 0) {
@@ -927,20 +1006,16 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (cp.ntiles < lanes) lanes = static_cast<int>(std::max<int64_t>(cp.ntiles, 1));
   cp.lanes = lanes;
   cp.unit_warps = uw;
-  cp.grid = (nlocal_tbs * lanes + units_per_block - 1) / units_per_block;
+  cp.grid = (weight * lanes + units_per_block - 1) / units_per_block;
   // op-major tile groups: the largest G (<= tiles of a lane) whose order is deadlock-free here
   const int64_t max_tiles = cp.ntiles > 0 ? (cp.ntiles + lanes - 1) / lanes : 0;
-  const int64_t min_tiles = cp.ntiles / lanes;
   int G = c->cfg.group > 0 ? c->cfg.group : static_cast<int>(std::min<int64_t>(std::max<int64_t>(max_tiles, 1), 64));
   RankIR& mir = *c->irs[id];
   for (; G > 1; G /= 2) {
-    const auto key = std::make_tuple(max_tiles, G, ir.slots);
+    const auto key = std::make_tuple(cp.ntiles, lanes, G, ir.slots);
     auto f = mir.order_ok.find(key);
-    if (f == mir.order_ok.end()) {
-      const bool okay = order_is_deadlock_free(p, mir.eff_direct, max_tiles, G, ir.slots) &&
-                        (min_tiles == max_tiles || order_is_deadlock_free(p, mir.eff_direct, min_tiles, G, ir.slots));
-      f = mir.order_ok.emplace(key, okay).first;
-    }
+    if (f == mir.order_ok.end())
+      f = mir.order_ok.emplace(key, order_is_deadlock_free(p, mir.eff_direct, cp.ntiles, lanes, mir.mult, G, ir.slots)).first;
     if (f->second) break;
   }
   cp.group = std::max(G, 1);
@@ -980,7 +1055,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     return set_error(ncclInvalidUsage, "all %zu ranks hosted on device %d must issue the collective in one group (got %zu)",
                      plan.ranks.size(), dev, ops.size());
   CallPlan cp;
-  NCCL_TRY(plan_call(c0, *ds, id, p0.coll, p0.count, p0.dtype, p0.redop, plan.ntbs, plan.sys_scope, cp));
+  NCCL_TRY(plan_call(c0, *ds, id, p0.coll, p0.count, p0.dtype, p0.redop, plan.weight, plan.sys_scope, cp));
   const RankIR& ir0 = *c0->irs[id];
   const size_t esize = dtype_size(p0.dtype);
   const int64_t chunk_bytes = cp.chunk_elems * cp.kesize;
@@ -992,6 +1067,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.chans = plan.d_chans;
   a.sems = plan.d_sems;
   a.ntbs = plan.ntbs;
+  a.weight = plan.weight;
   a.lanes = cp.lanes;
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
@@ -1010,7 +1086,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     for (int r : plan.ranks)
       for (const auto& tb : c0->irs[id]->prog.gpus[r].tbs) max_nops = std::max(max_nops, static_cast<int>(tb.ops.size()));
     const int ops_per_block = static_cast<int>(std::min<int64_t>((cp.ntiles + cp.lanes - 1) / cp.lanes * max_nops, 1 << 20));
-    const size_t need = static_cast<size_t>(plan.ntbs) * cp.lanes * ops_per_block * 4 * sizeof(uint64_t);
+    const size_t need = static_cast<size_t>(plan.weight) * cp.lanes * ops_per_block * 4 * sizeof(uint64_t);
     DeviceGuard gt(dev);
     if (need > ds->trace_bytes) {
       if (ds->d_trace) cudaFree(ds->d_trace);
@@ -1022,7 +1098,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     CUDA_TRY(cudaMemsetAsync(ds->d_trace, 0, need, p0.stream));
     a.trace = ds->d_trace;
     a.trace_ops = ops_per_block;
-    ds->trace_grid = plan.ntbs * cp.lanes;
+    ds->trace_grid = plan.weight * cp.lanes;
     ds->trace_ops = ops_per_block;
     ds->trace_lanes = cp.lanes;
   }
@@ -1412,7 +1488,10 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
     ir->lanes = std::max(1, std::min(comm->cfg.max_lanes, (2 * sms + max_tbs - 1) / max_tbs));
   }
-  ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes);
+  ir->mult = comm->cfg.balance ? lane_multipliers(ir->prog) : std::vector<std::vector<int>>();
+  if (ir->mult.empty())
+    for (const auto& g : ir->prog.gpus) ir->mult.emplace_back(g.tbs.size(), 1);
+  ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes, ir->mult);
   {
     DeviceGuard g(comm->device);
     CUDA_TRY(cudaMalloc(&ir->arena, ir->lay.bytes));
@@ -1456,6 +1535,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "unit_warps") c.unit_warps = static_cast<int>(value);
   else if (k == "group") c.group = static_cast<int>(value);
   else if (k == "tma") c.tma = static_cast<int>(value);
+  else if (k == "balance") c.balance = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
@@ -1490,7 +1570,7 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
   const RankIR& ir = *comm->irs[info->ir_id];
   for (int r = 0; r < comm->nranks; ++r)
     if (comm->clique->local[r] && comm->clique->local[r]->device == comm->device) {
-      ntbs += static_cast<int>(ir.prog.gpus[r].tbs.size());
+      for (int m : ir.mult[r]) ntbs += m;
       ++nlocal;
     }
   CallPlan cp;
@@ -1582,7 +1662,7 @@ ncclResult_t gc3IrReplicate(gc3Ir_t ir, int instances, gc3Ir_t* out) {
 
 ncclResult_t gc3IrArenaLayout(gc3Ir_t ir, int rank, int lanes, int slots, int64_t slot_unit, char** json) {
   if (!ir || !json || rank < 0 || rank >= ir->p.ranks() || lanes < 1 || slots < 1 || slot_unit < 1) return ncclInvalidArgument;
-  const ArenaLayout a = make_layout(ir->p, rank, lanes, slots, slot_unit);
+  const ArenaLayout a = make_layout(ir->p, rank, lanes, slots, slot_unit, {});
   std::ostringstream os;
   os << "{\"n_in\": " << a.n_in << ", \"n_out\": " << a.n_out << ", \"bytes\": " << a.bytes << ", \"off_head\": " << a.off_head
      << ", \"off_tail\": " << a.off_tail << ", \"off_mine_in\": " << a.off_mine_in << ", \"off_mine_out\": " << a.off_mine_out
@@ -1616,7 +1696,7 @@ ncclResult_t gc3IrDirectMessages(gc3Ir_t ir, char** json) {
 
 ncclResult_t gc3IrOrderCheck(gc3Ir_t ir, int64_t tiles, int group, int slots, int* deadlock_free) {
   if (!ir || !deadlock_free || tiles < 0 || group < 1 || slots < 1) return ncclInvalidArgument;
-  *deadlock_free = order_is_deadlock_free(ir->p, {}, tiles, group, slots) ? 1 : 0;
+  *deadlock_free = order_is_deadlock_free(ir->p, {}, tiles, 1, {}, group, slots) ? 1 : 0;
   return ncclSuccess;
 }
 

@@ -180,3 +180,11 @@ def test_fifo_only_path(name, count):
 def test_direct_path_ll(name, count):
     _check(name, count, proto="ll")
     _check(name, count, proto="ll", dtype="bfloat16")
+
+
+@pytest.mark.parametrize("name,count", [("twostep_a2a_2x4", 5000), ("hier_ar_2x4_par1", 8 * 6000)])
+@pytest.mark.parametrize("balance", [0, 1])
+def test_lane_multipliers(name, count, balance):
+    """Per-component lane counts (balance=1) and uniform lanes (balance=0) give the same bits."""
+    _check(name, count, balance=balance, tile_bytes=1024)
+    _check(name, count, balance=balance, group=1, lanes=3, tile_bytes=2048)
