@@ -694,6 +694,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       }
       if (t == 0) stamp(q, 2);
       if (!unit_and(ok, uw, bar_id, n)) return;
+      if (a.discard && in && !in_d) {
+        // the consumed slot is dead until the sender refills it: drop its lines from L2 so they are
+        // never written back to HBM (the FIFO round trip stays on chip when the consumer is prompt)
+        const int64_t used = static_cast<int64_t>(op.count) * tbytes * (ll_in ? 2 : 1);
+        for (int64_t off = static_cast<int64_t>(t) * 128; off + 128 <= used; off += static_cast<int64_t>(n) * 128)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(in + off) : "memory");
+        unit_sync(uw, bar_id, n);
+      }
 
       // (3) publish: slot posted / slot freed / semaphore
       if (t == 0) {

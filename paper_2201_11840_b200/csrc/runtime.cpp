@@ -98,6 +98,7 @@ struct Config {
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
   int tma = 1;                       // bulk (TMA) copies for pure-copy ops on same-device peers
   int balance = 1;                   // per-component lane multipliers (lane_multipliers)
+  int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
 
@@ -115,6 +116,7 @@ Config config_from_env() {
   c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
   c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
   c.balance = static_cast<int>(env_int("GC3_BALANCE", c.balance));
+  c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
 }
 
@@ -1072,6 +1074,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
   a.tma_stages = cp.tma_stages;
+  a.discard = c0->cfg.discard;
   a.slots = ir0.slots;
   a.sys_scope = plan.sys_scope ? 1 : 0;
   a.chunk_elems = cp.chunk_elems;
@@ -1536,6 +1539,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "group") c.group = static_cast<int>(value);
   else if (k == "tma") c.tma = static_cast<int>(value);
   else if (k == "balance") c.balance = static_cast<int>(value);
+  else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
