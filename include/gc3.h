@@ -103,7 +103,8 @@ ncclResult_t ncclGroupStart(void);
 ncclResult_t ncclGroupEnd(void);
 
 /* ---- GC3 extensions ------------------------------------------------------------------------ */
-/* Registers a GC3-IR program (file path, or the JSON text itself if it starts with '{') on this
+/* Registers a GC3-IR program (file path, or the text itself: GC3-IR JSON if it starts with '{', an
+ * MSCCL algorithm XML if it starts with '<'; a file is XML if its content starts with '<') on this
  * rank; every rank must register the same programs in the same order (collective, like comm init).
  * instances > 1 applies the runtime parallelization rewrite (program.hpp:366-419; SURVEY.md
  * Finding 5). The IR is loaded with the reference schema rules, validated (ir.hpp:341-439) against
@@ -150,6 +151,12 @@ typedef struct gc3Ir* gc3Ir_t;
 /* ir.hpp:226-310. On a schema error returns ncclInvalidArgument and, if err is non-NULL, sets
  * *err to a malloc'd "path\tmessage" string (free with gc3Free). */
 ncclResult_t gc3IrParse(const char* text, gc3Ir_t* ir, char** err);
+/* MSCCL algorithm XML (the paper runtime's format) into the
+ * same program: one dependency per step, `nop` steps carry extra dependencies and (fold_nops != 0)
+ * are folded back into the following op. Errors: ncclInvalidArgument, *err = "xml: path: message". */
+ncclResult_t gc3IrParseXml(const char* text, int fold_nops, gc3Ir_t* ir, char** err);
+/* The program as MSCCL XML (multi-dependency ops expanded into nop chains); malloc'd. */
+ncclResult_t gc3IrToXml(gc3Ir_t ir, char** text);
 /* ir.hpp:145-186: canonical JSON (malloc'd, free with gc3Free) */
 ncclResult_t gc3IrSerialize(gc3Ir_t ir, char** text);
 /* ir.hpp:341-439: newline-separated issues ("" if valid) against an nodes x gpus_per_node

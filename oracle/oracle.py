@@ -122,3 +122,49 @@ def reduce_arrays(a, b, dtype, redop="sum"):
                            REDOPS[redop] if isinstance(redop, str) else redop)
     assert rc == 0
     return out
+
+
+def collective(ir, coll, arrays, count, dtype, redop="sum", **run_kw):
+    """NCCL-level oracle: the recvbuff of every rank after `coll` over `count` (NCCL's count
+    argument) with the IR, from per-rank sendbuff arrays (numpy, raw bits).
+
+    Buffer mapping: AllReduce / ReduceScatter run the in-place IR on the send
+    data (ReduceScatter returns the rank's owned block); AllGather and AlltoAll map IR input/output
+    to sendbuff/recvbuff.  A rank block (AllReduce: count; AllGather: sendcount; ReduceScatter:
+    recvcount; AlltoAll: count per peer) is cut into the IR's c chunks per block of
+    ce = ceil(count / c) elements; when c does not divide count the last chunks are clipped:
+    element p of a block is element p % ce of chunk p // ce (each block padded to c * ce here;
+    ops map chunk position x to position x, so padding never mixes into real elements).
+    """
+    if not isinstance(ir, FlatIR):
+        ir = FlatIR(ir)
+    R, (nin, nout, nsc) = ir.nranks, ir.nchunks
+    c = nin if coll in ("allreduce", "allgather") else nin // R
+    ce = -(-count // c) if count else 0
+    pb = c * ce
+    nblk = 1 if coll in ("allreduce", "allgather") else R
+
+    def pad(a):
+        out = np.zeros(nblk * pb, dtype=a.dtype)
+        for b in range(nblk):
+            out[b * pb:b * pb + count] = a[b * count:(b + 1) * count]
+        return out
+
+    def unpad(a, blocks):
+        return np.concatenate([a[b * pb:b * pb + count] for b in range(blocks)]) if blocks else a[:0]
+
+    bufs = []
+    for r in range(R):
+        inp = pad(np.ascontiguousarray(arrays[r]))
+        out = inp if ir.inplace else np.zeros(max(nout, 1) * ce, dtype=inp.dtype)
+        sc = np.zeros(max(nsc, 1) * ce, dtype=inp.dtype)
+        bufs.append([inp, out, sc])
+    if count:
+        rc, err = ir.run(bufs, ce, dtype, redop, **run_kw)
+        if rc != 0:
+            raise RuntimeError(err)
+    if coll == "reducescatter":
+        return [bufs[r][0][r * pb:r * pb + count].copy() for r in range(R)]
+    if coll == "allreduce":
+        return [unpad(bufs[r][0], 1) for r in range(R)]
+    return [unpad(bufs[r][1], R) for r in range(R)]

@@ -38,6 +38,7 @@
 #include "../../include/gc3.h"
 #include "devplan.hpp"
 #include "ir.hpp"
+#include "msccl_xml.hpp"
 
 namespace gc3 {
 
@@ -302,8 +303,10 @@ struct gc3Comm {
   std::vector<std::vector<char*>> peer_arena;
   char* scratch = nullptr;
   size_t scratch_bytes = 0;
-  char* work = nullptr;  // ReduceScatter working buffer
+  char* work = nullptr;  // ReduceScatter working buffer; padded input block(s) of ragged calls
   size_t work_bytes = 0;
+  char* work2 = nullptr;  // padded output blocks of ragged AllGather / AlltoAll calls
+  size_t work2_bytes = 0;
   ncclResult_t async_error = ncclSuccess;
   std::string last_error;
   bool destroyed = false;
@@ -371,7 +374,7 @@ ncclResult_t device_state(Clique* cl, int dev, DeviceState*& out) {
 bool read_ir_text(const char* arg, std::string& text) {
   const char* p = arg;
   while (*p == ' ' || *p == '\n' || *p == '\t' || *p == '\r') ++p;
-  if (*p == '{') {
+  if (*p == '{' || *p == '<') {  // GC3-IR JSON or MSCCL XML text
     text = arg;
     return true;
   }
@@ -807,27 +810,33 @@ void traffic(const Program& p, int rank, int64_t chunk_bytes, int64_t& sent, int
     }
 }
 
-// IR chunk geometry of a collective call: returns elements per chunk or -1 if not divisible.
-int64_t chunk_elems_for(const Program& p, int coll, size_t count, int nranks) {
+// IR chunk geometry of a collective call. The NCCL count of one rank's block (AllReduce: count;
+// AllGather: sendcount; ReduceScatter: recvcount; AlltoAll: count per peer) is split into the IR's
+// c chunks per block of ceil(count / c) elements; when c does not divide the count the last chunks
+// are clipped ("ragged": element p of a block is element p % ce of chunk p / ce, the runtime pads
+// each block to c x ce elements in work buffers). Returns elements per chunk, -1 if the IR's shape
+// does not fit the collective.
+int64_t chunk_elems_for(const Program& p, int coll, size_t count, int nranks, bool* ragged = nullptr) {
   const int cin = p.nchunks[0];
   if (cin <= 0) return -1;
+  int c = cin;
   switch (coll) {
-    case kAllReduce: return count % cin ? -1 : static_cast<int64_t>(count / cin);
+    case kAllReduce: break;
     case kAllGather:
       if (p.nchunks[1] != nranks * cin) return -1;
-      return count % cin ? -1 : static_cast<int64_t>(count / cin);
-    case kReduceScatter: {
+      break;
+    case kReduceScatter:
       if (cin % nranks) return -1;
-      const int c = cin / nranks;
-      return count % c ? -1 : static_cast<int64_t>(count / c);
-    }
-    case kAllToAll: {
+      c = cin / nranks;
+      break;
+    case kAllToAll:
       if (cin % nranks || p.nchunks[1] != cin) return -1;
-      const int c = cin / nranks;
-      return count % c ? -1 : static_cast<int64_t>(count / c);
-    }
+      c = cin / nranks;
+      break;
+    default: return -1;
   }
-  return -1;
+  if (ragged) *ragged = count % c != 0;
+  return static_cast<int64_t>((count + c - 1) / c);
 }
 
 // bytes used for size_range selection: the per-rank message buffer size
@@ -1061,6 +1070,16 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   const RankIR& ir0 = *c0->irs[id];
   const size_t esize = dtype_size(p0.dtype);
   const int64_t chunk_bytes = cp.chunk_elems * cp.kesize;
+  bool ragged = false;
+  const int64_t ce = chunk_elems_for(ir0.prog, p0.coll, p0.count, c0->nranks, &ragged);
+  const int cblk = (p0.coll == kAllReduce || p0.coll == kAllGather) ? ir0.prog.nchunks[0] : ir0.prog.nchunks[0] / c0->nranks;
+  struct PostCopy {  // result copies after the launch (cudaMemcpy2DAsync arguments)
+    char* dst;
+    size_t dpitch;
+    const char* src;
+    size_t spitch, width, rows;
+  };
+  std::vector<PostCopy> post;
 
   LaunchArgs a{};
   a.tbs = plan.d_tbs;
@@ -1132,26 +1151,56 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     NCCL_TRY(ensure_buffer(c, c->scratch, c->scratch_bytes, std::max<size_t>(scratch_need, 256)));
     char* in = nullptr;
     char* out = nullptr;
+    // blk: one rank block of the user's buffers; pblk: the same block padded to c x ce elements
+    // (equal unless the call is ragged, see chunk_elems_for)
+    const size_t blk = p0.count * esize, pblk = static_cast<size_t>(cblk) * ce * esize;
+    const int R = c->nranks;
+    char* send = const_cast<char*>(static_cast<const char*>(q->send));
+    char* recv = static_cast<char*>(q->recv);
     switch (p0.coll) {
       case kAllReduce:  // in-place IR on `input` (core.hpp:305-327)
-        if (q->send != q->recv) CUDA_TRY(cudaMemcpyAsync(q->recv, q->send, p0.count * esize, cudaMemcpyDeviceToDevice, stream));
-        in = out = static_cast<char*>(q->recv);
+        if (ragged) {
+          NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, pblk));
+          CUDA_TRY(cudaMemcpyAsync(c->work, send, blk, cudaMemcpyDeviceToDevice, stream));
+          in = out = c->work;
+          post.push_back({recv, blk, c->work, pblk, blk, 1});
+        } else {
+          if (send != recv) CUDA_TRY(cudaMemcpyAsync(recv, send, blk, cudaMemcpyDeviceToDevice, stream));
+          in = out = recv;
+        }
         break;
       case kAllGather:
-        in = const_cast<char*>(static_cast<const char*>(q->send));
-        out = static_cast<char*>(q->recv);
+        if (ragged) {
+          NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, pblk));
+          NCCL_TRY(ensure_buffer(c, c->work2, c->work2_bytes, pblk * R));
+          CUDA_TRY(cudaMemcpyAsync(c->work, send, blk, cudaMemcpyDeviceToDevice, stream));
+          in = c->work;
+          out = c->work2;
+          post.push_back({recv, blk, c->work2, pblk, blk, static_cast<size_t>(R)});
+        } else {
+          in = send;
+          out = recv;
+        }
         break;
-      case kReduceScatter: {  // in-place IR over R*c chunks; rank r owns [r*c, (r+1)*c)
-        const size_t total = p0.count * esize * c->nranks;
-        NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, total));
-        CUDA_TRY(cudaMemcpyAsync(c->work, q->send, total, cudaMemcpyDeviceToDevice, stream));
+      case kReduceScatter:  // in-place IR over R*c chunks; rank r owns [r*c, (r+1)*c)
+        NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, pblk * R));
+        CUDA_TRY(cudaMemcpy2DAsync(c->work, pblk, send, blk, blk, R, cudaMemcpyDeviceToDevice, stream));
         in = out = c->work;
+        post.push_back({recv, blk, c->work + static_cast<size_t>(c->rank) * pblk, pblk, blk, 1});
         break;
-      }
       case kAllToAll:
         if (q->send == q->recv) return set_error(ncclInvalidArgument, "in-place AllToAll is not supported");
-        in = const_cast<char*>(static_cast<const char*>(q->send));
-        out = static_cast<char*>(q->recv);
+        if (ragged) {
+          NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, pblk * R));
+          NCCL_TRY(ensure_buffer(c, c->work2, c->work2_bytes, pblk * R));
+          CUDA_TRY(cudaMemcpy2DAsync(c->work, pblk, send, blk, blk, R, cudaMemcpyDeviceToDevice, stream));
+          in = c->work;
+          out = c->work2;
+          post.push_back({recv, blk, c->work2, pblk, blk, static_cast<size_t>(R)});
+        } else {
+          in = send;
+          out = recv;
+        }
         break;
     }
     if (ir.prog.inplace) out = in;
@@ -1160,14 +1209,8 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][2] = c->scratch;
   }
   CUDA_TRY(interp_launch(cp.fn, a, cp.grid, cp.smem, stream));
-  for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
-    if (p0.coll != kReduceScatter) continue;
-    Pending* q = nullptr;
-    for (Pending* x : ops)
-      if (x->comm->rank == plan.ranks[slot]) q = x;
-    const size_t bytes = p0.count * esize;
-    CUDA_TRY(cudaMemcpyAsync(q->recv, q->comm->work + q->comm->rank * bytes, bytes, cudaMemcpyDeviceToDevice, stream));
-  }
+  for (const PostCopy& pc : post)
+    CUDA_TRY(cudaMemcpy2DAsync(pc.dst, pc.dpitch, pc.src, pc.spitch, pc.width, pc.rows, cudaMemcpyDeviceToDevice, stream));
   for (cudaStream_t s : others) {
     cudaEvent_t ev;
     CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1338,6 +1381,7 @@ static void release_comm(Comm* c) {
     if (ir->arena) cudaFree(ir->arena);
   if (c->scratch) cudaFree(c->scratch);
   if (c->work) cudaFree(c->work);
+  if (c->work2) cudaFree(c->work2);
   cl->local[c->rank] = nullptr;
   const std::string dir = shm_dir(cl->key);
   unlink((dir + "/rank" + std::to_string(c->rank)).c_str());
@@ -1463,8 +1507,14 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
   std::string text;
   if (!read_ir_text(path_or_json, text)) return set_error(ncclSystemError, "io: cannot open IR file %s", path_or_json);
   auto ir = std::make_unique<RankIR>();
-  SchemaError se;
-  if (!parse_program(text, ir->prog, se)) return set_error(ncclInvalidArgument, "%s", se.what().c_str());
+  size_t first = text.find_first_not_of(" \t\r\n");
+  if (first != std::string::npos && text[first] == '<') {  // MSCCL algorithm file (msccl_xml.hpp)
+    std::string e;
+    if (!parse_msccl_xml(text, ir->prog, e)) return set_error(ncclInvalidArgument, "%s", e.c_str());
+  } else {
+    SchemaError se;
+    if (!parse_program(text, ir->prog, se)) return set_error(ncclInvalidArgument, "%s", se.what().c_str());
+  }
   if (instances > 1) ir->prog = replicate_instances(ir->prog, instances);
   Topology topo;
   topo.nodes = 1;
@@ -1629,6 +1679,24 @@ ncclResult_t gc3IrParse(const char* text, gc3Ir_t* ir, char** err) {
   return ncclSuccess;
 }
 
+ncclResult_t gc3IrParseXml(const char* text, int fold_nops, gc3Ir_t* ir, char** err) {
+  if (!text || !ir) return ncclInvalidArgument;
+  auto h = std::make_unique<gc3Ir>();
+  std::string e;
+  if (!parse_msccl_xml(text, h->p, e, fold_nops != 0)) {
+    if (err) *err = dup_cstr(e);
+    *ir = nullptr;
+    return ncclInvalidArgument;
+  }
+  if (err) *err = nullptr;
+  *ir = h.release();
+  return ncclSuccess;
+}
+ncclResult_t gc3IrToXml(gc3Ir_t ir, char** text) {
+  if (!ir || !text) return ncclInvalidArgument;
+  *text = dup_cstr(to_msccl_xml(ir->p));
+  return ncclSuccess;
+}
 ncclResult_t gc3IrSerialize(gc3Ir_t ir, char** text) {
   if (!ir || !text) return ncclInvalidArgument;
   *text = dup_cstr(serialize(ir->p));

@@ -86,6 +86,8 @@ def lib():
         "gc3GetTrace": [vp, ctypes.c_void_p, sz, ctypes.POINTER(i), ctypes.POINTER(i), ctypes.POINTER(i)],
         "gc3IrParse": [cp, ctypes.POINTER(vp), ctypes.POINTER(vp)],
         "gc3IrSerialize": [vp, ctypes.POINTER(vp)],
+        "gc3IrParseXml": [cp, i, ctypes.POINTER(vp), ctypes.POINTER(vp)],
+        "gc3IrToXml": [vp, ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -136,6 +138,21 @@ class IR:
             e.path, e.message = path, msg
             raise e
         self._h = h
+
+    @classmethod
+    def from_xml(cls, text, fold_nops=True):
+        """An MSCCL algorithm XML file's text as a program (msccl_xml.hpp)."""
+        h, err = ctypes.c_void_p(), ctypes.c_void_p()
+        rc = lib().gc3IrParseXml(text.encode() if isinstance(text, str) else text, int(fold_nops), ctypes.byref(h),
+                                 ctypes.byref(err))
+        if rc != 0:
+            raise NcclError(rc, _take(err.value))
+        return cls._wrap(h)
+
+    def to_xml(self):
+        out = ctypes.c_void_p()
+        check(lib().gc3IrToXml(self._h, ctypes.byref(out)))
+        return _take(out.value)
 
     @classmethod
     def _wrap(cls, h):

@@ -5,7 +5,7 @@ import json
 import numpy as np
 import torch
 
-from oracle.oracle import FlatIR
+from oracle.oracle import collective
 
 TORCH_DT = {"float32": torch.float32, "bfloat16": torch.bfloat16, "float16": torch.float16, "int32": torch.int32,
             "float64": torch.float64, "int64": torch.int64, "uint8": torch.uint8, "int8": torch.int8,
@@ -41,27 +41,9 @@ def to_np_bits(t, dtype):
 
 def oracle_collective(ir_json, coll, inputs, count, dtype, op="sum"):
     """Expected recvbuffs (numpy, raw bits) of every rank from the CPU oracle."""
-    ir = FlatIR(json.loads(ir_json) if isinstance(ir_json, str) else ir_json)
-    R, (nin, nout, nsc) = ir.nranks, ir.nchunks
-    arrays = [to_np_bits(x, dtype) for x in inputs]
-    if coll == "allreduce":
-        ce = count // nin
-    elif coll == "allgather":
-        ce = count // nin
-    else:
-        ce = count // (nin // R)
-    bufs = []
-    for r in range(R):
-        inp = arrays[r].copy()
-        out = inp if ir.inplace else np.zeros(max(nout, 1) * ce, dtype=inp.dtype)
-        sc = np.zeros(max(nsc, 1) * ce, dtype=inp.dtype)
-        bufs.append([inp, out, sc])
     odt = {"bfloat16": 9, "float16": 6}.get(dtype, dtype)
-    rc, err = ir.run(bufs, ce, odt, op)
-    assert rc == 0, err
-    if coll == "reducescatter":
-        return [bufs[r][0][r * count:(r + 1) * count].copy() for r in range(R)]
-    return [bufs[r][1].copy() for r in range(R)]
+    return collective(json.loads(ir_json) if isinstance(ir_json, str) else ir_json, coll,
+                      [to_np_bits(x, dtype) for x in inputs], count, odt, op)
 
 
 def run_collective(comms, coll, inputs, count, dtype, op="sum", inplace=False, stream=None):

@@ -188,3 +188,64 @@ def test_lane_multipliers(name, count, balance):
     """Per-component lane counts (balance=1) and uniform lanes (balance=0) give the same bits."""
     _check(name, count, balance=balance, tile_bytes=1024)
     _check(name, count, balance=balance, group=1, lanes=3, tile_bytes=2048)
+
+
+@pytest.mark.parametrize("name,count,dtype,instances", [
+    ("ring_ar_8_ch1", 8 * 1000 + 3, "float32", 1), ("ring_ar_8_ch1", 5, "float32", 1),
+    ("hier_ar_2x4_par1", 8 * 4096 + 7, "bfloat16", 1), ("ring_ar_8_ch8_inst4", 32 * 100 + 31, "float32", 1),
+    ("ring_ag_8", 1001, "float32", 4), ("ring_ag_4", 3, "bfloat16", 2),
+    ("ring_rs_8", 777, "float32", 4), ("ring_rs_2", 1, "int32", 3),
+    ("twostep_a2a_2x4", 1003, "float32", 3), ("twostep_a2a_1x8", 2, "float16", 4),
+])
+def test_ragged_counts(name, count, dtype, instances):
+    """Counts the IR's chunks do not divide: chunks of ceil(count / c) elements, the last ones
+    clipped (the runtime stages through padded work buffers); bit-exact vs the oracle's clipping."""
+    _check(name, count, dtype, instances=instances)
+    _check(name, count, dtype, instances=instances, proto="ll")
+
+
+@pytest.mark.parametrize("coll,name", [("allreduce", "ring_ar_8_ch1"), ("allgather", "ring_ag_8"),
+                                       ("reducescatter", "ring_rs_8"), ("alltoall", "twostep_a2a_2x4")])
+def test_zero_count_is_a_noop(coll, name):
+    from gpu_util import run_collective
+    comms, irj = _setup(name)
+    try:
+        outs = run_collective(comms, coll, [torch.zeros(0, device="cuda") for _ in comms], 0, "float32")
+        torch.cuda.synchronize()
+        assert all(o.numel() == 0 for o in outs)
+        assert comms[0].async_error()[0] == 0
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+@pytest.mark.parametrize("name,count,fold", [("hier_ar_2x4_par1", 8 * 3000, True), ("twostep_a2a_2x4", 2000, False),
+                                             ("ring_rs_8", 1000, True)])
+def test_msccl_xml_registration(name, count, fold, tmp_path):
+    """gc3RegisterIR with an MSCCL algorithm file (csrc/msccl_xml.cpp): same bits as the oracle run
+    on the GC3-IR the XML came from (fold=False registers the nop-expanded text)."""
+    from paper_2201_11840_b200 import gc3
+    from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
+    ir = gc3.IR(read_ir(name))
+    xml = ir.to_xml()
+    if not fold:  # register the nop-expanded program text (MSCCL's one-dependency encoding kept)
+        xml = gc3.IR.from_xml(xml, fold_nops=False).to_xml()
+    f = tmp_path / (name + ".xml")
+    f.write_text(xml)
+    irj = json.loads(read_ir(name))
+    R = len(irj["gpus"])
+    comms = gc3.init_all([0] * R)
+    try:
+        for c in comms:
+            c.register_ir(str(f))
+        coll = irj["collective"]
+        inputs = [make_input(input_len(coll, count, R), "float32", 7 + r) for r in range(R)]
+        expected = oracle_collective(irj, coll, [x.clone() for x in inputs], count, "float32")
+        outs = run_collective(comms, coll, inputs, count, "float32")
+        torch.cuda.synchronize()
+        assert comms[0].async_error()[0] == 0
+        for r in range(R):
+            assert np.array_equal(to_np_bits(outs[r], "float32"), expected[r])
+    finally:
+        for c in comms:
+            c.destroy()

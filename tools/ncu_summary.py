@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """Summarise ncu artefacts from gpurun_out/ into committed profiles/ files.
 
-    python tools/ncu_summary.py <tag> <config> <ir> <bytes_per_rank> [--world 1]
+    python tools/ncu_summary.py <tag> <config> <ir> <bytes_per_rank> [--world 1] [--out DIR]
+    python tools/ncu_summary.py --merge gpurun_out/<tag>/profiles     # box-side summaries -> profiles/
 
 Reads gpurun_out/<tag>/launches_<config>.csv (the `--metrics gpu__time_duration.sum` launch list)
 and gpurun_out/<tag>/prof_<config>.ncu-rep (one `--set full` capture of the interpreter), writes
@@ -78,8 +79,27 @@ def stalls(rep, top=8):
     return [(s / tot, ln, src) for s, ln, src in sorted(lines, reverse=True)[:top]]
 
 
+def merge(src):
+    dst = os.path.join(REPO, "profiles")
+    os.makedirs(dst, exist_ok=True)
+    for f in os.listdir(src):
+        if f.endswith(".md"):
+            with open(os.path.join(src, f)) as a, open(os.path.join(dst, f), "w") as b:
+                b.write(a.read())
+    sj = os.path.join(src, "ncu_summary.json")
+    if os.path.exists(sj):
+        p = os.path.join(dst, "ncu_summary.json")
+        allr = json.load(open(p)) if os.path.exists(p) else {}
+        allr.update(json.load(open(sj)))
+        with open(p, "w") as f:
+            json.dump(allr, f, indent=1, sort_keys=True)
+
+
 def main():
+    if sys.argv[1] == "--merge":
+        return merge(sys.argv[2])
     tag, cfg, ir, nbytes = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+    outdir = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else os.path.join(REPO, "profiles")
     world = int(sys.argv[sys.argv.index("--world") + 1]) if "--world" in sys.argv else 1
     src = os.path.join(REPO, "gpurun_out", tag)
     md = [f"# ncu summary — {tag}, config {cfg} ({ir}, {nbytes} B per rank, {world} GPU)", ""]
@@ -114,11 +134,11 @@ def main():
         if st:
             md += ["", "## Top stall instructions (warp-stall samples, SASS)", "", "| share | address | instruction |", "|---|---|---|"]
             md += [f"| {s:.1%} | {ln} | `{src_.replace('|', '/')}` |" for s, ln, src_ in st]
-    os.makedirs(os.path.join(REPO, "profiles"), exist_ok=True)
-    with open(os.path.join(REPO, "profiles", f"{tag}_{cfg}.md"), "w") as f:
+    os.makedirs(outdir, exist_ok=True)
+    with open(os.path.join(outdir, f"{tag}_{cfg}.md"), "w") as f:
         f.write("\n".join(md) + "\n")
     if rec:
-        p = os.path.join(REPO, "profiles", "ncu_summary.json")
+        p = os.path.join(outdir, "ncu_summary.json")
         allr = json.load(open(p)) if os.path.exists(p) else {}
         allr[f"{ir}:{nbytes}:{world}"] = rec
         with open(p, "w") as f:
