@@ -20,21 +20,25 @@ constexpr int kMaxLocalRanks = 16;
 constexpr int kThreads = GC3_THREADS;  // CUDA threads per interpreter block
 
 enum : uint8_t { kOpSend = 0, kOpRecv, kOpCopy, kOpReduce, kOpRrc, kOpRcs, kOpRrcs, kOpRrs, kOpNop };
-enum : uint8_t { kInDirect = 1, kOutDirect = 2 };
+enum : uint8_t { kInDirect = 1, kOutDirect = 2, kInPull = 4, kOutPull = 8 };
 
-struct DevOp {  // 24 bytes
+struct DevOp {  // 32 bytes
   uint8_t opcode;
   uint8_t src_buf;
   uint8_t dst_buf;
   uint8_t has_dep;
   int16_t ndeps;
-  uint8_t direct;  // bit 0: the incoming message is already in place (in_direct);
-                   // bit 1: write the outgoing message into the receiver's buffer (out_direct)
-  uint8_t pad;
+  uint8_t direct;  // kInDirect: the incoming message is already in place;
+                   // kOutDirect: write the outgoing message into the receiver's buffer;
+                   // kInPull: read the incoming message from the sender's span (in_buf, in_off);
+                   // kOutPull: the outgoing message stays in this rank's span (publish only)
+  uint8_t in_buf;  // kInPull: sender's buffer id
   int32_t src_off;
   int32_t dst_off;
   int32_t count;
   int32_t dep_begin;
+  int32_t in_off;  // kInPull: sender's chunk offset
+  int32_t pad;
 };
 
 struct DevDep {
@@ -54,7 +58,7 @@ struct DevTb {
   int32_t peer_slot;  // rank slot of the send peer when it runs in the same launch, else -1
   int32_t mult;       // lane multiplier: this thread block runs lanes x mult lanes (work balance)
   int32_t unit_base;  // sum of the multipliers of the launch's earlier thread blocks
-  int32_t pad;
+  int32_t recv_slot;  // rank slot of the receive peer when it runs in the same launch, else -1
 };
 
 // One side of one connection for one lane.  The FIFO and `head` live in the receiver's memory,

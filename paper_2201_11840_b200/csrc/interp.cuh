@@ -34,6 +34,17 @@
 #ifndef GC3_MINBLOCKS
 #define GC3_MINBLOCKS 1
 #endif
+#ifndef GC3_TAIL_UNROLL  // vectors in flight per thread in the predicated tail of a data move
+#define GC3_TAIL_UNROLL 4
+#endif
+#ifndef GC3_MOVE_NOINLINE  // compile the data mover once per reduction instead of at every op site
+#define GC3_MOVE_NOINLINE 1
+#endif
+#if GC3_MOVE_NOINLINE
+#define GC3_MOVE_ATTR __noinline__
+#else
+#define GC3_MOVE_ATTR
+#endif
 
 namespace gc3 {
 namespace dev {
@@ -235,11 +246,27 @@ __device__ __forceinline__ void move_vec(const uint4* a, const uint4* b, uint4* 
       if (TWO) st_vec(o1 + i + k * n, v);
     }
   }
-  for (; i < nvec; i += n) {
-    const uint4 x = ld_cg(a + i);
-    const uint4 v = RED ? R::template vec<uint4>(x, ld_cg(b + i)) : x;
-    st_vec(o0 + i, v);
-    if (TWO) st_vec(o1 + i, v);
+  // the rest (< U vectors per thread) in predicated passes of T: a small tile costs one or two
+  // memory round trips instead of one per vector
+  constexpr int T = U < GC3_TAIL_UNROLL ? U : GC3_TAIL_UNROLL;
+  for (; i < nvec; i += T * n) {
+    uint4 x[T], y[T];
+#pragma unroll
+    for (int k = 0; k < T; ++k)
+      if (i + k * n < nvec) x[k] = ld_cg(a + i + k * n);
+    if (RED) {
+#pragma unroll
+      for (int k = 0; k < T; ++k)
+        if (i + k * n < nvec) y[k] = ld_cg(b + i + k * n);
+    }
+#pragma unroll
+    for (int k = 0; k < T; ++k) {
+      if (i + k * n < nvec) {
+        const uint4 v = RED ? R::template vec<uint4>(x[k], y[k]) : x[k];
+        st_vec(o0 + i + k * n, v);
+        if (TWO) st_vec(o1 + i + k * n, v);
+      }
+    }
   }
 }
 
@@ -258,7 +285,7 @@ __device__ __forceinline__ void move_elems(const char* a, const char* b, char* o
 }
 
 template <class R>
-__device__ void move(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, int t, int n) {
+__device__ GC3_MOVE_ATTR void move(const char* a, const char* b, char* o0, char* o1, int64_t nbytes, int t, int n) {
   if (nbytes <= 0) return;
   if (!o0) {
     o0 = o1;
@@ -444,27 +471,46 @@ __device__ __forceinline__ bool is_send(int op) { return op == kOpSend || op == 
 
 // ------------------------------------------------------------------ LL op body
 // Lines of the incoming/outgoing message are distributed over the unit's threads; every thread
-// polls the flags of its own lines only. inl == nullptr: the incoming message is in place (direct)
-// or absent; outl == nullptr: the outgoing message goes to outd (direct, plain stores) or is absent.
+// polls the flags of its own lines only. The incoming message comes from inl (LL lines), inp (pulled
+// from the sender's span; its head flag was acquired before the op) or is in place (direct) or
+// absent; the outgoing one goes to outl (LL lines), outd (direct, plain stores) or nowhere (pulled).
 template <class R>
 __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl,
-                      uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, const Ctx& c, int t, int n) {
+                      const char* inp, uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, const Ctx& c, int t,
+                      int n) {
+  constexpr int U = 4;  // lines in flight per thread: their loads are issued together, then polled
   const int64_t lines_per_seg = tbytes >> 3;
   const int64_t nlines = lines_per_seg * count;
   const bool send = is_send(opcode);
-  for (int64_t k = t; k < nlines; k += n) {
-    const int j = static_cast<int>(k / lines_per_seg);
-    const int64_t off = ((k - j * lines_per_seg) << 3) + j * chunk_bytes;
-    char* src = src0 + off;
-    char* dst = dst0 + off;
-    uint2 msg = make_uint2(0, 0);
-    if (inl) {
-      uint4 l = ld_volatile_line(inl + k);
-      if (l.y != in_flag || l.w != in_flag) {
+  // ops that read their local span: send, rrc, rrcs, rrs, and rcs whose message is already in place
+  const bool reads_src = opcode == kOpSend || opcode == kOpRrc || opcode == kOpRrcs || opcode == kOpRrs ||
+                         (opcode == kOpRcs && !inl && !inp);
+  for (int64_t k0 = t; k0 < nlines; k0 += static_cast<int64_t>(U) * n) {
+    uint4 l[U];
+    uint2 own[U];
+    int64_t off[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + static_cast<int64_t>(u) * n;
+      if (k >= nlines) continue;
+      const int64_t j = k / lines_per_seg;
+      off[u] = ((k - j * lines_per_seg) << 3) + j * chunk_bytes;
+      if (inl) l[u] = ld_volatile_line(inl + k);
+      if (inp) {  // pulled: the sender's span, laid out like the local one
+        const uint2 m = ld_cg8(inp + off[u]);
+        l[u] = make_uint4(m.x, in_flag, m.y, in_flag);
+      }
+      if (reads_src) own[u] = ld_cg8(src0 + off[u]);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + static_cast<int64_t>(u) * n;
+      if (k >= nlines || !inl) continue;
+      if (l[u].y != in_flag || l[u].w != in_flag) {
         const uint64_t start = globaltimer();
         for (int it = 0;; ++it) {
-          l = ld_volatile_line(inl + k);
-          if (l.y == in_flag && l.w == in_flag) break;
+          l[u] = ld_volatile_line(inl + k);
+          if (l[u].y == in_flag && l[u].w == in_flag) break;
           if ((it & 255) == 255) {
             if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
             if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
@@ -474,30 +520,38 @@ __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
           }
         }
       }
-      msg = make_uint2(l.x, l.z);
     }
-    uint2 v;
-    switch (opcode) {
-      case kOpSend: v = ld_cg8(src); break;
-      case kOpRecv:
-        if (inl) st_vec8(dst, msg);
-        continue;
-      case kOpRrc: st_vec8(dst, R::template vec<uint2>(ld_cg8(src), msg)); continue;
-      case kOpRcs:
-        if (inl) {
-          v = msg;
-          st_vec8(src, v);
-        } else {
-          v = ld_cg8(src);  // direct: the message is already in the local span
-        }
-        break;
-      case kOpRrcs: v = R::template vec<uint2>(ld_cg8(src), msg); st_vec8(src, v); break;
-      case kOpRrs: v = R::template vec<uint2>(ld_cg8(src), msg); break;
-      default: continue;
-    }
-    if (send) {
-      if (outl) st_volatile_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag));
-      else st_vec8(outd + off, v);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = k0 + static_cast<int64_t>(u) * n;
+      if (k >= nlines) continue;
+      const bool has_msg = inl || inp;
+      const uint2 msg = has_msg ? make_uint2(l[u].x, l[u].z) : make_uint2(0, 0);
+      char* src = src0 + off[u];
+      char* dst = dst0 + off[u];
+      uint2 v;
+      switch (opcode) {
+        case kOpSend: v = own[u]; break;
+        case kOpRecv:
+          if (has_msg) st_vec8(dst, msg);
+          continue;
+        case kOpRrc: st_vec8(dst, R::template vec<uint2>(own[u], msg)); continue;
+        case kOpRcs:
+          if (has_msg) {
+            v = msg;
+            st_vec8(src, v);
+          } else {
+            v = own[u];  // direct: the message is already in the local span
+          }
+          break;
+        case kOpRrcs: v = R::template vec<uint2>(own[u], msg); st_vec8(src, v); break;
+        case kOpRrs: v = R::template vec<uint2>(own[u], msg); break;
+        default: continue;
+      }
+      if (send) {
+        if (outl) st_volatile_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag));
+        else if (outd) st_vec8(outd + off[u], v);
+      }
     }
   }
   return true;
@@ -529,6 +583,13 @@ __device__ __forceinline__ void unit_sync(int uw, int bar_id, int n) {
 
 template <class R, bool LL>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
+  // every rank's buffers of this launch, staged in shared memory once: ops index them by rank slot
+  // and buffer id (a dynamically indexed kernel parameter would be copied to local memory)
+  __shared__ char* s_bufs[kMaxLocalRanks * 3];
+#pragma unroll
+  for (int i = 0; i < kMaxLocalRanks * 3; ++i)
+    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / 3][i % 3];
+  __syncthreads();
   const int uw = a.unit_warps;
   const int n = uw * 32;                         // threads per unit
   const int uib = threadIdx.x / n;               // unit in this block
@@ -562,22 +623,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int64_t chunk_bytes = chunk_elems * R::kEsize;
   const uint64_t slots = static_cast<uint64_t>(a.slots);
   const uint64_t epoch = a.epoch;
-  // this rank's buffers and the send peer's (direct writes), selected with constant indices (a
-  // dynamically indexed kernel parameter would be copied to local memory)
-  char *b0 = nullptr, *b1 = nullptr, *b2 = nullptr, *q0 = nullptr, *q1 = nullptr, *q2 = nullptr;
-#pragma unroll
-  for (int i = 0; i < kMaxLocalRanks; ++i) {
-    if (i == tb.rank_slot) {
-      b0 = a.bufs[i][0];
-      b1 = a.bufs[i][1];
-      b2 = a.bufs[i][2];
-    }
-    if (i == tb.peer_slot) {
-      q0 = a.bufs[i][0];
-      q1 = a.bufs[i][1];
-      q2 = a.bufs[i][2];
-    }
-  }
+  char* const* const mine = s_bufs + 3 * tb.rank_slot;                          // this rank's buffers
+  char* const* const peer = s_bufs + 3 * (tb.peer_slot >= 0 ? tb.peer_slot : 0);  // send peer's (direct)
+  char* const* const rpeer = s_bufs + 3 * (tb.recv_slot >= 0 ? tb.recv_slot : 0); // receive peer's (pull)
   const DevChan* const cin = has_in ? a.chans + tb.chan_in + lane : nullptr;
   const DevChan* const cout = has_out ? a.chans + tb.chan_out + lane : nullptr;
   uint64_t rcvd = has_in ? *cin->mine : 0;
@@ -613,12 +661,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       const DevOp op = ops[s];
       const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
       const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
-      const bool ll_in = LL && recv && !in_d, ll_out = LL && send && !out_d;
+      const bool in_p = (op.direct & kInPull) != 0, out_p = (op.direct & kOutPull) != 0;
+      const bool in_fifo = recv && !in_d && !in_p, out_fifo = send && !out_d && !out_p;
+      const bool ll_in = LL && in_fifo, ll_out = LL && out_fifo;
       c.step = s;
       if (t == 0) stamp(q, 0);
       // (1) preconditions, polled in parallel
       bool ok = true;
-      if (t == 0 && send && !out_d) ok = wait_geq(cout->tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
+      if (t == 0 && out_fifo) ok = wait_geq(cout->tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
       if (t == 1 && recv && !ll_in) ok = wait_geq(cin->head, rcvd + 1, sys, c, 3);
       for (int d = t - 2; d >= 0 && d < op.ndeps; d += n - 2) {
         const DevDep dd = a.deps[op.dep_begin + d];
@@ -636,33 +686,44 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       if (!unit_and(ok, uw, bar_id, n)) return;
       if (t == 0) stamp(q, 1);
 
-      // (2) the transfer, with the reduction fused in
-      auto sel = [&](int b) { return b == 0 ? b0 : (b == 1 ? b1 : b2); };
-      auto selp = [&](int b) { return b == 0 ? q0 : (b == 1 ? q1 : q2); };
-      char* src = sel(op.src_buf) + op.src_off * chunk_bytes + t0_bytes;
-      char* dst = sel(op.dst_buf) + op.dst_off * chunk_bytes + t0_bytes;
-      char* peer_dst = out_d ? selp(op.dst_buf) + op.dst_off * chunk_bytes + t0_bytes : nullptr;
-      const char* in = recv && !in_d ? cin->fifo + static_cast<int64_t>(rcvd % slots) * cin->slot_bytes : nullptr;
-      char* out = send && !out_d ? cout->fifo + static_cast<int64_t>(sent % slots) * cout->slot_bytes : nullptr;
+      // (2) the transfer, with the reduction fused in. The incoming message is read from `in`
+      // (FIFO slot, or the sender's span when pulled; segment j at + j * in_stride) unless it is
+      // already in place; the outgoing one is written to `out` (FIFO slot, or the receiver's span
+      // when direct) unless it is pulled from this rank's span.
+      char* src = mine[op.src_buf] + op.src_off * chunk_bytes + t0_bytes;
+      char* dst = mine[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes;
+      const char* in = nullptr;
+      int64_t in_stride = tbytes;
+      if (in_fifo) in = cin->fifo + static_cast<int64_t>(rcvd % slots) * cin->slot_bytes;
+      if (in_p) {
+        in = rpeer[op.in_buf] + op.in_off * chunk_bytes + t0_bytes;
+        in_stride = chunk_bytes;
+      }
+      char* out = nullptr;
+      int64_t out_stride = tbytes;
+      if (out_fifo) out = cout->fifo + static_cast<int64_t>(sent % slots) * cout->slot_bytes;
+      if (out_d) {
+        out = peer[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes;
+        out_stride = chunk_bytes;
+      }
       if (ll_in || ll_out) {
         ok = ll_op<R>(op.opcode, op.count, src, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
-                      ll_out ? reinterpret_cast<uint4*>(out) : nullptr, peer_dst, static_cast<uint32_t>(rcvd + 1),
-                      static_cast<uint32_t>(sent + 1), c, t, n);
+                      in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
+                      static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), c, t, n);
       } else if (tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
                  ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
-                   reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(peer_dst) | static_cast<uintptr_t>(tbytes) |
-                   static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
+                   reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) | static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
         if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier
-          char* mo = out_d ? peer_dst : out;
-          const int64_t smo = out_d ? chunk_bytes : tbytes;
           fence_proxy_async_global();  // generic-proxy acquires above -> async-proxy reads
           switch (op.opcode) {
-            case kOpSend: tma_copy(tma, src, chunk_bytes, mo, smo, nullptr, 0, tbytes, op.count); break;
-            case kOpRecv: tma_copy(tma, in, tbytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
+            case kOpSend:
+              if (out) tma_copy(tma, src, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
+              break;
+            case kOpRecv: tma_copy(tma, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
             case kOpCopy: tma_copy(tma, src, chunk_bytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
             case kOpRcs:
-              if (in_d) tma_copy(tma, src, chunk_bytes, mo, smo, nullptr, 0, tbytes, op.count);
-              else tma_copy(tma, in, tbytes, src, chunk_bytes, mo, smo, tbytes, op.count);
+              if (!in_d) tma_copy(tma, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count);
+              else if (out) tma_copy(tma, src, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
               break;
             default: break;
           }
@@ -672,19 +733,21 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         for (int j = 0; j < op.count; ++j) {
           char* sj = src + j * chunk_bytes;
           char* dj = dst + j * chunk_bytes;
-          const char* mi = in ? in + j * tbytes : nullptr;
-          char* mo = out_d ? peer_dst + j * chunk_bytes : (out ? out + j * tbytes : nullptr);
+          const char* mi = in ? in + j * in_stride : nullptr;
+          char* mo = out ? out + j * out_stride : nullptr;
           switch (op.opcode) {
-            case kOpSend: move<R>(sj, nullptr, mo, nullptr, tbytes, t, n); break;
+            case kOpSend:
+              if (mo) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
+              break;
             case kOpRecv:
-              if (!in_d) move<R>(mi, nullptr, dj, nullptr, tbytes, t, n);
+              if (mi) move<R>(mi, nullptr, dj, nullptr, tbytes, t, n);
               break;
             case kOpCopy: move<R>(sj, nullptr, dj, nullptr, tbytes, t, n); break;
             case kOpReduce: move<R>(dj, sj, dj, nullptr, tbytes, t, n); break;
             case kOpRrc: move<R>(sj, mi, dj, nullptr, tbytes, t, n); break;
             case kOpRcs:
-              if (in_d) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
-              else move<R>(mi, nullptr, sj, mo, tbytes, t, n);
+              if (mi) move<R>(mi, nullptr, sj, mo, tbytes, t, n);
+              else if (mo) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
               break;
             case kOpRrcs: move<R>(sj, mi, sj, mo, tbytes, t, n); break;
             case kOpRrs: move<R>(sj, mi, nullptr, mo, tbytes, t, n); break;
@@ -694,10 +757,10 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       }
       if (t == 0) stamp(q, 2);
       if (!unit_and(ok, uw, bar_id, n)) return;
-      if (a.discard && in && !in_d) {
+      if (a.discard && in_fifo && !ll_in) {
         // the consumed slot is dead until the sender refills it: drop its lines from L2 so they are
         // never written back to HBM (the FIFO round trip stays on chip when the consumer is prompt)
-        const int64_t used = static_cast<int64_t>(op.count) * tbytes * (ll_in ? 2 : 1);
+        const int64_t used = static_cast<int64_t>(op.count) * tbytes;
         for (int64_t off = static_cast<int64_t>(t) * 128; off + 128 <= used; off += static_cast<int64_t>(n) * 128)
           asm volatile("discard.global.L2 [%0], 128;" ::"l"(in + off) : "memory");
         unit_sync(uw, bar_id, n);

@@ -95,7 +95,7 @@ struct Config {
   int64_t tile_bytes = 0;            // 0: automatic
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
   int trace = 0;                     // record the in-kernel %globaltimer event log
-  int direct = 1;                    // write dead receive spans directly (see direct_messages)
+  int direct = 3;                    // bit 0: direct messages, bit 1: pulled messages (direct_messages)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
   int tma = 1;                       // bulk (TMA) copies for pure-copy ops on same-device peers
   int balance = 1;                   // per-component lane multipliers (lane_multipliers)
@@ -112,7 +112,7 @@ Config config_from_env() {
   c.tile_bytes = env_int("GC3_TILE_BYTES", c.tile_bytes);
   c.timeout_ms = env_int("GC3_TIMEOUT_MS", c.timeout_ms);
   c.trace = static_cast<int>(env_int("GC3_TRACE", 0));
-  c.direct = static_cast<int>(env_int("GC3_DIRECT", 1));
+  c.direct = static_cast<int>(env_int("GC3_DIRECT", c.direct));
   c.unit_warps = static_cast<int>(env_int("GC3_UNIT_WARPS", c.unit_warps));
   c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
   c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
@@ -442,19 +442,30 @@ ncclResult_t peer_arena(Comm* c, int id, int r, char*& out) {
   return ncclSuccess;
 }
 
-// Builds the device plan of IR `id` on `dev` for the ranks the clique hosts there.
-// Direct messages. A receive that only stores the message (recv, rcs) may have it written by the
-// sender straight into the receive's local span when no op of the receiving rank touches that span
-// before the receive, and none touches it unordered with it: the span is then dead until the
-// receive, so writing it early is indistinguishable from writing it at the receive. Order is the
-// happens-before relation of sequential execution, declared deps and the k-th send -> k-th receive
-// matching (the graph of scheduler.hpp:652-717). The sender addresses the span through its own
-// op's dst fields (lowering.hpp:71), which must name it exactly.
-// Returns flags[rank][tb index][step] with kInDirect on such receives and kOutDirect on their sends.
-std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p) {
+// Message transports, decided statically from the happens-before relation of the program:
+// sequential execution, declared deps and the k-th send -> k-th receive matching (the graph of
+// scheduler.hpp:652-717). An edge a -> b means a's data movement is finished before b's starts.
+//
+// Direct (kInDirect / kOutDirect). A receive that only stores the message (recv, rcs) may have it
+// written by the sender straight into the receive's local span x when every other access of x on
+// the receiving rank is ordered with that write: before the send, or after the receive. The sender
+// addresses x through its own op's dst fields (lowering.hpp:71), which must name it exactly.
+//
+// Pull (kInPull / kOutPull). A message whose content is a span Y the sender stores (send reads Y;
+// rcs and rrcs write the message to Y) may stay there: the receive reads Y from the sender's
+// buffers once the sender has published it, provided every write to Y on the sending rank is
+// ordered with that window: before the send, or after the receive. This removes the FIFO round trip
+// of reducing receives (rrc, rrcs, rrs), which can never be direct.
+//
+// A receive op u that writes a span (recv, rcs) may have its data written at its sender's op x(u)
+// (if that message is direct), so "after the receive" is checked at both u and x(u).
+// Returns flags[rank][tb index][step]; pull_src (optional) gets the sender span (buf, off) of
+// every kInPull receive.
+std::vector<std::vector<std::vector<uint8_t>>> direct_messages(
+    const Program& p, bool pull, std::vector<std::vector<std::vector<std::pair<int, int>>>>* pull_src) {
   const int R = p.ranks();
   std::vector<std::vector<std::vector<uint8_t>>> flags(R);
-  std::vector<std::vector<int>> base(R);  // unit index of (rank, tb, 0)
+  std::vector<std::vector<int>> base(R);  // node index of (rank, tb, 0)
   int n = 0;
   for (int r = 0; r < R; ++r) {
     flags[r].resize(p.gpus[r].tbs.size());
@@ -463,6 +474,11 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p)
       base[r].push_back(n);
       n += static_cast<int>(p.gpus[r].tbs[t].ops.size());
     }
+  }
+  if (pull_src) {
+    pull_src->assign(R, {});
+    for (int r = 0; r < R; ++r)
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) (*pull_src)[r].emplace_back(p.gpus[r].tbs[t].ops.size(), std::make_pair(-1, -1));
   }
   if (n == 0 || n > 65536) return flags;
   std::vector<std::vector<int>> succ(n);
@@ -484,10 +500,15 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p)
         if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0) conns[{tb.recv_peer, r, tb.channel}].second.push_back({r, static_cast<int>(t), static_cast<int>(s)});
       }
     }
+  std::vector<int> sender_of(n, -1);  // receive node -> matched send node
   for (auto& [key, c] : conns) {
     if (c.first.size() != c.second.size()) return flags;  // unbalanced: no direct messages at all
-    for (size_t k = 0; k < c.first.size(); ++k)
-      succ[base[c.first[k].rank][c.first[k].tb] + c.first[k].step].push_back(base[c.second[k].rank][c.second[k].tb] + c.second[k].step);
+    for (size_t k = 0; k < c.first.size(); ++k) {
+      const int su = base[c.first[k].rank][c.first[k].tb] + c.first[k].step;
+      const int ru = base[c.second[k].rank][c.second[k].tb] + c.second[k].step;
+      succ[su].push_back(ru);
+      sender_of[ru] = su;
+    }
   }
   // reachability (reverse topological order); a cycle means no static order, so nothing is direct
   std::vector<int> indeg(n, 0), order;
@@ -516,20 +537,40 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p)
   auto overlaps = [&](const Span& x, const Span& y) {
     return storage(x.b) == storage(y.b) && x.off < y.off + y.count && y.off < x.off + x.count;
   };
-  auto accesses = [&](const Op& op, std::vector<Span>& out) {  // local reads + writes (lowering.hpp:96-119)
+  // local reads + writes (lowering.hpp:96-119); writes only with `writes_only`
+  auto accesses = [&](const Op& op, bool writes_only, std::vector<Span>& out) {
     out.clear();
     switch (op.op) {
-      case Opcode::send: case Opcode::rrs: out.push_back({op.src_buf, op.src_off, op.count}); break;
+      case Opcode::send: case Opcode::rrs:
+        if (!writes_only) out.push_back({op.src_buf, op.src_off, op.count});
+        break;
       case Opcode::recv: out.push_back({op.dst_buf, op.dst_off, op.count}); break;
       case Opcode::rcs: case Opcode::rrcs: out.push_back({op.src_buf, op.src_off, op.count}); break;
       case Opcode::copy: case Opcode::reduce: case Opcode::rrc:
-        out.push_back({op.src_buf, op.src_off, op.count});
+        if (!writes_only) out.push_back({op.src_buf, op.src_off, op.count});
         out.push_back({op.dst_buf, op.dst_off, op.count});
         break;
       default: break;
     }
   };
+  // is every access u (on `rank`) of span x ordered with the window [send su, receive ru]?
   std::vector<Span> acc;
+  auto window_clear = [&](int rank, int self, const Span& x, int su, int ru, bool writes_only) {
+    for (size_t t = 0; t < p.gpus[rank].tbs.size(); ++t)
+      for (size_t s = 0; s < p.gpus[rank].tbs[t].ops.size(); ++s) {
+        const int u = base[rank][t] + static_cast<int>(s);
+        if (u == self) continue;
+        const Op& op = p.gpus[rank].tbs[t].ops[s];
+        accesses(op, writes_only, acc);
+        for (const Span& y : acc) {
+          if (!overlaps(x, y)) continue;
+          if (!reaches(ru, u) && !reaches(u, su)) return false;
+          const bool msg_write = (op.op == Opcode::recv || op.op == Opcode::rcs) && sender_of[u] >= 0;
+          if (msg_write && !reaches(sender_of[u], su) && !reaches(ru, sender_of[u])) return false;
+        }
+      }
+    return true;
+  };
   for (auto& [key, c] : conns) {
     for (size_t k = 0; k < c.second.size(); ++k) {
       const Ref rx = c.second[k], tx = c.first[k];
@@ -538,19 +579,28 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p)
       if (rop.op != Opcode::recv && rop.op != Opcode::rcs) continue;
       const Span x = rop.op == Opcode::recv ? Span{rop.dst_buf, rop.dst_off, rop.count} : Span{rop.src_buf, rop.src_off, rop.count};
       if (storage(sop.dst_buf) != storage(x.b) || sop.dst_off != x.off || sop.count != x.count) continue;
-      const int ru = base[rx.rank][rx.tb] + rx.step;
-      bool ok = true;
-      for (size_t t = 0; t < p.gpus[rx.rank].tbs.size() && ok; ++t)
-        for (size_t s = 0; s < p.gpus[rx.rank].tbs[t].ops.size() && ok; ++s) {
-          const int u = base[rx.rank][t] + static_cast<int>(s);
-          if (u == ru) continue;
-          accesses(p.gpus[rx.rank].tbs[t].ops[s], acc);
-          for (const Span& y : acc)
-            if (overlaps(x, y) && !reaches(ru, u)) ok = false;  // before or unordered with the receive
-        }
-      if (ok) {
+      const int ru = base[rx.rank][rx.tb] + rx.step, su = base[tx.rank][tx.tb] + tx.step;
+      if (window_clear(rx.rank, ru, x, su, ru, false)) {
         flags[rx.rank][rx.tb][rx.step] |= kInDirect;
         flags[tx.rank][tx.tb][tx.step] |= kOutDirect;
+      }
+    }
+  }
+  if (!pull) return flags;
+  for (auto& [key, c] : conns) {
+    for (size_t k = 0; k < c.second.size(); ++k) {
+      const Ref rx = c.second[k], tx = c.first[k];
+      if (flags[rx.rank][rx.tb][rx.step] & kInDirect) continue;
+      const Op& rop = p.gpus[rx.rank].tbs[rx.tb].ops[rx.step];
+      const Op& sop = p.gpus[tx.rank].tbs[tx.tb].ops[tx.step];
+      if (sop.op != Opcode::send && sop.op != Opcode::rcs && sop.op != Opcode::rrcs) continue;  // rrs stores nothing
+      if (sop.count != rop.count) continue;
+      const Span y{sop.src_buf, sop.src_off, sop.count};
+      const int ru = base[rx.rank][rx.tb] + rx.step, su = base[tx.rank][tx.tb] + tx.step;
+      if (window_clear(tx.rank, su, y, su, ru, true)) {
+        flags[rx.rank][rx.tb][rx.step] |= kInPull;
+        flags[tx.rank][tx.tb][tx.step] |= kOutPull;
+        if (pull_src) (*pull_src)[rx.rank][rx.tb][rx.step] = {static_cast<int>(sop.src_buf), sop.src_off};
       }
     }
   }
@@ -564,7 +614,7 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(const Program& p)
 // passes its units make per tile (a direct receive moves nothing; its sender does the writing).
 std::vector<std::vector<int>> lane_multipliers(const Program& p) {
   const int R = p.ranks();
-  const auto direct = direct_messages(p);
+  const auto direct = direct_messages(p, true, nullptr);
   std::vector<int> base(R + 1, 0);
   for (int r = 0; r < R; ++r) base[r + 1] = base[r] + static_cast<int>(p.gpus[r].tbs.size());
   std::vector<int> parent(base[R]);
@@ -581,14 +631,18 @@ std::vector<std::vector<int>> lane_multipliers(const Program& p) {
       int w = 0;
       for (size_t s = 0; s < tb.ops.size(); ++s) {
         const Op& op = tb.ops[s];
-        const bool in_d = !direct.empty() && (direct[r][t][s] & kInDirect);
+        const uint8_t f = direct.empty() ? 0 : direct[r][t][s];
+        const bool in_d = f & kInDirect, out_p = f & kOutPull;
+        // reads + writes of the unit (the message: read unless direct-in, written unless pulled)
         int passes = 0;
         switch (op.op) {
-          case Opcode::send: case Opcode::copy: passes = 2; break;
+          case Opcode::send: passes = out_p ? 0 : 2; break;
+          case Opcode::copy: passes = 2; break;
           case Opcode::recv: passes = in_d ? 0 : 2; break;
-          case Opcode::reduce: case Opcode::rrc: case Opcode::rrs: passes = 3; break;
-          case Opcode::rcs: passes = in_d ? 2 : 3; break;
-          case Opcode::rrcs: passes = 4; break;
+          case Opcode::reduce: passes = 3; break;
+          case Opcode::rrc: case Opcode::rrs: passes = 3; break;
+          case Opcode::rcs: passes = (in_d ? 1 : 2) + (out_p ? 0 : 1); break;
+          case Opcode::rrcs: passes = 3 + (out_p ? 0 : 1); break;
           default: break;
         }
         w += passes * op.count;
@@ -633,7 +687,13 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   std::vector<DevChan> chans;
   plan.sys_scope = false;
   // direct messages only between ranks of this launch: the sender needs the receiver's buffers
-  const auto direct = c0->cfg.direct ? direct_messages(p) : std::vector<std::vector<std::vector<uint8_t>>>();
+  std::vector<std::vector<std::vector<std::pair<int, int>>>> pull_src;
+  auto direct = c0->cfg.direct ? direct_messages(p, (c0->cfg.direct & 2) != 0, &pull_src)
+                               : std::vector<std::vector<std::vector<uint8_t>>>();
+  if (!(c0->cfg.direct & 1))  // pulls only: drop the direct flags
+    for (auto& g : direct)
+      for (auto& tb : g)
+        for (auto& f : tb) f &= static_cast<uint8_t>(~(kInDirect | kOutDirect));
   auto slot_of = [&](int rank) {
     for (size_t i = 0; i < plan.ranks.size(); ++i)
       if (plan.ranks[i] == rank) return static_cast<int>(i);
@@ -649,8 +709,9 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         if (direct.empty() || slot_of(r) < 0) continue;
         for (size_t s = 0; s < tb.ops.size(); ++s) {
           const uint8_t f = direct[r][t][s];
-          if ((f & kInDirect) && tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0) eff[r][t][s] |= kInDirect;
-          if ((f & kOutDirect) && tb.send_peer >= 0 && slot_of(tb.send_peer) >= 0) eff[r][t][s] |= kOutDirect;
+          if ((f & (kInDirect | kInPull)) && tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0) eff[r][t][s] |= f & (kInDirect | kInPull);
+          if ((f & (kOutDirect | kOutPull)) && tb.send_peer >= 0 && slot_of(tb.send_peer) >= 0)
+            eff[r][t][s] |= f & (kOutDirect | kOutPull);
         }
       }
     }
@@ -688,7 +749,8 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       weight += mult[r][t];
       d.chan_in = d.chan_out = -1;
       d.peer_slot = tb.send_peer >= 0 ? slot_of(tb.send_peer) : -1;
-      const bool in_local = tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0;
+      d.recv_slot = tb.recv_peer >= 0 ? slot_of(tb.recv_peer) : -1;
+      const bool in_local = d.recv_slot >= 0;
       for (size_t s = 0; s < tb.ops.size(); ++s) {
         const Op& op = tb.ops[s];
         DevOp o{};
@@ -696,6 +758,12 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
           const uint8_t f = direct[r][t][s];
           if ((f & kInDirect) && in_local) o.direct |= kInDirect;
           if ((f & kOutDirect) && d.peer_slot >= 0) o.direct |= kOutDirect;
+          if ((f & kInPull) && in_local) {
+            o.direct |= kInPull;
+            o.in_buf = static_cast<uint8_t>(pull_src[r][t][s].first);
+            o.in_off = pull_src[r][t][s].second;
+          }
+          if ((f & kOutPull) && d.peer_slot >= 0) o.direct |= kOutPull;
         }
         o.opcode = static_cast<uint8_t>(op.op);
         o.src_buf = static_cast<uint8_t>(op.src_buf);
@@ -908,7 +976,7 @@ bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std:
           const int dn = static_cast<int>(p.gpus[u.r].tbs[ti].ops.size());
           if (du.pos < position(tile / du.lt, d.step, dn, du.ntl) + 1) ok = false;
         }
-        const bool direct_out = !direct.empty() && (direct[u.r][u.t][step] & kOutDirect);
+        const bool direct_out = !direct.empty() && (direct[u.r][u.t][step] & (kOutDirect | kOutPull));
         if (ok && op_receives(op.op)) {
           const auto& c = conn[{tb.recv_peer, u.r, tb.channel, u.lane}];
           if (c.first <= c.second) ok = false;
@@ -1749,7 +1817,7 @@ ncclResult_t gc3IrArenaLayout(gc3Ir_t ir, int rank, int lanes, int slots, int64_
 
 ncclResult_t gc3IrDirectMessages(gc3Ir_t ir, char** json) {
   if (!ir || !json) return ncclInvalidArgument;
-  const auto f = direct_messages(ir->p);
+  const auto f = direct_messages(ir->p, true, nullptr);
   std::ostringstream os;
   os << "[";
   for (size_t r = 0; r < f.size(); ++r) {

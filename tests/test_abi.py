@@ -73,15 +73,19 @@ def test_arena_layout_shapes(gc3lib):
 
 def test_direct_message_analysis(gc3lib):
     """AllToAll / AllGather receives land in spans no earlier op touches: all direct. Ring
-    AllReduce receives either reduce or overwrite spans the rank accessed before: none direct."""
+    AllReduce / ReduceScatter reducing receives combine with a live span: never direct; the
+    AllReduce broadcast receives (rcs / recv) overwrite spans whose earlier uses all happen before
+    the matching send: direct."""
     import json
-    for name, expect_all in [("twostep_a2a_1x8", True), ("ring_ag_8", True), ("ring_ar_8_ch1", False), ("ring_rs_8", False)]:
+    for name, direct_ops in [("twostep_a2a_1x8", {"recv"}), ("ring_ag_8", {"recv", "rcs"}),
+                             ("ring_ar_8_ch1", {"recv", "rcs"}), ("ring_rs_8", set()),
+                             ("hier_ar_2x4_par1", {"recv", "rcs"})]:
         irj = json.loads(read_ir(name))
         flags = gc3lib.IR(read_ir(name)).direct_messages()
-        recvs = [(r, t, s) for r, g in enumerate(irj["gpus"]) for t, tb in enumerate(g["threadblocks"])
+        recvs = [(r, t, s, o["opcode"]) for r, g in enumerate(irj["gpus"]) for t, tb in enumerate(g["threadblocks"])
                  for s, o in enumerate(tb["ops"]) if o["opcode"] in ("recv", "rcs", "rrc", "rrcs", "rrs")]
-        direct = [flags[r][t][s] & 1 for r, t, s in recvs]
-        assert all(direct) if expect_all else not any(direct), name
+        for r, t, s, op in recvs:
+            assert bool(flags[r][t][s] & 1) == (op in direct_ops), (name, r, t, s, op)
     # two-step: the scratch staging recv is direct, and so is the final coalesced receive
     f = gc3lib.IR(read_ir("twostep_a2a_2x4")).direct_messages()
     assert sum(x & 1 for g in f for tb in g for x in tb) == 56
