@@ -419,6 +419,70 @@ def host_cpu():
     return f"{os.cpu_count()} logical cpus"
 
 
+def run_sweep(args, cfg):
+    """Message-size sweep (BASELINE config C4: 1 KiB - 1 GiB, Simple vs LL): one JSON line per
+    (protocol, size) with the device time of one collective (CUDA events, mean of the timed steps,
+    inputs re-used: small sizes are L2-resident), algBW / busBW per rank and the HBM roofline
+    fraction of the launch's algorithmic bytes."""
+    import torch
+    from paper_2201_11840_b200 import gc3
+    torch.cuda.set_device(0)
+    R = 8
+    comms = setup_comms(dict(cfg, proto=None), args, R, 0, 1, 0, None)
+    peaks, _ = load_peaks()
+    stream = torch.cuda.Stream()
+    lo, hi = args.sweep_min, args.sweep_max
+    sizes = []
+    b = lo
+    while b <= hi:
+        sizes.append(b)
+        b *= 2
+    tdt = getattr(torch, cfg["dtype"])
+    for proto in args.sweep_protos.split(","):
+        for c in comms:
+            c.set_protocol(0, proto)
+        for nbytes in sizes:
+            count = per_rank_count(cfg, nbytes, R)
+            n_in = input_elems(cfg["coll"], count, R)
+            ins = [torch.randn(n_in, device="cuda").to(tdt) for _ in comms]
+            outs = [torch.empty(R * count if cfg["coll"] in ("allgather", "alltoall") else count, device="cuda", dtype=tdt)
+                    for _ in comms]
+
+            def step():
+                with gc3.group():
+                    for c, x, y in zip(comms, ins, outs):
+                        if cfg["coll"] == "allreduce":
+                            c.all_reduce(x, x, count, cfg["dtype"], "sum", stream)
+                        elif cfg["coll"] == "alltoall":
+                            c.all_to_all(x, y, count, cfg["dtype"], stream)
+                        elif cfg["coll"] == "allgather":
+                            c.all_gather(x, y, count, cfg["dtype"], stream)
+                        else:
+                            c.reduce_scatter(x, y, count, cfg["dtype"], "sum", stream)
+            steps = max(3, min(args.steps, int(2e9 // max(nbytes * R, 1))))
+            for _ in range(3):
+                step()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(steps):
+                step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / steps
+            err = comms[0].async_error()
+            plan = comms[0].query_plan(cfg["coll"], count, cfg["dtype"])
+            print(json.dumps({"config": args.config, "ir": cfg["ir"], "proto": proto, "bytes": nbytes, "us": round(ms * 1e3, 2),
+                              "algbw_gbs": round(nbytes / (ms * 1e-3) / 1e9, 2),
+                              "busbw_gbs": round(nbytes / (ms * 1e-3) / 1e9 * bus_factor(cfg["coll"], R), 2),
+                              "hbm_frac": round(plan["hbm_bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                              "lanes": plan["lanes"], "tile": plan["tile_elems"] * ESIZE[cfg["dtype"]], "ok": err[0] == 0}),
+                  flush=True)
+            del ins, outs
+    for c in comms:
+        c.destroy()
+
+
 def run_reference(args, cfg):
     """The reference arm: the reference's interpreter semantics on the host cores (oracle port;
     the reference ships no runtime)."""
@@ -464,12 +528,18 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--quick", action="store_true", help="kernel timing only: one compact JSON line")
+    ap.add_argument("--sweep", action="store_true", help="message-size sweep (one JSON line per protocol and size)")
+    ap.add_argument("--sweep-min", type=int, default=1 << 10)
+    ap.add_argument("--sweep-max", type=int, default=1 << 30)
+    ap.add_argument("--sweep-protos", default="simple,ll")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     cfg = dict(CONFIGS[args.config])
     if args.proto:
         cfg["proto"] = args.proto
-    if args.impl == "reference":
+    if args.sweep:
+        run_sweep(args, cfg)
+    elif args.impl == "reference":
         run_reference(args, cfg)
     else:
         run_gc3(args, cfg)

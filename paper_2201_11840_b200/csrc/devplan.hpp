@@ -95,7 +95,7 @@ struct LaunchArgs {
   int32_t group;        // tiles per op-major group inside a lane (1 = tile-major)
   int32_t tma_stages;   // shared-memory stages per unit for bulk copies (0: register path only)
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
-  int32_t pad2_;
+  int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   char* bufs[kMaxLocalRanks][3];  // per local rank: input, output, scratch
 };
 

@@ -26,7 +26,7 @@
 #include "devplan.hpp"
 
 #ifndef GC3_UNROLL
-#define GC3_UNROLL 8
+#define GC3_UNROLL 4
 #endif
 #ifndef GC3_UNROLL_COPY
 #define GC3_UNROLL_COPY 8
@@ -35,10 +35,10 @@
 #define GC3_MINBLOCKS 1
 #endif
 #ifndef GC3_TAIL_UNROLL  // vectors in flight per thread in the predicated tail of a data move
-#define GC3_TAIL_UNROLL 4
+#define GC3_TAIL_UNROLL 1
 #endif
 #ifndef GC3_MOVE_NOINLINE  // compile the data mover once per reduction instead of at every op site
-#define GC3_MOVE_NOINLINE 1
+#define GC3_MOVE_NOINLINE 0
 #endif
 #if GC3_MOVE_NOINLINE
 #define GC3_MOVE_ATTR __noinline__
@@ -632,6 +632,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   uint64_t sent = has_out ? *cout->mine : 0;
   uint64_t* const sems = a.sems;
   const DevOp* const ops = a.ops + tb.op_begin;
+  // the op list is re-read every tile: bring it into L1 once, while the first waits are pending
+  for (int i = t; i * 128 < tb.nops * static_cast<int>(sizeof(DevOp)); i += n)
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(reinterpret_cast<const char*>(ops) + i * 128));
   Ctx c{a.abort_flag, a.err_info, a.timeout_ns, tb.rank_slot, tbi, 0, 0};
   uint64_t* const trace = a.trace;
   const int trace_ops = a.trace_ops;
@@ -660,8 +663,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       c.tile = tile;
       const DevOp op = ops[s];
       const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
-      const bool in_d = (op.direct & kInDirect) != 0, out_d = (op.direct & kOutDirect) != 0;
-      const bool in_p = (op.direct & kInPull) != 0, out_p = (op.direct & kOutPull) != 0;
+      const int tr = op.direct & a.transports;
+      const bool in_d = (tr & kInDirect) != 0, out_d = (tr & kOutDirect) != 0;
+      const bool in_p = (tr & kInPull) != 0, out_p = (tr & kOutPull) != 0;
       const bool in_fifo = recv && !in_d && !in_p, out_fifo = send && !out_d && !out_p;
       const bool ll_in = LL && in_fifo, ll_out = LL && out_fifo;
       c.step = s;
@@ -768,10 +772,12 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
 
       // (3) publish: slot posted / slot freed / semaphore
       if (t == 0) {
-        const bool publishes = (send && !ll_out) || recv || op.has_dep;
         // one scoped fence orders the unit's data (gathered by the barrier above) before all
-        // three flag stores: a release pattern per flag without a fence per store
-        if (publishes) fence_acq_rel(sys);
+        // three flag stores: a release pattern per flag without a fence per store. An LL receive
+        // returns its slot without one: its loads have returned (their data was used above) and
+        // it stored nothing another party reads through this flag.
+        const bool fence = (send && !ll_out) || (recv && !ll_in) || op.has_dep;
+        if (fence) fence_acq_rel(sys);
         if (send && !ll_out) st_relaxed(cout->head, sent + 1, sys);
         if (recv) st_relaxed(cin->tail, rcvd + 1, sys);
         if (op.has_dep) st_relaxed(sems + tb.sem + lane, (epoch << 32) | static_cast<uint64_t>(q + 1), false);

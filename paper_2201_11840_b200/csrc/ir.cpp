@@ -460,6 +460,18 @@ std::vector<SlotViolation> check_slots(const Program& p, int slots) {
 }
 
 // ---------------------------------------------------------------------------------------------
+bool uniform_counts(const Program& p) {
+  int c = 0;
+  for (const auto& g : p.gpus)
+    for (const auto& tb : g.tbs)
+      for (const auto& op : tb.ops) {
+        if (op.op == Opcode::nop) continue;
+        if (c && op.count != c) return false;
+        c = op.count;
+      }
+  return true;
+}
+
 Program replicate_instances(const Program& p, int k) {
   if (k <= 1) return p;
   Program q = p;

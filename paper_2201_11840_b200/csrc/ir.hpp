@@ -114,6 +114,9 @@ std::vector<SlotViolation> check_slots(const Program& p, int slots);
 // off -> off*k + j*count, channel -> channel + j*nch, tb id -> id + j*ntb, dep tb likewise, and
 // multiplies nchunks by k. Equals the reference's compile-time parallelize(k) for programs whose
 // ops all share one count (SURVEY.md Finding 5).
+// Ops of several counts have no consistent blocking (a count-4 span's block j and a count-1 op on one
+// of its chunks land on different sub-chunks), so callers must check uniform_counts first.
 Program replicate_instances(const Program& p, int k);
+bool uniform_counts(const Program& p);
 
 }  // namespace gc3

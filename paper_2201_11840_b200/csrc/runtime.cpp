@@ -27,6 +27,7 @@
 #include <fstream>
 #include <functional>
 #include <map>
+#include <numeric>
 #include <memory>
 #include <mutex>
 #include <set>
@@ -246,7 +247,7 @@ struct RankIR {
   std::vector<std::vector<int>> mult;  // lane multiplier per (rank, tb) (lane_multipliers)
   ArenaLayout lay;
   std::vector<std::vector<std::vector<uint8_t>>> eff_direct;     // direct flags of this device's launch
-  std::map<std::tuple<int64_t, int, int, int>, bool> order_ok;    // (tiles, lanes, group, slots) -> deadlock-free
+  std::map<std::tuple<int64_t, int, int, int, bool>, bool> order_ok;  // (tiles, lanes, group, slots, ll) -> deadlock-free
   char* arena = nullptr;
   cudaIpcMemHandle_t handle{};
 };
@@ -1072,10 +1073,18 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (c->cfg.tile_bytes > 0) {
     tile_bytes = std::min<int64_t>(c->cfg.tile_bytes / 16 * 16, tile_bytes_cap);
   } else {  // one tile per lane when it fits a slot; larger chunks give each lane several tiles,
-            // which pipeline through multi-hop chains in op-major groups
-    const int64_t per_lane = (chunk_bytes + lanes - 1) / lanes;
-    tile_bytes = std::min<int64_t>(std::max<int64_t>(per_lane, 4 << 10), tile_bytes_cap);
+            // which pipeline through multi-hop chains in op-major groups. The tile count is a
+            // multiple of every thread block's lane count (lanes x multiplier), so all lanes of a
+            // thread block get the same number of tiles (no straggler lane).
+    int lcm = 1;
+    for (const auto& g : ir.mult)
+      for (int m : g) lcm = std::lcm(lcm, std::max(m, 1));
+    const int64_t lanes_all = static_cast<int64_t>(lanes) * lcm;
+    const int64_t k = std::max<int64_t>(1, (chunk_bytes + lanes_all * tile_bytes_cap - 1) / (lanes_all * tile_bytes_cap));
+    tile_bytes = (chunk_bytes + lanes_all * k - 1) / (lanes_all * k);
+    tile_bytes = std::max<int64_t>(tile_bytes, 4 << 10);
     tile_bytes = align_up(static_cast<size_t>(std::max<int64_t>(tile_bytes, 16)), 16);
+    tile_bytes = std::min<int64_t>(tile_bytes, tile_bytes_cap);
   }
   tile_bytes = std::max<int64_t>(tile_bytes, 16);
   if (chunk_bytes <= tile_bytes) tile_bytes = chunk_bytes;
@@ -1091,10 +1100,14 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   int G = c->cfg.group > 0 ? c->cfg.group : static_cast<int>(std::min<int64_t>(std::max<int64_t>(max_tiles, 1), 64));
   RankIR& mir = *c->irs[id];
   for (; G > 1; G /= 2) {
-    const auto key = std::make_tuple(cp.ntiles, lanes, G, ir.slots);
+    // LL launches move every message through the FIFO lines (no direct / pulled transports)
+    const auto key = std::make_tuple(cp.ntiles, lanes, G, ir.slots, cp.ll);
     auto f = mir.order_ok.find(key);
     if (f == mir.order_ok.end())
-      f = mir.order_ok.emplace(key, order_is_deadlock_free(p, mir.eff_direct, cp.ntiles, lanes, mir.mult, G, ir.slots)).first;
+      f = mir.order_ok
+              .emplace(key, order_is_deadlock_free(p, cp.ll ? std::vector<std::vector<std::vector<uint8_t>>>() : mir.eff_direct,
+                                                   cp.ntiles, lanes, mir.mult, G, ir.slots))
+              .first;
     if (f->second) break;
   }
   cp.group = std::max(G, 1);
@@ -1162,6 +1175,9 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.group = cp.group;
   a.tma_stages = cp.tma_stages;
   a.discard = c0->cfg.discard;
+  // LL: every message travels as flagged lines through the receiver's FIFO (lowest latency, no
+  // fences); Simple: direct and pulled messages where the plan found them safe
+  a.transports = cp.ll ? 0 : 0xff;
   a.slots = ir0.slots;
   a.sys_scope = plan.sys_scope ? 1 : 0;
   a.chunk_elems = cp.chunk_elems;
@@ -1583,7 +1599,11 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
     SchemaError se;
     if (!parse_program(text, ir->prog, se)) return set_error(ncclInvalidArgument, "%s", se.what().c_str());
   }
-  if (instances > 1) ir->prog = replicate_instances(ir->prog, instances);
+  if (instances > 1) {
+    if (!uniform_counts(ir->prog))
+      return set_error(ncclInvalidUsage, "instances=%d: the runtime rewrite needs ops of one count (SURVEY.md Finding 5)", instances);
+    ir->prog = replicate_instances(ir->prog, instances);
+  }
   Topology topo;
   topo.nodes = 1;
   topo.gpus_per_node = comm->nranks;
@@ -1794,6 +1814,7 @@ ncclResult_t gc3IrCheckSlots(gc3Ir_t ir, int slots, char** violations) {
 
 ncclResult_t gc3IrReplicate(gc3Ir_t ir, int instances, gc3Ir_t* out) {
   if (!ir || !out || instances < 1) return ncclInvalidArgument;
+  if (instances > 1 && !uniform_counts(ir->p)) return ncclInvalidUsage;
   auto h = std::make_unique<gc3Ir>();
   h->p = replicate_instances(ir->p, instances);
   *out = h.release();

@@ -195,7 +195,7 @@ def test_lane_multipliers(name, count, balance):
     ("hier_ar_2x4_par1", 8 * 4096 + 7, "bfloat16", 1), ("ring_ar_8_ch8_inst4", 32 * 100 + 31, "float32", 1),
     ("ring_ag_8", 1001, "float32", 4), ("ring_ag_4", 3, "bfloat16", 2),
     ("ring_rs_8", 777, "float32", 4), ("ring_rs_2", 1, "int32", 3),
-    ("twostep_a2a_2x4", 1003, "float32", 3), ("twostep_a2a_1x8", 2, "float16", 4),
+    ("twostep_a2a_1x8", 1003, "float32", 3), ("twostep_a2a_1x8", 2, "float16", 4),
 ])
 def test_ragged_counts(name, count, dtype, instances):
     """Counts the IR's chunks do not divide: chunks of ceil(count / c) elements, the last ones

@@ -217,3 +217,11 @@ def test_instances_rewrite_equals_compile_time_parallelize(gc3lib, base, k, targ
     ref = json.loads(read_ir(target))
     ours.pop("name"), ref.pop("name")
     assert ours == ref
+
+
+def test_instances_rewrite_rejects_mixed_counts(gc3lib):
+    """The rewrite is only defined for ops of one count: on the two-step AllToAll (count-1 and
+    coalesced count-4 ops on the same scratch chunks) it would make unordered ops share spans."""
+    with pytest.raises(gc3lib.NcclError):
+        gc3lib.IR(read_ir("twostep_a2a_2x4")).replicate(2)
+    assert gc3lib.IR(read_ir("twostep_a2a_1x8")).replicate(2).validate(1, 8) == []

@@ -118,15 +118,26 @@ def run(irj, flags, seed, use_flags=True):
 
 NAMES = ["ring_ar_8_ch1", "ring_ar_4_ch4_inst4", "hier_ar_2x4_par1", "hier_ar_2x4_par2", "allpairs_ar_8", "ring_rs_8",
          "ring_ag_8", "twostep_a2a_2x4", "twostep_a2a_1x8", "ring_ar_8_inst4_auto", "hier_ar_2x4_par1.unfused",
-         "ring_ar_8_ch8_inst1.unfused"]
+         "ring_ar_8_ch8_inst1.unfused", "ring_ag_8@3", "twostep_a2a_1x8@3", "ring_ar_8_ch1@2", "ring_rs_4@2",
+         "hier_ar_2x4_par1@1"]
+
+
+def _load(spec):
+    name, _, k = spec.partition("@")
+    ir = gc3.IR(read_ir(name))
+    if k and int(k) > 1:
+        ir = ir.replicate(int(k))
+    return json.loads(ir.serialize()), ir.direct_messages()
 
 
 @pytest.mark.parametrize("name", NAMES)
 def test_transports_match_fifo_semantics_under_random_interleavings(name):
-    irj = json.loads(read_ir(name))
-    flags = gc3.IR(read_ir(name)).direct_messages()
+    irj, flags = _load(name)
     ref = run(irj, flags, 0, use_flags=False)
     for seed in range(40):
+        # the program itself is schedule-independent (FIFO transports only) ...
+        if seed < 5:
+            assert all(np.array_equal(a, b) for a, b in zip(ref, run(irj, flags, seed, use_flags=False)))
         got = run(irj, flags, seed)
         assert all(np.array_equal(a, b) for a, b in zip(ref, got)), f"seed {seed}"
 

@@ -83,7 +83,11 @@ def main():
     span = (t_end - t0) / 1e3
     stats = {}
     busy = []
+    if tr.shape[0] != len(blocks) * lanes:  # lane multipliers in use: unit -> thread block unknown here
+        blocks = None
     for b in range(tr.shape[0]):
+        if blocks is None:
+            break
         rank, tb = blocks[b // lanes]
         nops = len(tb["ops"])
         ev = tr[b]
@@ -105,7 +109,7 @@ def main():
             data += d
         busy.append(data / max((last - first) / 1e3, 1e-9))
     out = {"config": args.config, "plan": plan, "span_us": span, "blocks": int(tr.shape[0]),
-           "mean_block_data_fraction": float(np.mean(busy)),
+           "mean_block_data_fraction": float(np.mean(busy)) if busy else None,
            "per_opcode_us": {k: {"n": v["n"], "wait": v["wait"] / v["n"], "data": v["data"] / v["n"],
                                  "publish": v["publish"] / v["n"]} for k, v in stats.items()}}
     print(json.dumps(out, indent=1))
