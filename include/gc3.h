@@ -180,6 +180,9 @@ ncclResult_t gc3IrOrderCheck(gc3Ir_t ir, int64_t tiles, int group, int slots, in
  * out receives nranks * bytes, rank-major. */
 ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, const void* payload, size_t bytes, void* out,
                                   int timeout_ms);
+/* per [rank][thread block] lane multipliers of the work balance (JSON); with balance on, thread block
+ * i of a launch runs lanes x mult lanes (units in launch order). */
+ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);
 ncclResult_t gc3IrFree(gc3Ir_t ir);
 void gc3Free(void* p);
 

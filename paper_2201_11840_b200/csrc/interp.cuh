@@ -34,6 +34,9 @@
 #ifndef GC3_MINBLOCKS
 #define GC3_MINBLOCKS 1
 #endif
+#ifndef GC3_LL_BATCH  // LL lines in flight per thread
+#define GC3_LL_BATCH 4
+#endif
 #ifndef GC3_TAIL_UNROLL  // vectors in flight per thread in the predicated tail of a data move
 #define GC3_TAIL_UNROLL 1
 #endif
@@ -96,13 +99,19 @@ __device__ __forceinline__ void st_vec(uint4* p, uint4 v) {
 __device__ __forceinline__ void st_vec8(void* p, uint2 v) {
   asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(p), "r"(v.x), "r"(v.y) : "memory");
 }
-__device__ __forceinline__ uint4 ld_volatile_line(const uint4* p) {
+// LL lines: strong (relaxed) 128-bit accesses at the scope of the peers (.gpu for same-device
+// loopback ranks: STRONG.GPU stays in L2; .sys across GPUs)
+__device__ __forceinline__ uint4 ld_line(const uint4* p, bool sys) {
   uint4 v;
-  asm volatile("ld.volatile.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  if (sys)
+    asm volatile("ld.relaxed.sys.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
+  else
+    asm volatile("ld.relaxed.gpu.global.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_volatile_line(uint4* p, uint4 v) {
-  asm volatile("st.volatile.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+__device__ __forceinline__ void st_line(uint4* p, uint4 v, bool sys) {
+  if (sys) asm volatile("st.relaxed.sys.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+  else asm volatile("st.relaxed.gpu.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 
 // ------------------------------------------------------------------ arithmetic
@@ -476,9 +485,9 @@ __device__ __forceinline__ bool is_send(int op) { return op == kOpSend || op == 
 // absent; the outgoing one goes to outl (LL lines), outd (direct, plain stores) or nowhere (pulled).
 template <class R>
 __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl,
-                      const char* inp, uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, const Ctx& c, int t,
-                      int n) {
-  constexpr int U = 4;  // lines in flight per thread: their loads are issued together, then polled
+                      const char* inp, uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, bool sys, const Ctx& c,
+                      int t, int n) {
+  constexpr int U = GC3_LL_BATCH;  // lines in flight per thread: their loads are issued together, then polled
   const int64_t lines_per_seg = tbytes >> 3;
   const int64_t nlines = lines_per_seg * count;
   const bool send = is_send(opcode);
@@ -495,7 +504,7 @@ __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
       if (k >= nlines) continue;
       const int64_t j = k / lines_per_seg;
       off[u] = ((k - j * lines_per_seg) << 3) + j * chunk_bytes;
-      if (inl) l[u] = ld_volatile_line(inl + k);
+      if (inl) l[u] = ld_line(inl + k, sys);
       if (inp) {  // pulled: the sender's span, laid out like the local one
         const uint2 m = ld_cg8(inp + off[u]);
         l[u] = make_uint4(m.x, in_flag, m.y, in_flag);
@@ -509,7 +518,7 @@ __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
       if (l[u].y != in_flag || l[u].w != in_flag) {
         const uint64_t start = globaltimer();
         for (int it = 0;; ++it) {
-          l[u] = ld_volatile_line(inl + k);
+          l[u] = ld_line(inl + k, sys);
           if (l[u].y == in_flag && l[u].w == in_flag) break;
           if ((it & 255) == 255) {
             if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
@@ -549,7 +558,7 @@ __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
         default: continue;
       }
       if (send) {
-        if (outl) st_volatile_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag));
+        if (outl) st_line(outl + k, make_uint4(v.x, out_flag, v.y, out_flag), sys);
         else if (outd) st_vec8(outd + off[u], v);
       }
     }
@@ -713,7 +722,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       if (ll_in || ll_out) {
         ok = ll_op<R>(op.opcode, op.count, src, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
                       in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
-                      static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), c, t, n);
+                      static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);
       } else if (tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
                  ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
                    reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) | static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {

@@ -1878,6 +1878,18 @@ ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, 
   return ncclSuccess;
 }
 
+ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json) {
+  if (!ir || !json) return ncclInvalidArgument;
+  const auto m = lane_multipliers(ir->p);
+  std::string o = "[";
+  for (size_t r = 0; r < m.size(); ++r) {
+    o += r ? ",[" : "[";
+    for (size_t t = 0; t < m[r].size(); ++t) o += (t ? "," : "") + std::to_string(m[r][t]);
+    o += "]";
+  }
+  *json = dup_cstr(o + "]");
+  return ncclSuccess;
+}
 ncclResult_t gc3IrFree(gc3Ir_t ir) {
   delete ir;
   return ncclSuccess;

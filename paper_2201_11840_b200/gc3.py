@@ -88,6 +88,7 @@ def lib():
         "gc3IrSerialize": [vp, ctypes.POINTER(vp)],
         "gc3IrParseXml": [cp, i, ctypes.POINTER(vp), ctypes.POINTER(vp)],
         "gc3IrToXml": [vp, ctypes.POINTER(vp)],
+        "gc3IrLaneMultipliers": [vp, ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -190,6 +191,12 @@ class IR:
         import json
         out = ctypes.c_void_p()
         check(lib().gc3IrDirectMessages(self._h, ctypes.byref(out)))
+        return json.loads(_take(out.value))
+
+    def lane_multipliers(self):
+        import json
+        out = ctypes.c_void_p()
+        check(lib().gc3IrLaneMultipliers(self._h, ctypes.byref(out)))
         return json.loads(_take(out.value))
 
     def order_deadlock_free(self, tiles, group, slots):

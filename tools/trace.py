@@ -72,19 +72,20 @@ def main():
     torch.cuda.synchronize()
     tr, lanes = comms[0].trace()
     plan = comms[0].query_plan(cfg["coll"], count, cfg["dtype"])
-    # block -> (rank, tb) in launch order
+    # unit -> (rank, tb) in launch order: thread block i runs lanes x mult_i units
+    mult = gc3.IR(open(path).read()).lane_multipliers()
     blocks = []
     for g in irj["gpus"]:
-        for tb in g["threadblocks"]:
-            blocks.append((g["rank"], tb))
+        for t, tb in enumerate(g["threadblocks"]):
+            blocks += [(g["rank"], tb)] * mult[g["rank"]][t]
     valid = tr[:, :, 3] > 0
     t0 = tr[:, :, 0][valid].min()
     t_end = tr[:, :, 3][valid].max()
     span = (t_end - t0) / 1e3
     stats = {}
     busy = []
-    if tr.shape[0] != len(blocks) * lanes:  # lane multipliers in use: unit -> thread block unknown here
-        blocks = None
+    if tr.shape[0] != len(blocks) * lanes:  # balance off (uniform lanes): one unit group per thread block
+        blocks = [(g["rank"], tb) for g in irj["gpus"] for tb in g["threadblocks"]]
     for b in range(tr.shape[0]):
         if blocks is None:
             break
