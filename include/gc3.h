@@ -180,6 +180,10 @@ ncclResult_t gc3IrOrderCheck(gc3Ir_t ir, int64_t tiles, int group, int slots, in
  * out receives nranks * bytes, rank-major. */
 ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, const void* payload, size_t bytes, void* out,
                                   int timeout_ms);
+/* [rank][tb][step] flags of the const-source analysis (1: the op's src read sees the caller's send
+ * buffer, 2: reduce's dst read does); *complete = 1 when every first read of `input` is covered, so
+ * in-place IRs need no pre-copy of sendbuff (SURVEY.md §7 hard part 6). */
+ncclResult_t gc3IrSourceReads(gc3Ir_t ir, int* complete, char** json);
 /* per [rank][thread block] lane multipliers of the work balance (JSON); with balance on, thread block
  * i of a launch runs lanes x mult lanes (units in launch order). */
 ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);

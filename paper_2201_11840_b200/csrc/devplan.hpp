@@ -21,6 +21,9 @@ constexpr int kThreads = GC3_THREADS;  // CUDA threads per interpreter block
 
 enum : uint8_t { kOpSend = 0, kOpRecv, kOpCopy, kOpReduce, kOpRrc, kOpRcs, kOpRrcs, kOpRrs, kOpNop };
 enum : uint8_t { kInDirect = 1, kOutDirect = 2, kInPull = 4, kOutPull = 8 };
+enum : uint8_t { kSrcFromSource = 1, kDstFromSource = 2 };
+constexpr int kBufs = 4;      // per rank: input, output, scratch, source (see LaunchArgs::bufs)
+constexpr int kSource = 3;
 
 struct DevOp {  // 32 bytes
   uint8_t opcode;
@@ -37,8 +40,10 @@ struct DevOp {  // 32 bytes
   int32_t dst_off;
   int32_t count;
   int32_t dep_begin;
-  int32_t in_off;  // kInPull: sender's chunk offset
-  int32_t pad;
+  int32_t in_off;   // kInPull: sender's chunk offset
+  uint8_t src_rbuf;  // buffer the src span is read from (kSource: the caller's const send buffer)
+  uint8_t dst_rbuf;  // buffer reduce's dst span is read from
+  uint8_t pad[2];
 };
 
 struct DevDep {
@@ -96,7 +101,9 @@ struct LaunchArgs {
   int32_t tma_stages;   // shared-memory stages per unit for bulk copies (0: register path only)
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
-  char* bufs[kMaxLocalRanks][3];  // per local rank: input, output, scratch
+  char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source (the caller's
+                                     // const data the in-place IR's first reads see; = input when
+                                     // the working buffer was pre-copied)
 };
 
 }  // namespace gc3

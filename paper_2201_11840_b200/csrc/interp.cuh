@@ -484,7 +484,7 @@ __device__ __forceinline__ bool is_send(int op) { return op == kOpSend || op == 
 // from the sender's span; its head flag was acquired before the op) or is in place (direct) or
 // absent; the outgoing one goes to outl (LL lines), outd (direct, plain stores) or nowhere (pulled).
 template <class R>
-__device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl,
+__device__ bool ll_op(int opcode, int count, char* src0, const char* srcr0, char* dst0, int64_t chunk_bytes, int64_t tbytes, const uint4* inl,
                       const char* inp, uint4* outl, char* outd, uint32_t in_flag, uint32_t out_flag, bool sys, const Ctx& c,
                       int t, int n) {
   constexpr int U = GC3_LL_BATCH;  // lines in flight per thread: their loads are issued together, then polled
@@ -509,7 +509,7 @@ __device__ bool ll_op(int opcode, int count, char* src0, char* dst0, int64_t chu
         const uint2 m = ld_cg8(inp + off[u]);
         l[u] = make_uint4(m.x, in_flag, m.y, in_flag);
       }
-      if (reads_src) own[u] = ld_cg8(src0 + off[u]);
+      if (reads_src) own[u] = ld_cg8((opcode == kOpRcs ? src0 : srcr0) + off[u]);
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -594,10 +594,10 @@ template <class R, bool LL>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
   // every rank's buffers of this launch, staged in shared memory once: ops index them by rank slot
   // and buffer id (a dynamically indexed kernel parameter would be copied to local memory)
-  __shared__ char* s_bufs[kMaxLocalRanks * 3];
+  __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
 #pragma unroll
-  for (int i = 0; i < kMaxLocalRanks * 3; ++i)
-    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / 3][i % 3];
+  for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
+    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
   __syncthreads();
   const int uw = a.unit_warps;
   const int n = uw * 32;                         // threads per unit
@@ -632,9 +632,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int64_t chunk_bytes = chunk_elems * R::kEsize;
   const uint64_t slots = static_cast<uint64_t>(a.slots);
   const uint64_t epoch = a.epoch;
-  char* const* const mine = s_bufs + 3 * tb.rank_slot;                          // this rank's buffers
-  char* const* const peer = s_bufs + 3 * (tb.peer_slot >= 0 ? tb.peer_slot : 0);  // send peer's (direct)
-  char* const* const rpeer = s_bufs + 3 * (tb.recv_slot >= 0 ? tb.recv_slot : 0); // receive peer's (pull)
+  char* const* const mine = s_bufs + kBufs * tb.rank_slot;                            // this rank's buffers
+  char* const* const peer = s_bufs + kBufs * (tb.peer_slot >= 0 ? tb.peer_slot : 0);  // send peer's (direct)
+  char* const* const rpeer = s_bufs + kBufs * (tb.recv_slot >= 0 ? tb.recv_slot : 0); // receive peer's (pull)
   const DevChan* const cin = has_in ? a.chans + tb.chan_in + lane : nullptr;
   const DevChan* const cout = has_out ? a.chans + tb.chan_out + lane : nullptr;
   uint64_t rcvd = has_in ? *cin->mine : 0;
@@ -705,6 +705,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       // when direct) unless it is pulled from this rank's span.
       char* src = mine[op.src_buf] + op.src_off * chunk_bytes + t0_bytes;
       char* dst = mine[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes;
+      // where the spans are read from: the caller's const buffer for first reads of an in-place IR
+      const char* srcr = mine[op.src_rbuf] + op.src_off * chunk_bytes + t0_bytes;
+      const char* dstr = mine[op.dst_rbuf] + op.dst_off * chunk_bytes + t0_bytes;
       const char* in = nullptr;
       int64_t in_stride = tbytes;
       if (in_fifo) in = cin->fifo + static_cast<int64_t>(rcvd % slots) * cin->slot_bytes;
@@ -720,7 +723,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         out_stride = chunk_bytes;
       }
       if (ll_in || ll_out) {
-        ok = ll_op<R>(op.opcode, op.count, src, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
+        ok = ll_op<R>(op.opcode, op.count, src, srcr, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
                       in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
                       static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);
       } else if (tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
@@ -730,10 +733,10 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
           fence_proxy_async_global();  // generic-proxy acquires above -> async-proxy reads
           switch (op.opcode) {
             case kOpSend:
-              if (out) tma_copy(tma, src, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
+              if (out) tma_copy(tma, srcr, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
               break;
             case kOpRecv: tma_copy(tma, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
-            case kOpCopy: tma_copy(tma, src, chunk_bytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
+            case kOpCopy: tma_copy(tma, srcr, chunk_bytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
             case kOpRcs:
               if (!in_d) tma_copy(tma, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count);
               else if (out) tma_copy(tma, src, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
@@ -746,24 +749,26 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         for (int j = 0; j < op.count; ++j) {
           char* sj = src + j * chunk_bytes;
           char* dj = dst + j * chunk_bytes;
+          const char* sr = srcr + j * chunk_bytes;
+          const char* dr = dstr + j * chunk_bytes;
           const char* mi = in ? in + j * in_stride : nullptr;
           char* mo = out ? out + j * out_stride : nullptr;
           switch (op.opcode) {
             case kOpSend:
-              if (mo) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
+              if (mo) move<R>(sr, nullptr, mo, nullptr, tbytes, t, n);
               break;
             case kOpRecv:
               if (mi) move<R>(mi, nullptr, dj, nullptr, tbytes, t, n);
               break;
-            case kOpCopy: move<R>(sj, nullptr, dj, nullptr, tbytes, t, n); break;
-            case kOpReduce: move<R>(dj, sj, dj, nullptr, tbytes, t, n); break;
-            case kOpRrc: move<R>(sj, mi, dj, nullptr, tbytes, t, n); break;
+            case kOpCopy: move<R>(sr, nullptr, dj, nullptr, tbytes, t, n); break;
+            case kOpReduce: move<R>(dr, sr, dj, nullptr, tbytes, t, n); break;
+            case kOpRrc: move<R>(sr, mi, dj, nullptr, tbytes, t, n); break;
             case kOpRcs:
               if (mi) move<R>(mi, nullptr, sj, mo, tbytes, t, n);
               else if (mo) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
               break;
-            case kOpRrcs: move<R>(sj, mi, sj, mo, tbytes, t, n); break;
-            case kOpRrs: move<R>(sj, mi, nullptr, mo, tbytes, t, n); break;
+            case kOpRrcs: move<R>(sr, mi, sj, mo, tbytes, t, n); break;
+            case kOpRrs: move<R>(sr, mi, nullptr, mo, tbytes, t, n); break;
             default: break;
           }
         }

@@ -97,6 +97,7 @@ struct Config {
   int64_t timeout_ms = 20000;        // device spin-wait watchdog
   int trace = 0;                     // record the in-kernel %globaltimer event log
   int direct = 3;                    // bit 0: direct messages, bit 1: pulled messages (direct_messages)
+  int source = 1;                    // in-place IRs read the caller's const buffer (source_reads)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
   int tma = 1;                       // bulk (TMA) copies for pure-copy ops on same-device peers
   int balance = 1;                   // per-component lane multipliers (lane_multipliers)
@@ -114,6 +115,7 @@ Config config_from_env() {
   c.timeout_ms = env_int("GC3_TIMEOUT_MS", c.timeout_ms);
   c.trace = static_cast<int>(env_int("GC3_TRACE", 0));
   c.direct = static_cast<int>(env_int("GC3_DIRECT", c.direct));
+  c.source = static_cast<int>(env_int("GC3_SOURCE", c.source));
   c.unit_warps = static_cast<int>(env_int("GC3_UNIT_WARPS", c.unit_warps));
   c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
   c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
@@ -255,6 +257,7 @@ struct RankIR {
 // Per-device execution state shared by the ranks a clique hosts on that device.
 struct DevicePlan {  // one registered IR on one device
   bool built = false;
+  bool source_complete = false;  // every first read of `input` reads the source buffer (source_reads)
   std::vector<int> ranks;  // local ranks in launch order (rank_slot -> rank)
   int ntbs = 0;
   int weight = 0;          // sum of lane multipliers: units = lanes x weight
@@ -462,74 +465,101 @@ ncclResult_t peer_arena(Comm* c, int id, int r, char*& out) {
 // (if that message is direct), so "after the receive" is checked at both u and x(u).
 // Returns flags[rank][tb index][step]; pull_src (optional) gets the sender span (buf, off) of
 // every kInPull receive.
+struct PullSrc {  // the sending op of a pulled message and the span it stores the message in
+  int buf = -1, off = -1, rank = -1, tb = -1, step = -1;
+};
+
+// Happens-before graph over every op of every rank: sequential order, declared deps and the k-th
+// send -> k-th receive message edges (the graph of scheduler.hpp:652-717), with its transitive
+// closure. ok == false when connections are unbalanced or the graph has a cycle.
+struct HbGraph {
+  struct Ref {
+    int rank, tb, step;
+  };
+  bool ok = false;
+  int n = 0;
+  std::vector<std::vector<int>> base;  // node index of (rank, tb, 0)
+  std::vector<int> sender_of;          // receive node -> matched send node
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<Ref>, std::vector<Ref>>> conns;  // (src, dst, ch)
+  size_t words = 0;
+  std::vector<uint64_t> reach;
+  bool reaches(int a, int b) const { return (reach[static_cast<size_t>(a) * words + b / 64] >> (b % 64)) & 1; }
+  int node(int r, int t, int s) const { return base[r][t] + s; }
+
+  explicit HbGraph(const Program& p) {
+    const int R = p.ranks();
+    base.resize(R);
+    for (int r = 0; r < R; ++r)
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+        base[r].push_back(n);
+        n += static_cast<int>(p.gpus[r].tbs[t].ops.size());
+      }
+    if (n == 0 || n > 65536) return;
+    std::vector<std::vector<int>> succ(n);
+    for (int r = 0; r < R; ++r)
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+        const ThreadBlock& tb = p.gpus[r].tbs[t];
+        for (size_t s = 0; s < tb.ops.size(); ++s) {
+          const int u = base[r][t] + static_cast<int>(s);
+          if (s + 1 < tb.ops.size()) succ[u].push_back(u + 1);
+          for (const Dep& d : tb.ops[s].deps) {
+            const int ti = tb_index(p, r, d.tb);
+            if (ti >= 0 && d.step >= 0 && d.step < static_cast<int>(p.gpus[r].tbs[ti].ops.size())) succ[base[r][ti] + d.step].push_back(u);
+          }
+          if (op_sends(tb.ops[s].op) && tb.send_peer >= 0) conns[{r, tb.send_peer, tb.channel}].first.push_back({r, static_cast<int>(t), static_cast<int>(s)});
+          if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0) conns[{tb.recv_peer, r, tb.channel}].second.push_back({r, static_cast<int>(t), static_cast<int>(s)});
+        }
+      }
+    sender_of.assign(n, -1);
+    for (auto& [key, c] : conns) {
+      if (c.first.size() != c.second.size()) return;  // unbalanced
+      for (size_t k = 0; k < c.first.size(); ++k) {
+        const int su = base[c.first[k].rank][c.first[k].tb] + c.first[k].step;
+        const int ru = base[c.second[k].rank][c.second[k].tb] + c.second[k].step;
+        succ[su].push_back(ru);
+        sender_of[ru] = su;
+      }
+    }
+    std::vector<int> indeg(n, 0), order;
+    for (int u = 0; u < n; ++u)
+      for (int v : succ[u]) ++indeg[v];
+    for (int u = 0; u < n; ++u)
+      if (!indeg[u]) order.push_back(u);
+    for (size_t i = 0; i < order.size(); ++i)
+      for (int v : succ[order[i]])
+        if (--indeg[v] == 0) order.push_back(v);
+    if (static_cast<int>(order.size()) != n) return;  // cycle: no static order
+    words = (n + 63) / 64;
+    reach.assign(static_cast<size_t>(n) * words, 0);
+    for (auto it = order.rbegin(); it != order.rend(); ++it) {
+      uint64_t* ru = &reach[static_cast<size_t>(*it) * words];
+      ru[*it / 64] |= 1ull << (*it % 64);
+      for (int v : succ[*it])
+        for (size_t w = 0; w < words; ++w) ru[w] |= reach[static_cast<size_t>(v) * words + w];
+    }
+    ok = true;
+  }
+};
+
 std::vector<std::vector<std::vector<uint8_t>>> direct_messages(
-    const Program& p, bool pull, std::vector<std::vector<std::vector<std::pair<int, int>>>>* pull_src) {
+    const Program& p, bool pull, std::vector<std::vector<std::vector<PullSrc>>>* pull_src) {
   const int R = p.ranks();
   std::vector<std::vector<std::vector<uint8_t>>> flags(R);
-  std::vector<std::vector<int>> base(R);  // node index of (rank, tb, 0)
-  int n = 0;
   for (int r = 0; r < R; ++r) {
     flags[r].resize(p.gpus[r].tbs.size());
-    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
-      flags[r][t].assign(p.gpus[r].tbs[t].ops.size(), 0);
-      base[r].push_back(n);
-      n += static_cast<int>(p.gpus[r].tbs[t].ops.size());
-    }
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) flags[r][t].assign(p.gpus[r].tbs[t].ops.size(), 0);
   }
   if (pull_src) {
     pull_src->assign(R, {});
     for (int r = 0; r < R; ++r)
-      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) (*pull_src)[r].emplace_back(p.gpus[r].tbs[t].ops.size(), std::make_pair(-1, -1));
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) (*pull_src)[r].emplace_back(p.gpus[r].tbs[t].ops.size(), PullSrc{});
   }
-  if (n == 0 || n > 65536) return flags;
-  std::vector<std::vector<int>> succ(n);
-  struct Ref {
-    int rank, tb, step;
-  };
-  std::map<std::tuple<int, int, int>, std::pair<std::vector<Ref>, std::vector<Ref>>> conns;
-  for (int r = 0; r < R; ++r)
-    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
-      const ThreadBlock& tb = p.gpus[r].tbs[t];
-      for (size_t s = 0; s < tb.ops.size(); ++s) {
-        const int u = base[r][t] + static_cast<int>(s);
-        if (s + 1 < tb.ops.size()) succ[u].push_back(u + 1);
-        for (const Dep& d : tb.ops[s].deps) {
-          const int ti = tb_index(p, r, d.tb);
-          if (ti >= 0 && d.step >= 0 && d.step < static_cast<int>(p.gpus[r].tbs[ti].ops.size())) succ[base[r][ti] + d.step].push_back(u);
-        }
-        if (op_sends(tb.ops[s].op) && tb.send_peer >= 0) conns[{r, tb.send_peer, tb.channel}].first.push_back({r, static_cast<int>(t), static_cast<int>(s)});
-        if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0) conns[{tb.recv_peer, r, tb.channel}].second.push_back({r, static_cast<int>(t), static_cast<int>(s)});
-      }
-    }
-  std::vector<int> sender_of(n, -1);  // receive node -> matched send node
-  for (auto& [key, c] : conns) {
-    if (c.first.size() != c.second.size()) return flags;  // unbalanced: no direct messages at all
-    for (size_t k = 0; k < c.first.size(); ++k) {
-      const int su = base[c.first[k].rank][c.first[k].tb] + c.first[k].step;
-      const int ru = base[c.second[k].rank][c.second[k].tb] + c.second[k].step;
-      succ[su].push_back(ru);
-      sender_of[ru] = su;
-    }
-  }
-  // reachability (reverse topological order); a cycle means no static order, so nothing is direct
-  std::vector<int> indeg(n, 0), order;
-  for (int u = 0; u < n; ++u)
-    for (int v : succ[u]) ++indeg[v];
-  for (int u = 0; u < n; ++u)
-    if (!indeg[u]) order.push_back(u);
-  for (size_t i = 0; i < order.size(); ++i)
-    for (int v : succ[order[i]])
-      if (--indeg[v] == 0) order.push_back(v);
-  if (static_cast<int>(order.size()) != n) return flags;
-  const size_t words = (n + 63) / 64;
-  std::vector<uint64_t> reach(static_cast<size_t>(n) * words, 0);
-  for (auto it = order.rbegin(); it != order.rend(); ++it) {
-    uint64_t* ru = &reach[static_cast<size_t>(*it) * words];
-    ru[*it / 64] |= 1ull << (*it % 64);
-    for (int v : succ[*it])
-      for (size_t w = 0; w < words; ++w) ru[w] |= reach[static_cast<size_t>(v) * words + w];
-  }
-  auto reaches = [&](int a, int b) { return (reach[static_cast<size_t>(a) * words + b / 64] >> (b % 64)) & 1; };
+  const HbGraph g(p);
+  if (!g.ok) return flags;
+  using Ref = HbGraph::Ref;
+  const auto& base = g.base;
+  const auto& sender_of = g.sender_of;
+  auto reaches = [&](int a, int b) { return g.reaches(a, b); };
   auto storage = [&](Buf b) { return p.inplace && b == Buf::output ? Buf::input : b; };
   struct Span {
     Buf b;
@@ -572,7 +602,7 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(
       }
     return true;
   };
-  for (auto& [key, c] : conns) {
+  for (auto& [key, c] : g.conns) {
     for (size_t k = 0; k < c.second.size(); ++k) {
       const Ref rx = c.second[k], tx = c.first[k];
       const Op& rop = p.gpus[rx.rank].tbs[rx.tb].ops[rx.step];
@@ -588,7 +618,7 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(
     }
   }
   if (!pull) return flags;
-  for (auto& [key, c] : conns) {
+  for (auto& [key, c] : g.conns) {
     for (size_t k = 0; k < c.second.size(); ++k) {
       const Ref rx = c.second[k], tx = c.first[k];
       if (flags[rx.rank][rx.tb][rx.step] & kInDirect) continue;
@@ -601,10 +631,82 @@ std::vector<std::vector<std::vector<uint8_t>>> direct_messages(
       if (window_clear(tx.rank, su, y, su, ru, true)) {
         flags[rx.rank][rx.tb][rx.step] |= kInPull;
         flags[tx.rank][tx.tb][tx.step] |= kOutPull;
-        if (pull_src) (*pull_src)[rx.rank][rx.tb][rx.step] = {static_cast<int>(sop.src_buf), sop.src_off};
+        if (pull_src) (*pull_src)[rx.rank][rx.tb][rx.step] = {static_cast<int>(sop.src_buf), sop.src_off, tx.rank, tx.tb, tx.step};
       }
     }
   }
+  return flags;
+}
+
+// Reads of the caller's const send buffer (SURVEY.md §7 hard part 6). AllReduce and ReduceScatter
+// IRs run in place on `input` (core.hpp:305-327, 351-375), but NCCL's sendbuff is const and usually
+// differs from recvbuff. A read of an input span that no write on its rank happens before sees the
+// caller's data, so it can read sendbuff itself and the working buffer needs no pre-copy. Returns
+// flags[rank][tb][step] (kSrcFromSource: the op's src read; kDstFromSource: reduce's dst read), and
+// `complete` = every input read is either remapped or preceded by a write (otherwise the runtime
+// keeps the pre-copy).
+std::vector<std::vector<std::vector<uint8_t>>> source_reads(const Program& p, bool& complete) {
+  const int R = p.ranks();
+  std::vector<std::vector<std::vector<uint8_t>>> flags(R);
+  for (int r = 0; r < R; ++r) {
+    flags[r].resize(p.gpus[r].tbs.size());
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) flags[r][t].assign(p.gpus[r].tbs[t].ops.size(), 0);
+  }
+  complete = false;
+  if (!p.inplace || R < 2) return flags;
+  const HbGraph g(p);
+  if (!g.ok) return flags;
+  auto is_input = [&](Buf b) { return b == Buf::input || b == Buf::output; };
+  auto writes = [&](const Op& op, int& off, int& cnt) {  // the op's local write span, if any
+    switch (op.op) {
+      case Opcode::recv: case Opcode::copy: case Opcode::reduce: case Opcode::rrc:
+        if (!is_input(op.dst_buf)) return false;
+        off = op.dst_off, cnt = op.count;
+        return true;
+      case Opcode::rcs: case Opcode::rrcs:
+        if (!is_input(op.src_buf)) return false;
+        off = op.src_off, cnt = op.count;
+        return true;
+      default: return false;
+    }
+  };
+  // 0: remappable, 1: a write happens before (reads the working buffer), 2: unordered write
+  auto classify = [&](int r, int u, int off, int cnt) {
+    int verdict = 0;
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t)
+      for (size_t s = 0; s < p.gpus[r].tbs[t].ops.size(); ++s) {
+        const int w = g.node(r, static_cast<int>(t), static_cast<int>(s));
+        if (w == u) continue;
+        int wo, wc;
+        if (!writes(p.gpus[r].tbs[t].ops[s], wo, wc) || !(wo < off + cnt && off < wo + wc)) continue;
+        if (g.reaches(w, u)) verdict = std::max(verdict, 1);
+        else if (!g.reaches(u, w)) verdict = 2;
+      }
+    return verdict;
+  };
+  complete = true;
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t)
+      for (size_t s = 0; s < p.gpus[r].tbs[t].ops.size(); ++s) {
+        const Op& op = p.gpus[r].tbs[t].ops[s];
+        const int u = g.node(r, static_cast<int>(t), static_cast<int>(s));
+        bool reads_src = false, reads_dst = false;
+        switch (op.op) {
+          case Opcode::send: case Opcode::copy: case Opcode::rrc: case Opcode::rrcs: case Opcode::rrs: reads_src = true; break;
+          case Opcode::reduce: reads_src = reads_dst = true; break;
+          default: break;  // recv writes only; rcs reads its span only after writing it (or after a direct write)
+        }
+        if (reads_src && is_input(op.src_buf)) {
+          const int v = classify(r, u, op.src_off, op.count);
+          if (v == 0) flags[r][t][s] |= kSrcFromSource;
+          if (v == 2) complete = false;
+        }
+        if (reads_dst && is_input(op.dst_buf)) {
+          const int v = classify(r, u, op.dst_off, op.count);
+          if (v == 0) flags[r][t][s] |= kDstFromSource;
+          if (v == 2) complete = false;
+        }
+      }
   return flags;
 }
 
@@ -688,7 +790,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   std::vector<DevChan> chans;
   plan.sys_scope = false;
   // direct messages only between ranks of this launch: the sender needs the receiver's buffers
-  std::vector<std::vector<std::vector<std::pair<int, int>>>> pull_src;
+  std::vector<std::vector<std::vector<PullSrc>>> pull_src;
+  bool source_complete = false;
+  const auto source = c0->cfg.source ? source_reads(p, source_complete) : std::vector<std::vector<std::vector<uint8_t>>>();
+  plan.source_complete = c0->cfg.source && source_complete;
   auto direct = c0->cfg.direct ? direct_messages(p, (c0->cfg.direct & 2) != 0, &pull_src)
                                : std::vector<std::vector<std::vector<uint8_t>>>();
   if (!(c0->cfg.direct & 1))  // pulls only: drop the direct flags
@@ -760,15 +865,22 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
           if ((f & kInDirect) && in_local) o.direct |= kInDirect;
           if ((f & kOutDirect) && d.peer_slot >= 0) o.direct |= kOutDirect;
           if ((f & kInPull) && in_local) {
+            const PullSrc& ps = pull_src[r][t][s];
             o.direct |= kInPull;
-            o.in_buf = static_cast<uint8_t>(pull_src[r][t][s].first);
-            o.in_off = pull_src[r][t][s].second;
+            o.in_buf = static_cast<uint8_t>(ps.buf);
+            o.in_off = ps.off;
+            // a send whose read of the span comes from the caller's buffer is pulled from there too
+            if (plan.source_complete && p.gpus[ps.rank].tbs[ps.tb].ops[ps.step].op == Opcode::send &&
+                (source[ps.rank][ps.tb][ps.step] & kSrcFromSource))
+              o.in_buf = kSource;
           }
           if ((f & kOutPull) && d.peer_slot >= 0) o.direct |= kOutPull;
         }
         o.opcode = static_cast<uint8_t>(op.op);
         o.src_buf = static_cast<uint8_t>(op.src_buf);
         o.dst_buf = static_cast<uint8_t>(op.dst_buf);
+        o.src_rbuf = plan.source_complete && (source[r][t][s] & kSrcFromSource) ? kSource : o.src_buf;
+        o.dst_rbuf = plan.source_complete && (source[r][t][s] & kDstFromSource) ? kSource : o.dst_buf;
         o.has_dep = op.has_dep ? 1 : 0;
         o.src_off = op.src_off;
         o.dst_off = op.dst_off;
@@ -1241,6 +1353,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     const int R = c->nranks;
     char* send = const_cast<char*>(static_cast<const char*>(q->send));
     char* recv = static_cast<char*>(q->recv);
+    char* source = nullptr;  // what the in-place IR's first reads see (source_reads); null: `in`
     switch (p0.coll) {
       case kAllReduce:  // in-place IR on `input` (core.hpp:305-327)
         if (ragged) {
@@ -1249,7 +1362,10 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
           in = out = c->work;
           post.push_back({recv, blk, c->work, pblk, blk, 1});
         } else {
-          if (send != recv) CUDA_TRY(cudaMemcpyAsync(recv, send, blk, cudaMemcpyDeviceToDevice, stream));
+          if (send != recv) {
+            if (plan.source_complete) source = send;  // first reads come from sendbuff: no pre-copy
+            else CUDA_TRY(cudaMemcpyAsync(recv, send, blk, cudaMemcpyDeviceToDevice, stream));
+          }
           in = out = recv;
         }
         break;
@@ -1268,7 +1384,9 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
         break;
       case kReduceScatter:  // in-place IR over R*c chunks; rank r owns [r*c, (r+1)*c)
         NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, pblk * R));
-        CUDA_TRY(cudaMemcpy2DAsync(c->work, pblk, send, blk, blk, R, cudaMemcpyDeviceToDevice, stream));
+        if (!ragged && plan.source_complete) source = send;  // first reads come from sendbuff
+        else if (!ragged) CUDA_TRY(cudaMemcpyAsync(c->work, send, blk * R, cudaMemcpyDeviceToDevice, stream));
+        else CUDA_TRY(cudaMemcpy2DAsync(c->work, pblk, send, blk, blk, R, cudaMemcpyDeviceToDevice, stream));
         in = out = c->work;
         post.push_back({recv, blk, c->work + static_cast<size_t>(c->rank) * pblk, pblk, blk, 1});
         break;
@@ -1291,6 +1409,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][0] = in;
     a.bufs[slot][1] = out;
     a.bufs[slot][2] = c->scratch;
+    a.bufs[slot][kSource] = source ? source : in;
   }
   CUDA_TRY(interp_launch(cp.fn, a, cp.grid, cp.smem, stream));
   for (const PostCopy& pc : post)
@@ -1673,6 +1792,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "timeout_ms") c.timeout_ms = value;
   else if (k == "trace") c.trace = static_cast<int>(value);
   else if (k == "direct") c.direct = static_cast<int>(value);
+  else if (k == "source") c.source = static_cast<int>(value);
   else if (k == "unit_warps") c.unit_warps = static_cast<int>(value);
   else if (k == "group") c.group = static_cast<int>(value);
   else if (k == "tma") c.tma = static_cast<int>(value);
@@ -1878,6 +1998,24 @@ ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, 
   return ncclSuccess;
 }
 
+ncclResult_t gc3IrSourceReads(gc3Ir_t ir, int* complete, char** json) {
+  if (!ir || !json || !complete) return ncclInvalidArgument;
+  bool c = false;
+  const auto f = source_reads(ir->p, c);
+  *complete = c ? 1 : 0;
+  std::string o = "[";
+  for (size_t r = 0; r < f.size(); ++r) {
+    o += r ? ",[" : "[";
+    for (size_t t = 0; t < f[r].size(); ++t) {
+      o += t ? ",[" : "[";
+      for (size_t k = 0; k < f[r][t].size(); ++k) o += (k ? "," : "") + std::to_string(f[r][t][k]);
+      o += "]";
+    }
+    o += "]";
+  }
+  *json = dup_cstr(o + "]");
+  return ncclSuccess;
+}
 ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json) {
   if (!ir || !json) return ncclInvalidArgument;
   const auto m = lane_multipliers(ir->p);

@@ -89,6 +89,7 @@ def lib():
         "gc3IrParseXml": [cp, i, ctypes.POINTER(vp), ctypes.POINTER(vp)],
         "gc3IrToXml": [vp, ctypes.POINTER(vp)],
         "gc3IrLaneMultipliers": [vp, ctypes.POINTER(vp)],
+        "gc3IrSourceReads": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -192,6 +193,13 @@ class IR:
         out = ctypes.c_void_p()
         check(lib().gc3IrDirectMessages(self._h, ctypes.byref(out)))
         return json.loads(_take(out.value))
+
+    def source_reads(self):
+        """(complete, flags[rank][tb][step]) of the const-source analysis."""
+        import json
+        out, comp = ctypes.c_void_p(), ctypes.c_int()
+        check(lib().gc3IrSourceReads(self._h, ctypes.byref(comp), ctypes.byref(out)))
+        return bool(comp.value), json.loads(_take(out.value))
 
     def lane_multipliers(self):
         import json

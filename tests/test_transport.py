@@ -28,18 +28,28 @@ SENDS = {"send", "rcs", "rrcs", "rrs"}
 RECVS = {"recv", "rrc", "rcs", "rrcs", "rrs"}
 
 
-def run(irj, flags, seed, use_flags=True):
+def run(irj, flags, seed, use_flags=True, source=None):
+    """source: flags of the const-source analysis; the working input then starts as garbage and
+    flagged reads see the caller's (initial) data instead."""
     R = len(irj["gpus"])
     nin, nout, nsc = irj["nchunks"]["input"], irj["nchunks"]["output"], irj["nchunks"]["scratch"]
     rng = np.random.default_rng(1234)
-    bufs = []
+    bufs, const = [], []
     for r in range(R):
         inp = rng.integers(-1000, 1000, nin).astype(np.int64)
+        const.append(inp.copy())
+        if source is not None:
+            inp[:] = 77777  # the working buffer is not initialised
         out = inp if irj["inplace"] else np.zeros(max(nout, 1), np.int64)
         bufs.append([inp, out, np.zeros(max(nsc, 1), np.int64)])
 
     def span(r, b, off, cnt):
         return bufs[r][BUFS[b]][off:off + cnt]
+
+    def rspan(r, b, off, cnt, t, s, bit):  # a read: from the caller's buffer when flagged
+        if source is not None and source[r][t][s] & bit:
+            return const[r][off:off + cnt]
+        return span(r, b, off, cnt)
 
     tbs = [(r, t, tb) for r, g in enumerate(irj["gpus"]) for t, tb in enumerate(g["threadblocks"])]
     ids = {(r, tb["id"]): t for r, g in enumerate(irj["gpus"]) for t, tb in enumerate(g["threadblocks"])}
@@ -71,6 +81,8 @@ def run(irj, flags, seed, use_flags=True):
         oc, cnt = op["opcode"], op["count"]
         src = span(r, op["src_buf"], op["src_off"], cnt)
         dst = span(r, op["dst_buf"], op["dst_off"], cnt)
+        srcr = rspan(r, op["src_buf"], op["src_off"], cnt, t, s, 1)
+        dstr = rspan(r, op["dst_buf"], op["dst_off"], cnt, t, s, 2)
         msg = None
         if oc in RECVS:
             key = (tb["recv_peer"], r, tb["channel"])
@@ -79,34 +91,36 @@ def run(irj, flags, seed, use_flags=True):
             sr, sop = posted[key][k]
             if f & 1:      # direct: already in place
                 msg = None
-            elif f & 4:    # pulled: the sender's span now
-                msg = span(sr, sop["src_buf"], sop["src_off"], cnt).copy()
+            elif f & 4:    # pulled: the sender's span now (its read buffer when it is a send)
+                st, ss = sop["_pos"]
+                msg = (rspan(sr, sop["src_buf"], sop["src_off"], cnt, st, ss, 1) if sop["opcode"] == "send"
+                       else span(sr, sop["src_buf"], sop["src_off"], cnt)).copy()
             else:
                 msg = fifo[key].pop(0)
         out = None
         if oc == "send":
-            out = src.copy()
+            out = srcr.copy()
         elif oc == "recv":
             if msg is not None:
                 dst[:] = msg
         elif oc == "copy":
-            dst[:] = src
+            dst[:] = srcr
         elif oc == "reduce":
-            dst[:] = dst + src
+            dst[:] = dstr + srcr
         elif oc == "rrc":
-            dst[:] = src + msg
+            dst[:] = srcr + msg
         elif oc == "rcs":
             if msg is not None:
                 src[:] = msg
             out = src.copy()
         elif oc == "rrcs":
-            src[:] = src + msg
+            src[:] = srcr + msg
             out = src.copy()
         elif oc == "rrs":
-            out = src + msg
+            out = srcr + msg
         if oc in SENDS:
             key = (r, tb["send_peer"], tb["channel"])
-            posted.setdefault(key, []).append((r, op))
+            posted.setdefault(key, []).append((r, dict(op, _pos=(t, s))))
             if f & 2:      # direct: into the receiver's span named by this op's dst fields
                 span(tb["send_peer"], op["dst_buf"], op["dst_off"], cnt)[:] = out
             elif not f & 8:
@@ -183,3 +197,29 @@ def test_a_racy_pull_would_be_caught():
     forced = [[[8, 0]], [[4]]]
     ref = run(irj, flags, 0, use_flags=False)
     assert any(not np.array_equal(run(irj, forced, s)[1], ref[1]) for s in range(40))
+
+
+@pytest.mark.parametrize("name", ["ring_ar_8_ch1", "ring_rs_8", "ring_rs_4@2", "hier_ar_2x4_par1", "allpairs_ar_8",
+                                  "ring_ar_8_inst4_auto", "hier_ar_2x4_par1.unfused", "allpairs_ar_4.unfused",
+                                  "ring_ar_4_ch4_inst4"])
+def test_const_source_reads_need_no_precopy(name):
+    """In-place AllReduce / ReduceScatter IRs read the caller's const buffer where no write comes
+    first (runtime.cpp source_reads): with the working buffer left uninitialised, every
+    interleaving (with the chosen transports) still gives the all-FIFO, pre-copied result."""
+    spec, _, k = name.partition("@")
+    ir = gc3.IR(read_ir(spec))
+    if k:
+        ir = ir.replicate(int(k))
+    irj, flags = json.loads(ir.serialize()), ir.direct_messages()
+    complete, source = ir.source_reads()
+    assert complete, name
+    assert any(x for g in source for tb in g for x in tb)
+    ref = run(irj, flags, 0, use_flags=False)
+    R = len(irj["gpus"])
+    c = irj["nchunks"]["input"] // R
+    for seed in range(30):
+        got = run(irj, flags, seed, source=source)
+        for r, (a, b) in enumerate(zip(ref, got)):
+            if irj["collective"] == "reducescatter":  # only the owned block is the result
+                a, b = a[r * c:(r + 1) * c], b[r * c:(r + 1) * c]
+            assert np.array_equal(a, b), f"seed {seed} rank {r}"
