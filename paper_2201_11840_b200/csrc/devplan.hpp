@@ -101,6 +101,8 @@ struct LaunchArgs {
   int32_t tma_stages;   // shared-memory stages per unit for bulk copies (0: register path only)
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
+  int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
+  int32_t pad3_;
   char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source (the caller's
                                      // const data the in-place IR's first reads see; = input when
                                      // the working buffer was pre-copied)

@@ -35,7 +35,7 @@
 #define GC3_MINBLOCKS 1
 #endif
 #ifndef GC3_LL_BATCH  // LL lines in flight per thread
-#define GC3_LL_BATCH 4
+#define GC3_LL_BATCH 1
 #endif
 #ifndef GC3_TAIL_UNROLL  // vectors in flight per thread in the predicated tail of a data move
 #define GC3_TAIL_UNROLL 1
@@ -355,6 +355,7 @@ __device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
@@ -369,7 +370,8 @@ struct Tma {
   char* stage;    // stages x kStageBytes of shared memory
   uint64_t* bar;  // one mbarrier per stage
   int stages;
-  uint32_t seq;   // pieces issued so far (stage = seq % stages, parity = (seq / stages) & 1)
+  uint32_t* seq;  // (shared) pieces issued so far: stage = seq % stages, parity = (seq / stages) & 1;
+                  // written by thread 0 at the end of an op, read by the unit's threads in a later one
 };
 
 // Copies `count` segments of `nbytes` (segment j: a + j*sa -> o0 + j*s0 [, o1 + j*s1]).
@@ -387,7 +389,7 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     d0 = o0 + j * s0 + off;
     d1 = o1 ? o1 + j * s1 + off : nullptr;
   };
-  const uint32_t base = m.seq;
+  const uint32_t base = *m.seq;
   const int64_t prime = min(static_cast<int64_t>(m.stages), total);
   for (int64_t p = 0; p < prime; ++p) {
     const char* src;
@@ -410,20 +412,79 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     bulk_store(d0, sm, bytes);
     if (d1) bulk_store(d1, sm, bytes);
     bulk_commit();
-    const int64_t np = p + m.stages;
-    if (np < total) {  // refill this stage once the store has read it
-      bulk_wait_read_all();
+    // refill the previous piece's stage once its store has read it: the store just issued stays in
+    // flight (wait_group.read 1), so loads and stores overlap instead of alternating
+    const int64_t rp = m.stages > 1 ? p - 1 : p, np = rp + m.stages;
+    if (rp >= 0 && np < total) {
+      if (m.stages > 1) bulk_wait_read_1();
+      else bulk_wait_read_all();  // one stage: it is the one just stored
+      const uint32_t rg = base + static_cast<uint32_t>(rp);
       const char* nsrc;
       char *n0, *n1;
       uint32_t nbytes_p;
       piece(np, nsrc, n0, n1, nbytes_p);
-      uint64_t* bar = m.bar + g % m.stages;
+      uint64_t* bar = m.bar + rg % m.stages;
       mbar_expect_tx(bar, nbytes_p);
-      bulk_load(sm, nsrc, nbytes_p, bar);
+      bulk_load(m.stage + static_cast<size_t>(rg % m.stages) * kStageBytes, nsrc, nbytes_p, bar);
     }
   }
   bulk_wait_all();
-  m.seq = base + static_cast<uint32_t>(total);
+  *m.seq = base + static_cast<uint32_t>(total);
+}
+
+__device__ __forceinline__ void unit_sync(int uw, int bar_id, int n);
+// Reductions through the bulk engine: both operands of every piece (half a stage each) are brought
+// into shared memory by cp.async.bulk, `stages` pieces in flight per unit regardless of registers;
+// every thread of the unit then combines its 16-byte vectors from shared memory (R::vec, operand
+// order a (op) b exactly as the register path) and stores the result with st.global to o0 [and o1].
+// Segment j: a + j*sa, b + j*sb -> o0 + j*s0 [, o1 + j*s1], nbytes each (all 16-byte aligned).
+template <class R>
+__device__ void tma_reduce(Tma& m, const char* a, int64_t sa, const char* b, int64_t sb, char* o0, int64_t s0, char* o1,
+                           int64_t s1, int64_t nbytes, int count, int t, int n, int uw, int bar_id) {
+  constexpr int P = kStageBytes / 2;  // bytes of one operand per piece
+  const int64_t per_seg = (nbytes + P - 1) / P;
+  const int64_t total = per_seg * count;
+  auto piece = [&](int64_t p, int64_t& j, int64_t& off, uint32_t& bytes) {
+    j = p / per_seg;
+    off = (p - j * per_seg) * P;
+    bytes = static_cast<uint32_t>(min(static_cast<int64_t>(P), nbytes - off));
+  };
+  const uint32_t base = *m.seq;
+  auto issue = [&](int64_t p) {  // thread 0: both operands of piece p into its stage
+    int64_t j, off;
+    uint32_t bytes;
+    piece(p, j, off, bytes);
+    const uint32_t g = base + static_cast<uint32_t>(p);
+    char* st = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
+    uint64_t* bar = m.bar + g % m.stages;
+    mbar_expect_tx(bar, 2 * bytes);
+    bulk_load(st, a + j * sa + off, bytes, bar);
+    bulk_load(st + P, b + j * sb + off, bytes, bar);
+  };
+  if (t == 0) {
+    fence_proxy_async_global();  // generic-proxy acquires (deps, flags) -> async-proxy reads
+    for (int64_t p = 0; p < min(static_cast<int64_t>(m.stages), total); ++p) issue(p);
+  }
+  for (int64_t p = 0; p < total; ++p) {
+    int64_t j, off;
+    uint32_t bytes;
+    piece(p, j, off, bytes);
+    const uint32_t g = base + static_cast<uint32_t>(p);
+    const char* st = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
+    mbar_wait(m.bar + g % m.stages, (g / m.stages) & 1);
+    const uint4* x = reinterpret_cast<const uint4*>(st);
+    const uint4* y = reinterpret_cast<const uint4*>(st + P);
+    uint4* d0 = reinterpret_cast<uint4*>(o0 + j * s0 + off);
+    uint4* d1 = o1 ? reinterpret_cast<uint4*>(o1 + j * s1 + off) : nullptr;
+    for (int v = t; v < static_cast<int>(bytes >> 4); v += n) {
+      const uint4 r = R::template vec<uint4>(x[v], y[v]);
+      st_vec(d0 + v, r);
+      if (d1) st_vec(d1 + v, r);
+    }
+    unit_sync(uw, bar_id, n);  // the stage is consumed: refill it
+    if (t == 0 && p + m.stages < total) issue(p + m.stages);
+  }
+  if (t == 0) *m.seq = base + static_cast<uint32_t>(total);
 }
 
 // ------------------------------------------------------------------ watchdog
@@ -610,7 +671,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   // TMA staging: a.tma_stages x kStageBytes of dynamic shared memory per unit, one mbarrier each
   extern __shared__ __align__(128) char s_stage[];
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
-  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * kStageBytes, s_bar[uib], a.tma_stages, 0};
+  __shared__ uint32_t s_seq[kThreads / 32];
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * kStageBytes, s_bar[uib], a.tma_stages, &s_seq[uib]};
+  if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
     for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -726,7 +789,21 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         ok = ll_op<R>(op.opcode, op.count, src, srcr, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
                       in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
                       static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);
-      } else if (tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
+      } else if (R::kReduce && (a.tma_ops & 2) && tma.stages >= 2 && in &&
+                 (op.opcode == kOpRrc || op.opcode == kOpRrcs || op.opcode == kOpRrs) &&
+                 ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(srcr) | reinterpret_cast<uintptr_t>(dst) |
+                   reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) |
+                   static_cast<uintptr_t>(chunk_bytes) | static_cast<uintptr_t>(in_stride)) & 15) == 0) {
+        // staged reduction: local operand (op.src read) (op) message, both through shared memory
+        switch (op.opcode) {
+          case kOpRrc: tma_reduce<R>(tma, srcr, chunk_bytes, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+          case kOpRrcs: tma_reduce<R>(tma, srcr, chunk_bytes, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id); break;
+          case kOpRrs:
+            if (out) tma_reduce<R>(tma, srcr, chunk_bytes, in, in_stride, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+            break;
+          default: break;
+        }
+      } else if ((a.tma_ops & 1) && tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
                  ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
                    reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) | static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
         if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier

@@ -99,7 +99,7 @@ struct Config {
   int direct = 3;                    // bit 0: direct messages, bit 1: pulled messages (direct_messages)
   int source = 1;                    // in-place IRs read the caller's const buffer (source_reads)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
-  int tma = 1;                       // bulk (TMA) copies for pure-copy ops on same-device peers
+  int tma = 3;                       // bulk (TMA) engine on same-device peers: bit 0 copies, bit 1 reductions
   int balance = 1;                   // per-component lane multipliers (lane_multipliers)
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
@@ -245,6 +245,7 @@ struct RankIR {
   int64_t slot_bytes = 0;
   int lanes = 1;  // lanes provisioned in the arena
   bool has_reduce = false;
+  bool has_chain = false;  // an op both receives and sends (rcs / rrcs / rrs): multi-hop chains
   int max_count = 1;
   std::vector<std::vector<int>> mult;  // lane multiplier per (rank, tb) (lane_multipliers)
   ArenaLayout lay;
@@ -1158,7 +1159,7 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   // units: `unit_warps` warps interpret one (thread block, lane); all units must be co-resident
   int uw = c->cfg.unit_warps;
   if (uw <= 0) {  // automatic: reductions move two operands per element, give them wider units
-    uw = ir.has_reduce ? 8 : 4;
+    uw = 4;
     while (uw > 1 && bps_plain * ds.num_sms * (kThreads / 32 / uw) < weight) uw /= 2;
   }
   if (uw < 1 || uw > kThreads / 32 || (kThreads / 32) % uw) uw = kThreads / 32;
@@ -1209,7 +1210,10 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.grid = (weight * lanes + units_per_block - 1) / units_per_block;
   // op-major tile groups: the largest G (<= tiles of a lane) whose order is deadlock-free here
   const int64_t max_tiles = cp.ntiles > 0 ? (cp.ntiles + lanes - 1) / lanes : 0;
-  int G = c->cfg.group > 0 ? c->cfg.group : static_cast<int>(std::min<int64_t>(std::max<int64_t>(max_tiles, 1), 64));
+  // (groups only pay off where tiles pipeline through multi-hop chains; single-hop programs such as
+  // AllToAll / two-step run tile-major)
+  int G = c->cfg.group > 0 ? c->cfg.group
+                           : (ir.has_chain ? static_cast<int>(std::min<int64_t>(std::max<int64_t>(max_tiles, 1), 64)) : 1);
   RankIR& mir = *c->irs[id];
   for (; G > 1; G /= 2) {
     // LL launches move every message through the FIFO lines (no direct / pulled transports)
@@ -1286,6 +1290,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
   a.tma_stages = cp.tma_stages;
+  a.tma_ops = c0->cfg.tma;
   a.discard = c0->cfg.discard;
   // LL: every message travels as flagged lines through the receiver's FIFO (lowest latency, no
   // fences); Simple: direct and pulled messages where the plan found them safe
@@ -1737,6 +1742,7 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
     for (const auto& tb : g.tbs)
       for (const auto& op : tb.ops) {
         if (op_reduces(op.op)) ir->has_reduce = true;
+        if (op_receives(op.op) && op_sends(op.op)) ir->has_chain = true;
         if (op_sends(op.op) || op_receives(op.op)) ir->max_count = std::max(ir->max_count, op.count);
       }
   ir->slots = std::max(1, comm->cfg.slots);
