@@ -20,7 +20,11 @@ constexpr int kMaxLocalRanks = 16;
 constexpr int kThreads = GC3_THREADS;  // CUDA threads per interpreter block
 
 enum : uint8_t { kOpSend = 0, kOpRecv, kOpCopy, kOpReduce, kOpRrc, kOpRcs, kOpRrcs, kOpRrs, kOpNop };
-enum : uint8_t { kInDirect = 1, kOutDirect = 2, kInPull = 4, kOutPull = 8 };
+enum : uint8_t { kInDirect = 1, kOutDirect = 2, kInPull = 4, kOutPull = 8,
+                 kMsgDep = 16,      // the receive waits its sender's semaphore (last `nmsg` deps), not the head
+                 kNoCtrIn = 32,     // the receive connection carries no FIFO message: no head/tail counters
+                 kPubSem = 64,      // publish this op's semaphore (a receive waits on it)
+                 kNoCtrOut = 128 }; // the send connection carries no FIFO message
 enum : uint8_t { kSrcFromSource = 1, kDstFromSource = 2 };
 constexpr int kBufs = 4;      // per rank: input, output, scratch, source (see LaunchArgs::bufs)
 constexpr int kSource = 3;
@@ -43,7 +47,8 @@ struct DevOp {  // 32 bytes
   int32_t in_off;   // kInPull: sender's chunk offset
   uint8_t src_rbuf;  // buffer the src span is read from (kSource: the caller's const send buffer)
   uint8_t dst_rbuf;  // buffer reduce's dst span is read from
-  uint8_t pad[2];
+  uint8_t nmsg;      // trailing deps that are message deps (kMsgDep; skipped in LL launches)
+  uint8_t pad;
 };
 
 struct DevDep {
@@ -102,7 +107,7 @@ struct LaunchArgs {
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
-  int32_t pad3_;
+  int32_t uniform;      // 1: every thread block runs `lanes` lanes (LL launches: FIFOs need matched lanes)
   char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source (the caller's
                                      // const data the in-place IR's first reads see; = input when
                                      // the working buffer was pre-copied)

@@ -679,16 +679,21 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // unit -> thread block: thread block i owns units [L0 * unit_base_i, L0 * (unit_base_i + mult_i))
+  // (uniform launches run every thread block on the base lanes)
   int tbi = 0;
-  for (int lo = 0, hi = a.ntbs - 1; lo < hi;) {
-    const int mid = (lo + hi + 1) / 2;
-    if (a.tbs[mid].unit_base * L0 <= unit) lo = mid;
-    else hi = mid - 1;
-    tbi = lo;
+  if (a.uniform) {
+    tbi = unit / L0;
+  } else {
+    for (int lo = 0, hi = a.ntbs - 1; lo < hi;) {
+      const int mid = (lo + hi + 1) / 2;
+      if (a.tbs[mid].unit_base * L0 <= unit) lo = mid;
+      else hi = mid - 1;
+      tbi = lo;
+    }
   }
   const DevTb tb = a.tbs[tbi];
-  const int lanes = L0 * tb.mult;
-  const int lane = unit - tb.unit_base * L0;
+  const int lanes = a.uniform ? L0 : L0 * tb.mult;
+  const int lane = a.uniform ? unit - tbi * L0 : unit - tb.unit_base * L0;
   const bool sys = a.sys_scope != 0;
   const bool has_in = tb.chan_in >= 0, has_out = tb.chan_out >= 0;
   const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
@@ -745,12 +750,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       // (1) preconditions, polled in parallel
       bool ok = true;
       if (t == 0 && out_fifo) ok = wait_geq(cout->tail, sent + 1 > slots ? sent + 1 - slots : 0, sys, c, 2);
-      if (t == 1 && recv && !ll_in) ok = wait_geq(cin->head, rcvd + 1, sys, c, 3);
-      for (int d = t - 2; d >= 0 && d < op.ndeps; d += n - 2) {
+      // direct / pulled receives wait on their sender's semaphore (the trailing message dep)
+      if (t == 1 && recv && !ll_in && !(tr & kMsgDep)) ok = wait_geq(cin->head, rcvd + 1, sys, c, 3);
+      const int ndeps = op.ndeps - ((tr & kMsgDep) ? 0 : op.nmsg);
+      for (int d = t - 2; d >= 0 && d < ndeps; d += n - 2) {
         const DevDep dd = a.deps[op.dep_begin + d];
         // the depended-on thread block may run a different lane count: find the lane that owns this
         // tile there and the tile's position in that lane's order
-        const int ld_lanes = L0 * dd.mult;
+        const int ld_lanes = a.uniform ? L0 : L0 * dd.mult;
         const int dl = static_cast<int>(tile % ld_lanes);
         const int64_t di = tile / ld_lanes;
         const int64_t dn = (ntiles - 1 - dl) / ld_lanes + 1;
@@ -867,15 +874,17 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         // three flag stores: a release pattern per flag without a fence per store. An LL receive
         // returns its slot without one: its loads have returned (their data was used above) and
         // it stored nothing another party reads through this flag.
-        const bool fence = (send && !ll_out) || (recv && !ll_in) || op.has_dep;
-        if (fence) fence_acq_rel(sys);
-        if (send && !ll_out) st_relaxed(cout->head, sent + 1, sys);
-        if (recv) st_relaxed(cin->tail, rcvd + 1, sys);
-        if (op.has_dep) st_relaxed(sems + tb.sem + lane, (epoch << 32) | static_cast<uint64_t>(q + 1), false);
+        // connections without FIFO messages keep no counters
+        const bool pub_head = send && !ll_out && !(tr & kNoCtrOut), pub_tail = recv && !(tr & kNoCtrIn);
+        const bool pub_sem = op.has_dep || (tr & kPubSem);
+        if (pub_head || (pub_tail && !ll_in) || pub_sem) fence_acq_rel(sys);
+        if (pub_head) st_relaxed(cout->head, sent + 1, sys);
+        if (pub_tail) st_relaxed(cin->tail, rcvd + 1, sys);
+        if (pub_sem) st_relaxed(sems + tb.sem + lane, (epoch << 32) | static_cast<uint64_t>(q + 1), false);
         stamp(q, 3);
       }
-      if (send) ++sent;
-      if (recv) ++rcvd;
+      if (send && !(tr & kNoCtrOut)) ++sent;
+      if (recv && !(tr & kNoCtrIn)) ++rcvd;
     }
   }
   if (t == 0) {  // persistent FIFO counters for the next launch

@@ -100,7 +100,8 @@ struct Config {
   int source = 1;                    // in-place IRs read the caller's const buffer (source_reads)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
   int tma = 3;                       // bulk (TMA) engine on same-device peers: bit 0 copies, bit 1 reductions
-  int balance = 1;                   // per-component lane multipliers (lane_multipliers)
+  int balance = 1;                   // per-component lane multipliers (lane_multipliers; 2: rounded up)
+  int mult_cap = 4;                  // largest lane multiplier
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
@@ -120,6 +121,7 @@ Config config_from_env() {
   c.group = static_cast<int>(env_int("GC3_GROUP", c.group));
   c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
   c.balance = static_cast<int>(env_int("GC3_BALANCE", c.balance));
+  c.mult_cap = static_cast<int>(env_int("GC3_MULT_CAP", c.mult_cap));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
 }
@@ -246,6 +248,7 @@ struct RankIR {
   int lanes = 1;  // lanes provisioned in the arena
   bool has_reduce = false;
   bool has_chain = false;  // an op both receives and sends (rcs / rrcs / rrs): multi-hop chains
+  uint8_t lane_mask = 0;   // transports assumed by the lane multipliers (transport_mask)
   int max_count = 1;
   std::vector<std::vector<int>> mult;  // lane multiplier per (rank, tb) (lane_multipliers)
   ArenaLayout lay;
@@ -542,6 +545,36 @@ struct HbGraph {
   }
 };
 
+// The sending op of every receive (k-th send -> k-th receive per connection, scheduler.hpp:251-273);
+// rank -1 where unmatched.
+std::vector<std::vector<std::vector<HbGraph::Ref>>> matched_senders(const Program& p) {
+  std::vector<std::vector<std::vector<HbGraph::Ref>>> out(p.ranks());
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<HbGraph::Ref>, std::vector<HbGraph::Ref>>> conns;
+  for (int r = 0; r < p.ranks(); ++r) {
+    out[r].resize(p.gpus[r].tbs.size());
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      out[r][t].assign(tb.ops.size(), HbGraph::Ref{-1, -1, -1});
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        if (op_sends(tb.ops[s].op) && tb.send_peer >= 0) conns[{r, tb.send_peer, tb.channel}].first.push_back({r, static_cast<int>(t), static_cast<int>(s)});
+        if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0) conns[{tb.recv_peer, r, tb.channel}].second.push_back({r, static_cast<int>(t), static_cast<int>(s)});
+      }
+    }
+  }
+  for (auto& [key, c] : conns)
+    for (size_t k = 0; k < c.second.size() && k < c.first.size(); ++k) out[c.second[k].rank][c.second[k].tb][c.second[k].step] = c.first[k];
+  return out;
+}
+
+// Receive-side transport mask a launch applies when every rank of the program runs in it (all
+// loopback ranks on one device): direct (config bit 0) and pulled (bit 1) messages.
+uint8_t transport_mask(int direct_cfg) {
+  uint8_t m = 0;
+  if (direct_cfg & 1) m |= kInDirect | kOutDirect;
+  if (direct_cfg & 2) m |= kInPull | kOutPull;
+  return m;
+}
+
 std::vector<std::vector<std::vector<uint8_t>>> direct_messages(
     const Program& p, bool pull, std::vector<std::vector<std::vector<PullSrc>>>* pull_src) {
   const int R = p.ranks();
@@ -716,9 +749,21 @@ std::vector<std::vector<std::vector<uint8_t>>> source_reads(const Program& p, bo
 // whose thread blocks move more bytes per tile (e.g. the coalesced count-G exchange of the two-step
 // AllToAll) gets proportionally more lanes. Weight of a thread block = chunk
 // passes its units make per tile (a direct receive moves nothing; its sender does the writing).
-std::vector<std::vector<int>> lane_multipliers(const Program& p) {
+std::vector<std::vector<int>> lane_multipliers(const Program& p, int mode, int cap, uint8_t mask) {
   const int R = p.ranks();
-  const auto direct = direct_messages(p, true, nullptr);
+  auto direct = direct_messages(p, true, nullptr);
+  for (auto& g : direct)
+    for (auto& tb : g)
+      for (auto& f : tb) f &= mask;
+  // connections that carry a FIFO message (under `mask`) need the same lanes at both ends
+  std::set<std::tuple<int, int, int>> fifo_conn;
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      for (size_t s = 0; s < tb.ops.size(); ++s)
+        if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0 && !(direct[r][t][s] & (kInDirect | kInPull)))
+          fifo_conn.insert({tb.recv_peer, r, tb.channel});
+    }
   std::vector<int> base(R + 1, 0);
   for (int r = 0; r < R; ++r) base[r + 1] = base[r] + static_cast<int>(p.gpus[r].tbs.size());
   std::vector<int> parent(base[R]);
@@ -728,7 +773,7 @@ std::vector<std::vector<int>> lane_multipliers(const Program& p) {
   for (int r = 0; r < R; ++r)
     for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
       const ThreadBlock& tb = p.gpus[r].tbs[t];
-      if (tb.send_peer >= 0 && tb.send_peer < R) {
+      if (tb.send_peer >= 0 && tb.send_peer < R && fifo_conn.count({r, tb.send_peer, tb.channel})) {
         const int rt = find_receiver(p, r, tb.send_peer, tb.channel);
         if (rt >= 0) parent[find(base[r] + static_cast<int>(t))] = find(base[tb.send_peer] + rt);
       }
@@ -762,7 +807,9 @@ std::vector<std::vector<int>> lane_multipliers(const Program& p) {
   for (int r = 0; r < R; ++r)
     for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
       const int w = comp_w[find(base[r] + static_cast<int>(t))];
-      mult[r].push_back(wmin > 0 ? std::max(1, std::min(4, (w + wmin / 2) / wmin)) : 1);
+      // mode 1: nearest multiple of the lightest component, mode 2: rounded up
+      const int k = wmin > 0 ? (mode >= 2 ? (w + wmin - 1) / wmin : (w + wmin / 2) / wmin) : 1;
+      mult[r].push_back(std::max(1, std::min(cap, k)));
     }
   return mult;
 }
@@ -806,27 +853,47 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       if (plan.ranks[i] == rank) return static_cast<int>(i);
     return -1;
   };
-  {  // the direct flags this launch applies (both ends in it), for the planner's deadlock check
-    std::vector<std::vector<std::vector<uint8_t>>> eff(p.ranks());
-    for (int r = 0; r < p.ranks(); ++r) {
-      eff[r].resize(p.gpus[r].tbs.size());
-      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
-        const ThreadBlock& tb = p.gpus[r].tbs[t];
-        eff[r][t].assign(tb.ops.size(), 0);
-        if (direct.empty() || slot_of(r) < 0) continue;
-        for (size_t s = 0; s < tb.ops.size(); ++s) {
-          const uint8_t f = direct[r][t][s];
-          if ((f & (kInDirect | kInPull)) && tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0) eff[r][t][s] |= f & (kInDirect | kInPull);
-          if ((f & (kOutDirect | kOutPull)) && tb.send_peer >= 0 && slot_of(tb.send_peer) >= 0)
-            eff[r][t][s] |= f & (kOutDirect | kOutPull);
+  // the transports this launch applies (both ends in it); with per-connection lanes (lane_mask) exactly
+  // the ones the lane multipliers assumed
+  std::vector<std::vector<std::vector<uint8_t>>> eff(p.ranks());
+  for (int r = 0; r < p.ranks(); ++r) {
+    eff[r].resize(p.gpus[r].tbs.size());
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      eff[r][t].assign(tb.ops.size(), 0);
+      if (direct.empty() || slot_of(r) < 0) continue;
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        uint8_t f = direct[r][t][s];
+        if (ir0.lane_mask) f &= ir0.lane_mask;
+        if ((f & (kInDirect | kInPull)) && tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0) eff[r][t][s] |= f & (kInDirect | kInPull);
+        if ((f & (kOutDirect | kOutPull)) && tb.send_peer >= 0 && slot_of(tb.send_peer) >= 0)
+          eff[r][t][s] |= f & (kOutDirect | kOutPull);
+      }
+    }
+  }
+  for (int r : plan.ranks) {
+    cl->local[r]->irs[id]->eff_direct = eff;
+    cl->local[r]->irs[id]->order_ok.clear();  // verdicts computed without the direct flags
+  }
+  // direct / pulled receives wait on their sender's semaphore (message deps), which works across
+  // thread blocks of different lane counts; connections without FIFO messages then need no
+  // head / tail counters at all (only when lanes may differ across connections, lane_mask)
+  const auto senders = matched_senders(p);
+  std::set<std::tuple<int, int, int>> fifo_conn;
+  std::set<std::tuple<int, int, int>> pub_sem;
+  for (int r = 0; r < p.ranks(); ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        if (!op_receives(tb.ops[s].op) || tb.recv_peer < 0) continue;
+        if (eff[r][t][s] & (kInDirect | kInPull)) {
+          const auto& sd = senders[r][t][s];
+          if (sd.rank >= 0) pub_sem.insert({sd.rank, sd.tb, sd.step});
+        } else {
+          fifo_conn.insert({tb.recv_peer, r, tb.channel});
         }
       }
     }
-    for (int r : plan.ranks) {
-      cl->local[r]->irs[id]->eff_direct = eff;
-      cl->local[r]->irs[id]->order_ok.clear();  // verdicts computed without the direct flags
-    }
-  }
   // semaphores: lanes x mult per thread block, in launch order
   const auto& mult = ir0.mult;
   std::map<std::pair<int, int>, int> sem_base;  // (rank, tb index) -> first semaphore
@@ -861,21 +928,21 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       for (size_t s = 0; s < tb.ops.size(); ++s) {
         const Op& op = tb.ops[s];
         DevOp o{};
-        if (!direct.empty()) {
-          const uint8_t f = direct[r][t][s];
-          if ((f & kInDirect) && in_local) o.direct |= kInDirect;
-          if ((f & kOutDirect) && d.peer_slot >= 0) o.direct |= kOutDirect;
-          if ((f & kInPull) && in_local) {
-            const PullSrc& ps = pull_src[r][t][s];
-            o.direct |= kInPull;
-            o.in_buf = static_cast<uint8_t>(ps.buf);
-            o.in_off = ps.off;
-            // a send whose read of the span comes from the caller's buffer is pulled from there too
-            if (plan.source_complete && p.gpus[ps.rank].tbs[ps.tb].ops[ps.step].op == Opcode::send &&
-                (source[ps.rank][ps.tb][ps.step] & kSrcFromSource))
-              o.in_buf = kSource;
-          }
-          if ((f & kOutPull) && d.peer_slot >= 0) o.direct |= kOutPull;
+        (void)in_local;
+        o.direct = eff[r][t][s];
+        if (o.direct & kInPull) {
+          const PullSrc& ps = pull_src[r][t][s];
+          o.in_buf = static_cast<uint8_t>(ps.buf);
+          o.in_off = ps.off;
+          // a send whose read of the span comes from the caller's buffer is pulled from there too
+          if (plan.source_complete && p.gpus[ps.rank].tbs[ps.tb].ops[ps.step].op == Opcode::send &&
+              (source[ps.rank][ps.tb][ps.step] & kSrcFromSource))
+            o.in_buf = kSource;
+        }
+        if (pub_sem.count({r, static_cast<int>(t), static_cast<int>(s)})) o.direct |= kPubSem;
+        if (ir0.lane_mask) {
+          if (op_sends(op.op) && tb.send_peer >= 0 && !fifo_conn.count({r, tb.send_peer, tb.channel})) o.direct |= kNoCtrOut;
+          if (op_receives(op.op) && tb.recv_peer >= 0 && !fifo_conn.count({tb.recv_peer, r, tb.channel})) o.direct |= kNoCtrIn;
         }
         o.opcode = static_cast<uint8_t>(op.op);
         o.src_buf = static_cast<uint8_t>(op.src_buf);
@@ -897,6 +964,20 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
           dd.nops = static_cast<int>(g.tbs[ti].ops.size());
           dd.mult = mult[r][ti];
           deps.push_back(dd);
+        }
+        if (o.direct & (kInDirect | kInPull)) {  // message dep on the sending op
+          const auto& sd = senders[r][t][s];
+          if (sd.rank >= 0 && sem_base.count({sd.rank, sd.tb})) {
+            DevDep dd{};
+            dd.sem = sem_base[{sd.rank, sd.tb}];
+            dd.step = sd.step;
+            dd.nops = static_cast<int>(p.gpus[sd.rank].tbs[sd.tb].ops.size());
+            dd.mult = mult[sd.rank][sd.tb];
+            deps.push_back(dd);
+            o.nmsg = 1;
+            o.ndeps = static_cast<int16_t>(o.ndeps + 1);
+            o.direct |= kMsgDep;
+          }
         }
         ops.push_back(o);
       }
@@ -1071,6 +1152,7 @@ bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std:
     return g0 * nops + step * gsize + (i - g0);
   };
   std::map<std::tuple<int, int, int, int>, std::pair<int64_t, int64_t>> conn;  // (src, dst, ch, lane) -> (sent, consumed)
+  const auto senders = matched_senders(p);
   for (bool progress = true; progress;) {
     progress = false;
     for (Unit& u : units) {
@@ -1091,7 +1173,13 @@ bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std:
           if (du.pos < position(tile / du.lt, d.step, dn, du.ntl) + 1) ok = false;
         }
         const bool direct_out = !direct.empty() && (direct[u.r][u.t][step] & (kOutDirect | kOutPull));
-        if (ok && op_receives(op.op)) {
+        const bool direct_in = !direct.empty() && (direct[u.r][u.t][step] & (kInDirect | kInPull));
+        if (ok && op_receives(op.op) && direct_in) {  // message dep: the sending op done for this tile
+          const auto& sd = senders[u.r][u.t][step];
+          const Unit& su = units[first[{sd.rank, sd.tb}] + static_cast<int>(tile % units[first[{sd.rank, sd.tb}]].lt)];
+          const int sn = static_cast<int>(p.gpus[sd.rank].tbs[sd.tb].ops.size());
+          if (su.pos < position(tile / su.lt, sd.step, sn, su.ntl) + 1) ok = false;
+        } else if (ok && op_receives(op.op)) {
           const auto& c = conn[{tb.recv_peer, u.r, tb.channel, u.lane}];
           if (c.first <= c.second) ok = false;
         }
@@ -1125,6 +1213,8 @@ struct CallPlan {
   int kesize = 1;                                          // kernel element size
   KernelFn fn = nullptr;
   int redop = -1;
+  bool uniform = false;  // every thread block on the base lanes (LL with per-connection lanes)
+  int weight = 0;        // units per lane: sum of multipliers, or thread blocks when uniform
 };
 
 ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count, int dtype, int redop, int weight, bool sys_scope,
@@ -1145,6 +1235,15 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.chunk_elems = chunk_bytes / cp.kesize;
   const int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
   cp.ll = proto == 1 && chunk_bytes % 8 == 0;
+  // an LL launch sends every message through lane-matched FIFOs: with per-connection lane counts
+  // (lane_mask) it runs every thread block on the base lanes instead
+  cp.uniform = cp.ll && ir.lane_mask != 0;
+  if (cp.uniform) {
+    weight = 0;
+    for (int r = 0; r < c->nranks; ++r)
+      if (c->clique->local[r] && c->clique->local[r]->device == ds.device) weight += static_cast<int>(p.gpus[r].tbs.size());
+  }
+  cp.weight = weight;
   const int64_t cap_bytes = cp.ll ? ir.slot_bytes / 2 : ir.slot_bytes;  // per tile (slots scale with count)
   int64_t tile_bytes_cap = cap_bytes / 16 * 16;
   if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot unit too small");
@@ -1190,8 +1289,9 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
             // multiple of every thread block's lane count (lanes x multiplier), so all lanes of a
             // thread block get the same number of tiles (no straggler lane).
     int lcm = 1;
-    for (const auto& g : ir.mult)
-      for (int m : g) lcm = std::lcm(lcm, std::max(m, 1));
+    if (!cp.uniform)
+      for (const auto& g : ir.mult)
+        for (int m : g) lcm = std::lcm(lcm, std::max(m, 1));
     const int64_t lanes_all = static_cast<int64_t>(lanes) * lcm;
     const int64_t k = std::max<int64_t>(1, (chunk_bytes + lanes_all * tile_bytes_cap - 1) / (lanes_all * tile_bytes_cap));
     tile_bytes = (chunk_bytes + lanes_all * k - 1) / (lanes_all * k);
@@ -1222,7 +1322,8 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     if (f == mir.order_ok.end())
       f = mir.order_ok
               .emplace(key, order_is_deadlock_free(p, cp.ll ? std::vector<std::vector<std::vector<uint8_t>>>() : mir.eff_direct,
-                                                   cp.ntiles, lanes, mir.mult, G, ir.slots))
+                                                   cp.ntiles, lanes, cp.uniform ? std::vector<std::vector<int>>() : mir.mult,
+                                                   G, ir.slots))
               .first;
     if (f->second) break;
   }
@@ -1285,7 +1386,8 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.chans = plan.d_chans;
   a.sems = plan.d_sems;
   a.ntbs = plan.ntbs;
-  a.weight = plan.weight;
+  a.weight = cp.weight;
+  a.uniform = cp.uniform ? 1 : 0;
   a.lanes = cp.lanes;
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
@@ -1309,7 +1411,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     for (int r : plan.ranks)
       for (const auto& tb : c0->irs[id]->prog.gpus[r].tbs) max_nops = std::max(max_nops, static_cast<int>(tb.ops.size()));
     const int ops_per_block = static_cast<int>(std::min<int64_t>((cp.ntiles + cp.lanes - 1) / cp.lanes * max_nops, 1 << 20));
-    const size_t need = static_cast<size_t>(plan.weight) * cp.lanes * ops_per_block * 4 * sizeof(uint64_t);
+    const size_t need = static_cast<size_t>(cp.weight) * cp.lanes * ops_per_block * 4 * sizeof(uint64_t);
     DeviceGuard gt(dev);
     if (need > ds->trace_bytes) {
       if (ds->d_trace) cudaFree(ds->d_trace);
@@ -1321,7 +1423,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     CUDA_TRY(cudaMemsetAsync(ds->d_trace, 0, need, p0.stream));
     a.trace = ds->d_trace;
     a.trace_ops = ops_per_block;
-    ds->trace_grid = plan.weight * cp.lanes;
+    ds->trace_grid = cp.weight * cp.lanes;
     ds->trace_ops = ops_per_block;
     ds->trace_lanes = cp.lanes;
   }
@@ -1754,7 +1856,15 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
     ir->lanes = std::max(1, std::min(comm->cfg.max_lanes, (2 * sms + max_tbs - 1) / max_tbs));
   }
-  ir->mult = comm->cfg.balance ? lane_multipliers(ir->prog) : std::vector<std::vector<int>>();
+  {  // direct / pulled messages (and lanes that differ across their connections) only when every
+     // rank runs in one launch: all ranks hosted here, on one device
+    bool one_launch = true;
+    for (int r = 0; r < comm->nranks; ++r)
+      one_launch = one_launch && comm->clique->local[r] && comm->clique->local[r]->device == comm->device;
+    ir->lane_mask = one_launch ? transport_mask(comm->cfg.direct) : 0;
+  }
+  ir->mult = comm->cfg.balance ? lane_multipliers(ir->prog, comm->cfg.balance, comm->cfg.mult_cap, ir->lane_mask)
+                               : std::vector<std::vector<int>>();
   if (ir->mult.empty())
     for (const auto& g : ir->prog.gpus) ir->mult.emplace_back(g.tbs.size(), 1);
   ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes, ir->mult);
@@ -1803,6 +1913,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "group") c.group = static_cast<int>(value);
   else if (k == "tma") c.tma = static_cast<int>(value);
   else if (k == "balance") c.balance = static_cast<int>(value);
+  else if (k == "mult_cap") c.mult_cap = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
@@ -2024,7 +2135,7 @@ ncclResult_t gc3IrSourceReads(gc3Ir_t ir, int* complete, char** json) {
 }
 ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json) {
   if (!ir || !json) return ncclInvalidArgument;
-  const auto m = lane_multipliers(ir->p);
+  const auto m = lane_multipliers(ir->p, 1, 4, transport_mask(3));
   std::string o = "[";
   for (size_t r = 0; r < m.size(); ++r) {
     o += r ? ",[" : "[";
