@@ -433,15 +433,17 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
 }
 
 __device__ __forceinline__ void unit_sync(int uw, int bar_id, int n);
-// Reductions through the bulk engine: both operands of every piece (half a stage each) are brought
-// into shared memory by cp.async.bulk, `stages` pieces in flight per unit regardless of registers;
-// every thread of the unit then combines its 16-byte vectors from shared memory (R::vec, operand
-// order a (op) b exactly as the register path) and stores the result with st.global to o0 [and o1].
-// Segment j: a + j*sa, b + j*sb -> o0 + j*s0 [, o1 + j*s1], nbytes each (all 16-byte aligned).
-template <class R>
-__device__ void tma_reduce(Tma& m, const char* a, int64_t sa, const char* b, int64_t sb, char* o0, int64_t s0, char* o1,
+// Streams through the bulk engine: the operand(s) of every piece (half a stage each when reducing)
+// are brought into shared memory by cp.async.bulk, `stages` pieces in flight per unit regardless of
+// registers; every thread of the unit then combines its 16-byte vectors from shared memory (R::vec,
+// operand order a (op) b exactly as the register path) and stores the result with st.global to o0
+// [and o1]. Stores leave from registers, so a stage is free as soon as it has been read: loads keep
+// (almost) every stage in flight, unlike bulk stores that hold their stage until they have read it.
+// Segment j: a + j*sa [, b + j*sb] -> o0 + j*s0 [, o1 + j*s1], nbytes each (all 16-byte aligned).
+template <class R, bool RED>
+__device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int64_t sb, char* o0, int64_t s0, char* o1,
                            int64_t s1, int64_t nbytes, int count, int t, int n, int uw, int bar_id) {
-  constexpr int P = kStageBytes / 2;  // bytes of one operand per piece
+  constexpr int P = RED ? kStageBytes / 2 : kStageBytes;  // bytes of one operand per piece
   const int64_t per_seg = (nbytes + P - 1) / P;
   const int64_t total = per_seg * count;
   auto piece = [&](int64_t p, int64_t& j, int64_t& off, uint32_t& bytes) {
@@ -450,16 +452,16 @@ __device__ void tma_reduce(Tma& m, const char* a, int64_t sa, const char* b, int
     bytes = static_cast<uint32_t>(min(static_cast<int64_t>(P), nbytes - off));
   };
   const uint32_t base = *m.seq;
-  auto issue = [&](int64_t p) {  // thread 0: both operands of piece p into its stage
+  auto issue = [&](int64_t p) {  // thread 0: the operands of piece p into its stage
     int64_t j, off;
     uint32_t bytes;
     piece(p, j, off, bytes);
     const uint32_t g = base + static_cast<uint32_t>(p);
     char* st = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
     uint64_t* bar = m.bar + g % m.stages;
-    mbar_expect_tx(bar, 2 * bytes);
+    mbar_expect_tx(bar, RED ? 2 * bytes : bytes);
     bulk_load(st, a + j * sa + off, bytes, bar);
-    bulk_load(st + P, b + j * sb + off, bytes, bar);
+    if (RED) bulk_load(st + P, b + j * sb + off, bytes, bar);
   };
   if (t == 0) {
     fence_proxy_async_global();  // generic-proxy acquires (deps, flags) -> async-proxy reads
@@ -477,11 +479,11 @@ __device__ void tma_reduce(Tma& m, const char* a, int64_t sa, const char* b, int
     uint4* d0 = reinterpret_cast<uint4*>(o0 + j * s0 + off);
     uint4* d1 = o1 ? reinterpret_cast<uint4*>(o1 + j * s1 + off) : nullptr;
     for (int v = t; v < static_cast<int>(bytes >> 4); v += n) {
-      const uint4 r = R::template vec<uint4>(x[v], y[v]);
+      const uint4 r = RED ? R::template vec<uint4>(x[v], y[v]) : x[v];
       st_vec(d0 + v, r);
       if (d1) st_vec(d1 + v, r);
     }
-    unit_sync(uw, bar_id, n);  // the stage is consumed: refill it
+    unit_sync(uw, bar_id, n);  // the stage is consumed (stores issued from registers): refill it
     if (t == 0 && p + m.stages < total) issue(p + m.stages);
   }
   if (t == 0) *m.seq = base + static_cast<uint32_t>(total);
@@ -803,17 +805,30 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
                    static_cast<uintptr_t>(chunk_bytes) | static_cast<uintptr_t>(in_stride)) & 15) == 0) {
         // staged reduction: local operand (op.src read) (op) message, both through shared memory
         switch (op.opcode) {
-          case kOpRrc: tma_reduce<R>(tma, srcr, chunk_bytes, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
-          case kOpRrcs: tma_reduce<R>(tma, srcr, chunk_bytes, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id); break;
+          case kOpRrc: tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+          case kOpRrcs: tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id); break;
           case kOpRrs:
-            if (out) tma_reduce<R>(tma, srcr, chunk_bytes, in, in_stride, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+            if (out) tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
             break;
           default: break;
         }
       } else if ((a.tma_ops & 1) && tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
                  ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
                    reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) | static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
-        if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier
+        if (a.tma_ops & 4) {  // bulk loads, stores from registers by the whole unit
+          switch (op.opcode) {
+            case kOpSend:
+              if (out) tma_stream<R, false>(tma, srcr, chunk_bytes, nullptr, 0, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+              break;
+            case kOpRecv: tma_stream<R, false>(tma, in, in_stride, nullptr, 0, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+            case kOpCopy: tma_stream<R, false>(tma, srcr, chunk_bytes, nullptr, 0, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+            case kOpRcs:
+              if (!in_d) tma_stream<R, false>(tma, in, in_stride, nullptr, 0, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id);
+              else if (out) tma_stream<R, false>(tma, src, chunk_bytes, nullptr, 0, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+              break;
+            default: break;
+          }
+        } else if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier
           fence_proxy_async_global();  // generic-proxy acquires above -> async-proxy reads
           switch (op.opcode) {
             case kOpSend:

@@ -1237,13 +1237,10 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.ll = proto == 1 && chunk_bytes % 8 == 0;
   // an LL launch sends every message through lane-matched FIFOs: with per-connection lane counts
   // (lane_mask) it runs every thread block on the base lanes instead
+  int ntbs_local = 0;
+  for (int r = 0; r < c->nranks; ++r)
+    if (c->clique->local[r] && c->clique->local[r]->device == ds.device) ntbs_local += static_cast<int>(p.gpus[r].tbs.size());
   cp.uniform = cp.ll && ir.lane_mask != 0;
-  if (cp.uniform) {
-    weight = 0;
-    for (int r = 0; r < c->nranks; ++r)
-      if (c->clique->local[r] && c->clique->local[r]->device == ds.device) weight += static_cast<int>(p.gpus[r].tbs.size());
-  }
-  cp.weight = weight;
   const int64_t cap_bytes = cp.ll ? ir.slot_bytes / 2 : ir.slot_bytes;  // per tile (slots scale with count)
   int64_t tile_bytes_cap = cap_bytes / 16 * 16;
   if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot unit too small");
@@ -1255,6 +1252,15 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     return f->second;
   };
   const int bps_plain = occupancy(0);
+  if (!cp.uniform && weight > ntbs_local) {
+    // balanced lanes only where they fit: if the multipliers leave much of the GPU idle (or do not
+    // fit at all) at 4-warp units, every thread block runs the base lanes instead
+    const int cap4 = bps_plain * ds.num_sms * (kThreads / 32 / 4);
+    const int lb = std::min(cap4 / weight, ir.lanes), lu = std::min(cap4 / ntbs_local, ir.lanes);
+    if (lb < 1 || 4LL * lb * weight < 3LL * lu * ntbs_local) cp.uniform = true;
+  }
+  if (cp.uniform) weight = ntbs_local;
+  cp.weight = weight;
   // units: `unit_warps` warps interpret one (thread block, lane); all units must be co-resident
   int uw = c->cfg.unit_warps;
   if (uw <= 0) {  // automatic: reductions move two operands per element, give them wider units

@@ -1,4 +1,4 @@
-o=gpurun_out/r01m; mkdir -p $o
-timeout 900 python -m pytest tests -m gpu -x -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
-for c in c1 c2 c3 c4 c5rs c5ag c2d; do timeout 120 python bench.py --config $c --quick --steps 20 >> $o/quick.jsonl 2>&1; done
-for c in c1 c4; do timeout 120 python bench.py --config $c --quick --steps 20 --proto ll >> $o/quick.jsonl 2>&1; done
+o=gpurun_out/r01o; mkdir -p $o
+GC3_TMA=7 timeout 900 python -m pytest tests -m gpu -x -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
+bash tools/envsweep.sh "c2 c2d c5ag c3 c4 c1" "GC3_TMA=3;GC3_TMA=7;GC3_TMA=7 GC3_UNIT_WARPS=8" > $o/env.txt 2>&1
+GC3_TMA=7 timeout 120 python tools/trace.py --config c2 --json $o/trace_c2.json > $o/trace_c2.log 2>&1
