@@ -93,8 +93,11 @@ struct LaunchArgs {
   int32_t slots;
   int32_t sys_scope;    // 1: peers on other GPUs (NVLink, .sys fences); 0: same-device loopback
   int64_t chunk_elems;  // elements per chunk
-  int64_t tile_elems;   // elements per tile
+  int64_t tile_elems;   // elements per (big) tile
   int64_t ntiles;
+  int64_t small_elems;  // tapered tiles: n_head small tiles, n_big big ones, then small ones to the end
+  int64_t n_head;
+  int64_t n_big;
   uint64_t epoch;       // launch counter of this device (semaphore tag)
   uint64_t timeout_ns;  // spin-wait watchdog; 0 disables
   int32_t* abort_flag;  // device word: any block that times out raises it

@@ -736,8 +736,13 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
     for (int jj = 0; jj < gsize; ++jj, ++q) {
       const int64_t i_tile = g0 + jj;
       const int64_t tile = lane + i_tile * lanes;
-      const int64_t t0 = tile * tile_elems;
-      const int64_t tbytes = min(tile_elems, chunk_elems - t0) * R::kEsize;
+      // tile geometry: n_head small tiles, n_big big tiles, small tiles to the end of the chunk
+      const int64_t nhb = a.n_head + a.n_big;
+      const int64_t t0 = tile < a.n_head ? tile * a.small_elems
+                         : tile < nhb    ? a.n_head * a.small_elems + (tile - a.n_head) * tile_elems
+                                         : a.n_head * a.small_elems + a.n_big * tile_elems + (tile - nhb) * a.small_elems;
+      const int64_t tlen = tile < a.n_head || tile >= nhb ? a.small_elems : tile_elems;
+      const int64_t tbytes = min(tlen, chunk_elems - t0) * R::kEsize;
       const int64_t t0_bytes = t0 * R::kEsize;
       c.tile = tile;
       const DevOp op = ops[s];

@@ -102,6 +102,7 @@ struct Config {
   int tma = 3;                       // bulk (TMA) engine on same-device peers: bit 0 copies, bit 1 reductions
   int balance = 1;                   // per-component lane multipliers (lane_multipliers; 2: rounded up)
   int mult_cap = 4;                  // largest lane multiplier
+  int taper = 1;                     // quarter tiles in the first and last round of every lane
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
@@ -122,6 +123,7 @@ Config config_from_env() {
   c.tma = static_cast<int>(env_int("GC3_TMA", c.tma));
   c.balance = static_cast<int>(env_int("GC3_BALANCE", c.balance));
   c.mult_cap = static_cast<int>(env_int("GC3_MULT_CAP", c.mult_cap));
+  c.taper = static_cast<int>(env_int("GC3_TAPER", c.taper));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
 }
@@ -1214,6 +1216,7 @@ struct CallPlan {
   KernelFn fn = nullptr;
   int redop = -1;
   bool uniform = false;  // every thread block on the base lanes (LL with per-connection lanes)
+  int64_t small_elems = 0, n_head = 0, n_big = 0;  // tapered tiles (see plan_call)
   int weight = 0;        // units per lane: sum of multipliers, or thread blocks when uniform
 };
 
@@ -1310,6 +1313,31 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   if (cp.ll && tile_bytes % 8) tile_bytes = tile_bytes / 8 * 8;
   cp.tile_elems = std::max<int64_t>(tile_bytes / cp.kesize, chunk_bytes > 0 ? 1 : 0);
   cp.ntiles = cp.tile_elems > 0 ? (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems : 0;
+  cp.small_elems = cp.tile_elems;
+  cp.n_head = 0;
+  cp.n_big = cp.ntiles;
+  {  // tapered tiles: the first and the last round of every lane use quarter tiles, so pipelines
+     // fill and drain in a quarter of the time (the drain is one unit moving its last tile alone)
+    int lcm = 1;
+    if (!cp.uniform)
+      for (const auto& g : ir.mult)
+        for (int m : g) lcm = std::lcm(lcm, std::max(m, 1));
+    const int64_t lanes_all = static_cast<int64_t>(lanes) * lcm;
+    const int64_t T = cp.tile_elems, C = cp.chunk_elems;
+    const int64_t align = std::max<int64_t>(1, 16 / cp.kesize);
+    const int64_t ts = (T / 4) / align * align;
+    const int64_t round_small = 4 * lanes_all * ts;  // one round of quarter tiles
+    if (c->cfg.taper && c->cfg.tile_bytes <= 0 && !cp.ll && ts * cp.kesize >= (4 << 10) && C >= 2 * round_small + 2 * lanes_all * T) {
+      const int64_t nh = 4 * lanes_all;
+      const int64_t nb = (C - 2 * round_small) / T;
+      const int64_t rest = C - nh * ts - nb * T;
+      const int64_t nt = (rest + ts - 1) / ts;
+      cp.small_elems = ts;
+      cp.n_head = nh;
+      cp.n_big = nb;
+      cp.ntiles = nh + nb + nt;
+    }
+  }
   if (cp.ntiles < lanes) lanes = static_cast<int>(std::max<int64_t>(cp.ntiles, 1));
   cp.lanes = lanes;
   cp.unit_warps = uw;
@@ -1408,6 +1436,9 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.chunk_elems = cp.chunk_elems;
   a.tile_elems = cp.tile_elems;
   a.ntiles = cp.ntiles;
+  a.small_elems = cp.small_elems;
+  a.n_head = cp.n_head;
+  a.n_big = cp.n_big;
   a.epoch = ++ds->epoch;
   a.timeout_ns = static_cast<uint64_t>(c0->cfg.timeout_ms) * 1000000ull;
   a.abort_flag = ds->d_abort;
@@ -1920,6 +1951,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "tma") c.tma = static_cast<int>(value);
   else if (k == "balance") c.balance = static_cast<int>(value);
   else if (k == "mult_cap") c.mult_cap = static_cast<int>(value);
+  else if (k == "taper") c.taper = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;

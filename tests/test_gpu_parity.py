@@ -249,3 +249,14 @@ def test_msccl_xml_registration(name, count, fold, tmp_path):
     finally:
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("name,count,dtype", [("hier_ar_2x4_par1", 8 * (1 << 20), "float32"),
+                                              ("twostep_a2a_2x4", 1 << 20, "bfloat16"),
+                                              ("ring_ar_8_ch1", 8 * (1 << 20) + 8 * 12345, "float32"),
+                                              ("ring_rs_8", 1 << 20, "int32")])
+def test_tapered_tiles(name, count, dtype):
+    """Quarter tiles in the first and last round of every lane (tapered geometry) on few lanes,
+    where it is active, vs uniform tiles: same bits as the oracle."""
+    _check(name, count, dtype, lanes=2, balance=0)
+    _check(name, count, dtype, lanes=2, balance=0, taper=0)
