@@ -107,6 +107,7 @@ struct LaunchArgs {
   int32_t unit_warps;   // warps interpreting one (thread block, lane); kThreads/32 divisible by it
   int32_t group;        // tiles per op-major group inside a lane (1 = tile-major)
   int32_t tma_stages;   // shared-memory stages per unit for bulk copies (0: register path only)
+  int32_t stage_bytes;  // bytes per stage
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions

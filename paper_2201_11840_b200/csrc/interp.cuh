@@ -328,7 +328,7 @@ __device__ GC3_MOVE_ATTR void move(const char* a, const char* b, char* o0, char*
 // Tensor Memory Accelerator's 1-D bulk engine: one thread keeps `stages` x kStageBytes in flight
 // (cp.async.bulk global->shared, completion on an mbarrier; cp.async.bulk shared->global as bulk
 // groups), so the unit's bandwidth no longer depends on registers or resident warps.
-constexpr int kStageBytes = 16 << 10;
+constexpr int kStageBytes = 16 << 10;  // largest stage (LaunchArgs::stage_bytes picks <= this)
 constexpr int kMaxStages = 8;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -367,7 +367,8 @@ __device__ __forceinline__ bool is_tma_copy(int op, bool in_direct) {
 
 // Per-unit bulk-copy pipeline state (lives in thread 0 of the unit).
 struct Tma {
-  char* stage;    // stages x kStageBytes of shared memory
+  char* stage;    // stages x sb bytes of shared memory
+  int sb;         // bytes per stage (a multiple of 1 KiB, <= kStageBytes)
   uint64_t* bar;  // one mbarrier per stage
   int stages;
   uint32_t* seq;  // (shared) pieces issued so far: stage = seq % stages, parity = (seq / stages) & 1;
@@ -379,12 +380,13 @@ struct Tma {
 // ordered for the generic proxy by the caller's fence.proxy.async).
 static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int64_t s0, char* o1, int64_t s1, int64_t nbytes,
                          int count) {
-  const int64_t per_seg = (nbytes + kStageBytes - 1) / kStageBytes;
+  const int SB = m.sb;
+  const int64_t per_seg = (nbytes + SB - 1) / SB;
   const int64_t total = per_seg * count;
   auto piece = [&](int64_t p, const char*& src, char*& d0, char*& d1, uint32_t& bytes) {
     const int64_t j = p / per_seg, k = p - j * per_seg;
-    const int64_t off = k * kStageBytes;
-    bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kStageBytes), nbytes - off));
+    const int64_t off = k * SB;
+    bytes = static_cast<uint32_t>(min(static_cast<int64_t>(SB), nbytes - off));
     src = a + j * sa + off;
     d0 = o0 + j * s0 + off;
     d1 = o1 ? o1 + j * s1 + off : nullptr;
@@ -399,7 +401,7 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     const uint32_t g = base + static_cast<uint32_t>(p);
     uint64_t* bar = m.bar + g % m.stages;
     mbar_expect_tx(bar, bytes);
-    bulk_load(m.stage + static_cast<size_t>(g % m.stages) * kStageBytes, src, bytes, bar);
+    bulk_load(m.stage + static_cast<size_t>(g % m.stages) * SB, src, bytes, bar);
   }
   for (int64_t p = 0; p < total; ++p) {
     const char* src;
@@ -407,7 +409,7 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     uint32_t bytes;
     piece(p, src, d0, d1, bytes);
     const uint32_t g = base + static_cast<uint32_t>(p);
-    char* sm = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
+    char* sm = m.stage + static_cast<size_t>(g % m.stages) * SB;
     mbar_wait(m.bar + g % m.stages, (g / m.stages) & 1);
     bulk_store(d0, sm, bytes);
     if (d1) bulk_store(d1, sm, bytes);
@@ -425,7 +427,7 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
       piece(np, nsrc, n0, n1, nbytes_p);
       uint64_t* bar = m.bar + rg % m.stages;
       mbar_expect_tx(bar, nbytes_p);
-      bulk_load(m.stage + static_cast<size_t>(rg % m.stages) * kStageBytes, nsrc, nbytes_p, bar);
+      bulk_load(m.stage + static_cast<size_t>(rg % m.stages) * SB, nsrc, nbytes_p, bar);
     }
   }
   bulk_wait_all();
@@ -443,7 +445,8 @@ __device__ __forceinline__ void unit_sync(int uw, int bar_id, int n);
 template <class R, bool RED>
 __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int64_t sb, char* o0, int64_t s0, char* o1,
                            int64_t s1, int64_t nbytes, int count, int t, int n, int uw, int bar_id) {
-  constexpr int P = RED ? kStageBytes / 2 : kStageBytes;  // bytes of one operand per piece
+  const int SB = m.sb;
+  const int P = RED ? SB / 2 : SB;  // bytes of one operand per piece
   const int64_t per_seg = (nbytes + P - 1) / P;
   const int64_t total = per_seg * count;
   auto piece = [&](int64_t p, int64_t& j, int64_t& off, uint32_t& bytes) {
@@ -457,7 +460,7 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
     uint32_t bytes;
     piece(p, j, off, bytes);
     const uint32_t g = base + static_cast<uint32_t>(p);
-    char* st = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
+    char* st = m.stage + static_cast<size_t>(g % m.stages) * SB;
     uint64_t* bar = m.bar + g % m.stages;
     mbar_expect_tx(bar, RED ? 2 * bytes : bytes);
     bulk_load(st, a + j * sa + off, bytes, bar);
@@ -472,7 +475,7 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
     uint32_t bytes;
     piece(p, j, off, bytes);
     const uint32_t g = base + static_cast<uint32_t>(p);
-    const char* st = m.stage + static_cast<size_t>(g % m.stages) * kStageBytes;
+    const char* st = m.stage + static_cast<size_t>(g % m.stages) * SB;
     mbar_wait(m.bar + g % m.stages, (g / m.stages) & 1);
     const uint4* x = reinterpret_cast<const uint4*>(st);
     const uint4* y = reinterpret_cast<const uint4*>(st + P);
@@ -670,11 +673,11 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const int L0 = a.lanes;  // base lanes; thread block i runs L0 x mult_i lanes
   if (unit >= a.weight * L0) return;  // a whole unit leaves together
   const int bar_id = 1 + uib;
-  // TMA staging: a.tma_stages x kStageBytes of dynamic shared memory per unit, one mbarrier each
+  // TMA staging: a.tma_stages x a.stage_bytes of dynamic shared memory per unit, one mbarrier each
   extern __shared__ __align__(128) char s_stage[];
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
   __shared__ uint32_t s_seq[kThreads / 32];
-  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * kStageBytes, s_bar[uib], a.tma_stages, &s_seq[uib]};
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib]};
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
     for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);

@@ -1217,6 +1217,7 @@ struct CallPlan {
   int redop = -1;
   bool uniform = false;  // every thread block on the base lanes (LL with per-connection lanes)
   int64_t small_elems = 0, n_head = 0, n_big = 0;  // tapered tiles (see plan_call)
+  int stage_bytes = 16 << 10;
   int weight = 0;        // units per lane: sum of multipliers, or thread blocks when uniform
 };
 
@@ -1274,8 +1275,11 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   const int units_per_block = kThreads / 32 / uw;
   // TMA staging for pure-copy ops (same-device peers; shared-memory stages per unit)
   cp.tma_stages = 0;
-  if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, kSmemBudget / (units_per_block * kStageBytesHost));
-  cp.smem = static_cast<size_t>(units_per_block) * cp.tma_stages * kStageBytesHost;
+  // three or more stages per unit: 16 KiB stages for wide units, smaller ones (>= 4 KiB) when
+  // many narrow units share the SM's shared memory
+  cp.stage_bytes = std::max(4 << 10, std::min(kStageBytesHost, kSmemBudget / (units_per_block * 3) / 1024 * 1024));
+  if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, kSmemBudget / (units_per_block * cp.stage_bytes));
+  cp.smem = static_cast<size_t>(units_per_block) * cp.tma_stages * cp.stage_bytes;
   int bps = occupancy(cp.smem);
   if (bps * ds.num_sms * units_per_block < weight && cp.smem) {  // staging would break co-residency
     cp.tma_stages = 0;
@@ -1426,6 +1430,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
   a.tma_stages = cp.tma_stages;
+  a.stage_bytes = cp.stage_bytes;
   a.tma_ops = c0->cfg.tma;
   a.discard = c0->cfg.discard;
   // LL: every message travels as flagged lines through the receiver's FIFO (lowest latency, no
