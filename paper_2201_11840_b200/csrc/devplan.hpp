@@ -48,7 +48,8 @@ struct DevOp {  // 32 bytes
   uint8_t src_rbuf;  // buffer the src span is read from (kSource: the caller's const send buffer)
   uint8_t dst_rbuf;  // buffer reduce's dst span is read from
   uint8_t nmsg;      // trailing deps that are message deps (kMsgDep; skipped in LL launches)
-  uint8_t pad;
+  uint8_t hot;       // 1: the data this op writes is read again soon (its message's receiver reads
+                     // it): stores keep it in L2 (evict_last)
 };
 
 struct DevDep {

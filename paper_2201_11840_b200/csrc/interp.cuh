@@ -353,6 +353,20 @@ __device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t
 __device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void bulk_store_hint(void* gmem, const void* smem, uint32_t bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem), "r"(smem_addr(smem)),
+               "r"(bytes), "l"(pol)
+               : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void st_vec_hint(uint4* p, uint4 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
@@ -373,6 +387,7 @@ struct Tma {
   int stages;
   uint32_t* seq;  // (shared) pieces issued so far: stage = seq % stages, parity = (seq / stages) & 1;
                   // written by thread 0 at the end of an op, read by the unit's threads in a later one
+  uint64_t pol;   // L2 policy for the stores of the current op (0: none)
 };
 
 // Copies `count` segments of `nbytes` (segment j: a + j*sa -> o0 + j*s0 [, o1 + j*s1]).
@@ -411,8 +426,13 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     const uint32_t g = base + static_cast<uint32_t>(p);
     char* sm = m.stage + static_cast<size_t>(g % m.stages) * SB;
     mbar_wait(m.bar + g % m.stages, (g / m.stages) & 1);
-    bulk_store(d0, sm, bytes);
-    if (d1) bulk_store(d1, sm, bytes);
+    if (m.pol) {
+      bulk_store_hint(d0, sm, bytes, m.pol);
+      if (d1) bulk_store_hint(d1, sm, bytes, m.pol);
+    } else {
+      bulk_store(d0, sm, bytes);
+      if (d1) bulk_store(d1, sm, bytes);
+    }
     bulk_commit();
     // refill the previous piece's stage once its store has read it: the store just issued stays in
     // flight (wait_group.read 1), so loads and stores overlap instead of alternating
@@ -483,8 +503,13 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
     uint4* d1 = o1 ? reinterpret_cast<uint4*>(o1 + j * s1 + off) : nullptr;
     for (int v = t; v < static_cast<int>(bytes >> 4); v += n) {
       const uint4 r = RED ? R::template vec<uint4>(x[v], y[v]) : x[v];
-      st_vec(d0 + v, r);
-      if (d1) st_vec(d1 + v, r);
+      if (m.pol) {
+        st_vec_hint(d0 + v, r, m.pol);
+        if (d1) st_vec_hint(d1 + v, r, m.pol);
+      } else {
+        st_vec(d0 + v, r);
+        if (d1) st_vec(d1 + v, r);
+      }
     }
     unit_sync(uw, bar_id, n);  // the stage is consumed (stores issued from registers): refill it
     if (t == 0 && p + m.stages < total) issue(p + m.stages);
@@ -677,7 +702,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   extern __shared__ __align__(128) char s_stage[];
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
   __shared__ uint32_t s_seq[kThreads / 32];
-  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib]};
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0};
+  const uint64_t pol_last = l2_evict_last_policy();
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
     for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
@@ -749,6 +775,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       const int64_t t0_bytes = t0 * R::kEsize;
       c.tile = tile;
       const DevOp op = ops[s];
+      tma.pol = op.hot ? pol_last : 0;
       const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
       const int tr = op.direct & a.transports;
       const bool in_d = (tr & kInDirect) != 0, out_d = (tr & kOutDirect) != 0;
