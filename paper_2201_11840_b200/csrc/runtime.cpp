@@ -102,7 +102,7 @@ struct Config {
   int tma = 3;                       // bulk (TMA) engine on same-device peers: bit 0 copies, bit 1 reductions
   int balance = 1;                   // per-component lane multipliers (lane_multipliers; 2: rounded up)
   int mult_cap = 4;                  // largest lane multiplier
-  int taper = 1;                     // quarter tiles in the first and last round of every lane
+  int taper = 0;                     // quarter tiles in the first and last round of every lane (measured: no gain)
   int l2hint = 1;                    // evict_last stores for data the receiver reads soon
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
@@ -889,6 +889,16 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       for (size_t s = 0; s < senders[r][t].size(); ++s)
         if (senders[r][t][s].rank >= 0)
           receiver_of[{senders[r][t][s].rank, senders[r][t][s].tb, senders[r][t][s].step}] = {r, static_cast<int>(t), static_cast<int>(s)};
+  // spans each rank reads (for the L2 hints): (buffer, first chunk, end chunk)
+  std::vector<std::vector<std::tuple<Buf, int, int>>> reads(p.ranks());
+  auto storage = [&](Buf b) { return p.inplace && b == Buf::output ? Buf::input : b; };
+  for (int r = 0; r < p.ranks(); ++r)
+    for (const auto& tb : p.gpus[r].tbs)
+      for (const auto& op : tb.ops) {
+        if (op.op == Opcode::recv || op.op == Opcode::nop) continue;
+        reads[r].emplace_back(op.src_buf, op.src_off, op.src_off + op.count);
+        if (op.op == Opcode::reduce) reads[r].emplace_back(op.dst_buf, op.dst_off, op.dst_off + op.count);
+      }
   std::set<std::tuple<int, int, int>> fifo_conn;
   std::set<std::tuple<int, int, int>> pub_sem;
   for (int r = 0; r < p.ranks(); ++r)
@@ -952,9 +962,13 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         if (pub_sem.count({r, static_cast<int>(t), static_cast<int>(s)})) o.direct |= kPubSem;
         if (c0->cfg.l2hint && op_sends(op.op)) {  // its receiver reads what it writes: keep it in L2
           const auto rcv = receiver_of.find({r, static_cast<int>(t), static_cast<int>(s)});
-          if (!(o.direct & kOutDirect)) o.hot = 1;  // FIFO slot or pulled span: read by the receive
-          else if (rcv != receiver_of.end() && p.gpus[std::get<0>(rcv->second)].tbs[std::get<1>(rcv->second)].ops[std::get<2>(rcv->second)].op == Opcode::rcs)
-            o.hot = 1;  // written into a span the receiver forwards from
+          if (!(o.direct & kOutDirect)) {
+            o.hot = 1;  // FIFO slot or pulled span: read by the receive
+          } else if (rcv != receiver_of.end()) {  // a span of the receiving rank some op reads again
+            const int rr = std::get<0>(rcv->second);
+            for (const auto& [b, lo, hi] : reads[rr])
+              if (storage(b) == storage(op.dst_buf) && lo < op.dst_off + op.count && op.dst_off < hi) o.hot = 1;
+          }
         }
         if (ir0.lane_mask) {
           if (op_sends(op.op) && tb.send_peer >= 0 && !fifo_conn.count({r, tb.send_peer, tb.channel})) o.direct |= kNoCtrOut;

@@ -258,5 +258,5 @@ def test_msccl_xml_registration(name, count, fold, tmp_path):
 def test_tapered_tiles(name, count, dtype):
     """Quarter tiles in the first and last round of every lane (tapered geometry) on few lanes,
     where it is active, vs uniform tiles: same bits as the oracle."""
-    _check(name, count, dtype, lanes=2, balance=0)
+    _check(name, count, dtype, lanes=2, balance=0, taper=1)
     _check(name, count, dtype, lanes=2, balance=0, taper=0)
