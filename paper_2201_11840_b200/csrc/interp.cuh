@@ -657,6 +657,90 @@ __device__ bool ll_op(int opcode, int count, char* src0, const char* srcr0, char
   return true;
 }
 
+// The data movement of one op on one tile (Simple transports): staged reductions, bulk copies or
+// the register path. `in` is the incoming message (FIFO slot or pulled span; segment j at
+// + j * in_stride; null when already in place or absent), `out` the outgoing one (FIFO slot or the
+// receiver's span; null when pulled or absent). Reads of the op's spans go through srcr / dstr.
+template <class R>
+__device__ __forceinline__ void transfer(const DevOp& op, bool in_d, char* src, char* dst, const char* srcr, const char* dstr,
+                                         const char* in, int64_t in_stride, char* out, int64_t out_stride, int64_t tbytes,
+                                         int64_t chunk_bytes, int tma_ops, Tma& tma, int t, int n, int uw, int bar_id) {
+  if (R::kReduce && (tma_ops & 2) && tma.stages >= 2 && in &&
+             (op.opcode == kOpRrc || op.opcode == kOpRrcs || op.opcode == kOpRrs) &&
+             ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(srcr) | reinterpret_cast<uintptr_t>(dst) |
+               reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) |
+               static_cast<uintptr_t>(chunk_bytes) | static_cast<uintptr_t>(in_stride)) & 15) == 0) {
+    // staged reduction: local operand (op.src read) (op) message, both through shared memory
+    switch (op.opcode) {
+      case kOpRrc: tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+      case kOpRrcs: tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id); break;
+      case kOpRrs:
+        if (out) tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+        break;
+      default: break;
+    }
+  } else if ((tma_ops & 1) && tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
+             ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
+               reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) | static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
+    if (tma_ops & 4) {  // bulk loads, stores from registers by the whole unit
+      switch (op.opcode) {
+        case kOpSend:
+          if (out) tma_stream<R, false>(tma, srcr, chunk_bytes, nullptr, 0, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+          break;
+        case kOpRecv: tma_stream<R, false>(tma, in, in_stride, nullptr, 0, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+        case kOpCopy: tma_stream<R, false>(tma, srcr, chunk_bytes, nullptr, 0, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
+        case kOpRcs:
+          if (!in_d) tma_stream<R, false>(tma, in, in_stride, nullptr, 0, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id);
+          else if (out) tma_stream<R, false>(tma, src, chunk_bytes, nullptr, 0, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
+          break;
+        default: break;
+      }
+    } else if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier
+      fence_proxy_async_global();  // generic-proxy acquires above -> async-proxy reads
+      switch (op.opcode) {
+        case kOpSend:
+          if (out) tma_copy(tma, srcr, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
+          break;
+        case kOpRecv: tma_copy(tma, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
+        case kOpCopy: tma_copy(tma, srcr, chunk_bytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
+        case kOpRcs:
+          if (!in_d) tma_copy(tma, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count);
+          else if (out) tma_copy(tma, src, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
+          break;
+        default: break;
+      }
+      fence_proxy_async_global();  // async-proxy writes -> the generic release below
+    }
+  } else {
+    for (int j = 0; j < op.count; ++j) {
+      char* sj = src + j * chunk_bytes;
+      char* dj = dst + j * chunk_bytes;
+      const char* sr = srcr + j * chunk_bytes;
+      const char* dr = dstr + j * chunk_bytes;
+      const char* mi = in ? in + j * in_stride : nullptr;
+      char* mo = out ? out + j * out_stride : nullptr;
+      switch (op.opcode) {
+        case kOpSend:
+          if (mo) move<R>(sr, nullptr, mo, nullptr, tbytes, t, n);
+          break;
+        case kOpRecv:
+          if (mi) move<R>(mi, nullptr, dj, nullptr, tbytes, t, n);
+          break;
+        case kOpCopy: move<R>(sr, nullptr, dj, nullptr, tbytes, t, n); break;
+        case kOpReduce: move<R>(dr, sr, dj, nullptr, tbytes, t, n); break;
+        case kOpRrc: move<R>(sr, mi, dj, nullptr, tbytes, t, n); break;
+        case kOpRcs:
+          if (mi) move<R>(mi, nullptr, sj, mo, tbytes, t, n);
+          else if (mo) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
+          break;
+        case kOpRrcs: move<R>(sr, mi, sj, mo, tbytes, t, n); break;
+        case kOpRrs: move<R>(sr, mi, nullptr, mo, tbytes, t, n); break;
+        default: break;
+      }
+    }
+  }
+}
+
 // ------------------------------------------------------------------ the interpreter
 // A "unit" of `unit_warps` warps interprets one (IR thread block, lane): for each tile of the lane,
 // for each op in order:
@@ -833,79 +917,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
         ok = ll_op<R>(op.opcode, op.count, src, srcr, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
                       in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
                       static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);
-      } else if (R::kReduce && (a.tma_ops & 2) && tma.stages >= 2 && in &&
-                 (op.opcode == kOpRrc || op.opcode == kOpRrcs || op.opcode == kOpRrs) &&
-                 ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(srcr) | reinterpret_cast<uintptr_t>(dst) |
-                   reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) |
-                   static_cast<uintptr_t>(chunk_bytes) | static_cast<uintptr_t>(in_stride)) & 15) == 0) {
-        // staged reduction: local operand (op.src read) (op) message, both through shared memory
-        switch (op.opcode) {
-          case kOpRrc: tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
-          case kOpRrcs: tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id); break;
-          case kOpRrs:
-            if (out) tma_stream<R, true>(tma, srcr, chunk_bytes, in, in_stride, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
-            break;
-          default: break;
-        }
-      } else if ((a.tma_ops & 1) && tma.stages > 0 && is_tma_copy(op.opcode, in_d) &&
-                 ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(in) |
-                   reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) | static_cast<uintptr_t>(chunk_bytes)) & 15) == 0) {
-        if (a.tma_ops & 4) {  // bulk loads, stores from registers by the whole unit
-          switch (op.opcode) {
-            case kOpSend:
-              if (out) tma_stream<R, false>(tma, srcr, chunk_bytes, nullptr, 0, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
-              break;
-            case kOpRecv: tma_stream<R, false>(tma, in, in_stride, nullptr, 0, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
-            case kOpCopy: tma_stream<R, false>(tma, srcr, chunk_bytes, nullptr, 0, dst, chunk_bytes, nullptr, 0, tbytes, op.count, t, n, uw, bar_id); break;
-            case kOpRcs:
-              if (!in_d) tma_stream<R, false>(tma, in, in_stride, nullptr, 0, src, chunk_bytes, out, out_stride, tbytes, op.count, t, n, uw, bar_id);
-              else if (out) tma_stream<R, false>(tma, src, chunk_bytes, nullptr, 0, out, out_stride, nullptr, 0, tbytes, op.count, t, n, uw, bar_id);
-              break;
-            default: break;
-          }
-        } else if (t == 0 && tbytes > 0) {  // one thread drives the bulk engine; the unit waits at the barrier
-          fence_proxy_async_global();  // generic-proxy acquires above -> async-proxy reads
-          switch (op.opcode) {
-            case kOpSend:
-              if (out) tma_copy(tma, srcr, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
-              break;
-            case kOpRecv: tma_copy(tma, in, in_stride, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
-            case kOpCopy: tma_copy(tma, srcr, chunk_bytes, dst, chunk_bytes, nullptr, 0, tbytes, op.count); break;
-            case kOpRcs:
-              if (!in_d) tma_copy(tma, in, in_stride, src, chunk_bytes, out, out_stride, tbytes, op.count);
-              else if (out) tma_copy(tma, src, chunk_bytes, out, out_stride, nullptr, 0, tbytes, op.count);
-              break;
-            default: break;
-          }
-          fence_proxy_async_global();  // async-proxy writes -> the generic release below
-        }
       } else {
-        for (int j = 0; j < op.count; ++j) {
-          char* sj = src + j * chunk_bytes;
-          char* dj = dst + j * chunk_bytes;
-          const char* sr = srcr + j * chunk_bytes;
-          const char* dr = dstr + j * chunk_bytes;
-          const char* mi = in ? in + j * in_stride : nullptr;
-          char* mo = out ? out + j * out_stride : nullptr;
-          switch (op.opcode) {
-            case kOpSend:
-              if (mo) move<R>(sr, nullptr, mo, nullptr, tbytes, t, n);
-              break;
-            case kOpRecv:
-              if (mi) move<R>(mi, nullptr, dj, nullptr, tbytes, t, n);
-              break;
-            case kOpCopy: move<R>(sr, nullptr, dj, nullptr, tbytes, t, n); break;
-            case kOpReduce: move<R>(dr, sr, dj, nullptr, tbytes, t, n); break;
-            case kOpRrc: move<R>(sr, mi, dj, nullptr, tbytes, t, n); break;
-            case kOpRcs:
-              if (mi) move<R>(mi, nullptr, sj, mo, tbytes, t, n);
-              else if (mo) move<R>(sj, nullptr, mo, nullptr, tbytes, t, n);
-              break;
-            case kOpRrcs: move<R>(sr, mi, sj, mo, tbytes, t, n); break;
-            case kOpRrs: move<R>(sr, mi, nullptr, mo, tbytes, t, n); break;
-            default: break;
-          }
-        }
+        transfer<R>(op, in_d, src, dst, srcr, dstr, in, in_stride, out, out_stride, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw,
+                    bar_id);
       }
       if (t == 0) stamp(q, 2);
       if (!unit_and(ok, uw, bar_id, n)) return;
