@@ -57,6 +57,7 @@ struct DevDep {
   int32_t step;  // depended-on step
   int32_t nops;  // op count of the depended-on thread block (progress encoding)
   int32_t mult;  // lane multiplier of the depended-on thread block (it has lanes x mult lanes)
+  int32_t tbi;   // launch index of the depended-on thread block (work-queue progress table)
 };
 
 struct DevTb {
@@ -113,6 +114,9 @@ struct LaunchArgs {
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
   int32_t uniform;      // 1: every thread block runs `lanes` lanes (LL launches: FIFOs need matched lanes)
+  int32_t wq;           // 1: work-queue mode (see interp.cuh interp_wq)
+  int32_t* wq_next;     // work-queue claim counter (zeroed before the launch)
+  uint64_t* prog;       // work-queue progress: [thread block][tile] = (epoch << 32) | steps done
   char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source (the caller's
                                      // const data the in-place IR's first reads see; = input when
                                      // the working buffer was pre-copied)

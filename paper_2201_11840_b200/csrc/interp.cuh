@@ -765,6 +765,89 @@ __device__ __forceinline__ void unit_sync(int uw, int bar_id, int n) {
   else asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(n) : "memory");
 }
 
+// Work-queue mode (programs whose messages are all direct or pulled, Simple protocol, every rank in
+// this launch). A work item is one (thread block, tile): the unit that claims it runs all of the
+// thread block's ops on that tile in order. Units claim items from one counter in tile-major order
+// (item = tile * ntbs + thread block), so a unit never idles while any work is left, whatever the
+// phase structure of the program. Deps and message deps wait on a per-(thread block, tile) progress
+// word; every dependency of an item is on the same tile, and with at least ntbs co-resident units all
+// items of a tile are claimed before any unit can block on one of them: no deadlock.
+#ifndef GC3_WQ_NOINLINE
+#define GC3_WQ_NOINLINE 1
+#endif
+#if GC3_WQ_NOINLINE
+#define GC3_WQ_ATTR __noinline__
+#else
+#define GC3_WQ_ATTR
+#endif
+struct WqArgs {  // the launch arguments the work queue reads (by value: no local copy of LaunchArgs)
+  const DevTb* tbs;
+  const DevOp* ops;
+  const DevDep* deps;
+  int32_t* wq_next;
+  uint64_t* prog;
+  int32_t* abort_flag;
+  uint64_t* err_info;
+  uint64_t timeout_ns;
+  int64_t chunk_elems, tile_elems, ntiles;
+  uint64_t epoch;
+  int ntbs, tma_ops;
+};
+
+template <class R>
+__device__ GC3_WQ_ATTR void interp_wq(const WqArgs a, char* const* s_bufs, Tma& tma, uint64_t pol_last, int t, int n, int uw, int uib,
+                          int bar_id) {
+  __shared__ int s_item[kThreads / 32];
+  const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
+  const int64_t chunk_bytes = chunk_elems * R::kEsize;
+  const int64_t nitems = ntiles * a.ntbs;
+  const uint64_t tag = a.epoch << 32;
+  for (;;) {
+    if (t == 0) s_item[uib] = static_cast<int>(atomicAdd(a.wq_next, 1));
+    unit_sync(uw, bar_id, n);
+    const int64_t item = s_item[uib];
+    if (item >= nitems) return;
+    const int tbi = static_cast<int>(item % a.ntbs);
+    const int64_t tile = item / a.ntbs;
+    const DevTb tb = a.tbs[tbi];
+    char* const* const mine = s_bufs + kBufs * tb.rank_slot;
+    char* const* const peer = s_bufs + kBufs * (tb.peer_slot >= 0 ? tb.peer_slot : 0);
+    char* const* const rpeer = s_bufs + kBufs * (tb.recv_slot >= 0 ? tb.recv_slot : 0);
+    const DevOp* const ops = a.ops + tb.op_begin;
+    const int64_t t0 = tile * tile_elems;
+    const int64_t tbytes = min(tile_elems, chunk_elems - t0) * R::kEsize;
+    const int64_t t0_bytes = t0 * R::kEsize;
+    Ctx c{a.abort_flag, a.err_info, a.timeout_ns, tb.rank_slot, tbi, 0, tile};
+    for (int s = 0; s < tb.nops; ++s) {
+      const DevOp op = ops[s];
+      c.step = s;
+      tma.pol = op.hot ? pol_last : 0;
+      bool ok = true;
+      for (int d = t; d < op.ndeps; d += n) {  // deps and message deps: same tile, progress words
+        const DevDep dd = a.deps[op.dep_begin + d];
+        ok = ok && wait_geq(a.prog + static_cast<int64_t>(dd.tbi) * ntiles + tile, tag | static_cast<uint64_t>(dd.step + 1), false, c, 1);
+      }
+      if (!unit_and(ok, uw, bar_id, n)) return;
+      const bool in_d = (op.direct & kInDirect) != 0, in_p = (op.direct & kInPull) != 0;
+      const bool out_d = (op.direct & kOutDirect) != 0;
+      char* src = mine[op.src_buf] + op.src_off * chunk_bytes + t0_bytes;
+      char* dst = mine[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes;
+      const char* srcr = mine[op.src_rbuf] + op.src_off * chunk_bytes + t0_bytes;
+      const char* dstr = mine[op.dst_rbuf] + op.dst_off * chunk_bytes + t0_bytes;
+      const char* in = in_p ? rpeer[op.in_buf] + op.in_off * chunk_bytes + t0_bytes : nullptr;
+      char* out = out_d ? peer[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes : nullptr;
+      transfer<R>(op, in_d, src, dst, srcr, dstr, in, chunk_bytes, out, chunk_bytes, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw,
+                  bar_id);
+      if (!unit_and(true, uw, bar_id, n)) return;
+      if (t == 0 && (op.has_dep || (op.direct & kPubSem))) {
+        fence_acq_rel(false);
+        st_relaxed(a.prog + static_cast<int64_t>(tbi) * ntiles + tile, tag | static_cast<uint64_t>(s + 1), false);
+      }
+    }
+    unit_sync(uw, bar_id, n);  // s_item is rewritten by thread 0 next
+  }
+}
+
 template <class R, bool LL>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
   // every rank's buffers of this launch, staged in shared memory once: ops index them by rank slot
@@ -788,6 +871,18 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   __shared__ uint32_t s_seq[kThreads / 32];
   Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0};
   const uint64_t pol_last = l2_evict_last_policy();
+  if (!LL && a.wq) {
+    if (t == 0) s_seq[uib] = 0;
+    if (t == 0 && a.tma_stages > 0) {
+      for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unit_sync(uw, bar_id, n);
+    const WqArgs w{a.tbs, a.ops, a.deps, a.wq_next, a.prog, a.abort_flag, a.err_info, a.timeout_ns,
+                   a.chunk_elems, a.tile_elems, a.ntiles, a.epoch, a.ntbs, a.tma_ops};
+    interp_wq<R>(w, s_bufs, tma, pol_last, t, n, uw, uib, bar_id);
+    return;
+  }
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
     for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);

@@ -104,6 +104,8 @@ struct Config {
   int mult_cap = 4;                  // largest lane multiplier
   int taper = 0;                     // quarter tiles in the first and last round of every lane (measured: no gain)
   int l2hint = 1;                    // evict_last stores for data the receiver reads soon
+  int wq = 1;                        // work-queue mode where possible (interp_wq)
+  int wq_items = 6;                  // work items per unit targeted by the work-queue tile size
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
@@ -126,6 +128,8 @@ Config config_from_env() {
   c.mult_cap = static_cast<int>(env_int("GC3_MULT_CAP", c.mult_cap));
   c.taper = static_cast<int>(env_int("GC3_TAPER", c.taper));
   c.l2hint = static_cast<int>(env_int("GC3_L2HINT", c.l2hint));
+  c.wq = static_cast<int>(env_int("GC3_WQ", c.wq));
+  c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
 }
@@ -265,6 +269,7 @@ struct RankIR {
 // Per-device execution state shared by the ranks a clique hosts on that device.
 struct DevicePlan {  // one registered IR on one device
   bool built = false;
+  bool wq_ok = false;  // work-queue mode possible (no FIFO message, one launch)
   bool source_complete = false;  // every first read of `input` reads the source buffer (source_reads)
   std::vector<int> ranks;  // local ranks in launch order (rank_slot -> rank)
   int ntbs = 0;
@@ -288,6 +293,9 @@ struct DeviceState {
   std::map<std::pair<KernelFn, size_t>, int> occupancy;  // (kernel, dynamic smem) -> blocks per SM
   uint64_t* d_trace = nullptr;  // event log of the last traced launch
   size_t trace_bytes = 0;
+  int32_t* d_wq_next = nullptr;  // work-queue claim counter
+  uint64_t* d_prog = nullptr;    // work-queue progress table
+  size_t prog_bytes = 0;
   int trace_grid = 0, trace_ops = 0, trace_lanes = 0;
 };
 
@@ -917,14 +925,18 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   // semaphores: lanes x mult per thread block, in launch order
   const auto& mult = ir0.mult;
   std::map<std::pair<int, int>, int> sem_base;  // (rank, tb index) -> first semaphore
+  std::map<std::pair<int, int>, int> launch_index;  // (rank, tb index) -> thread block index in the launch
   int sem_next = 0, weight = 0;
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
     const int r = plan.ranks[slot];
     for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
       sem_base[{r, static_cast<int>(t)}] = sem_next;
+      launch_index[{r, static_cast<int>(t)}] = static_cast<int>(launch_index.size());
       sem_next += L * mult[r][t];
     }
   }
+  // work-queue mode needs every message direct or pulled (no FIFO) and every rank in this launch
+  plan.wq_ok = ir0.lane_mask != 0 && fifo_conn.empty();
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
     const int r = plan.ranks[slot];
     Comm* c = cl->local[r];
@@ -993,6 +1005,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
           dd.step = dp.step;
           dd.nops = static_cast<int>(g.tbs[ti].ops.size());
           dd.mult = mult[r][ti];
+          dd.tbi = launch_index[{r, ti}];
           deps.push_back(dd);
         }
         if (o.direct & (kInDirect | kInPull)) {  // message dep on the sending op
@@ -1003,6 +1016,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
             dd.step = sd.step;
             dd.nops = static_cast<int>(p.gpus[sd.rank].tbs[sd.tb].ops.size());
             dd.mult = mult[sd.rank][sd.tb];
+            dd.tbi = launch_index[{sd.rank, sd.tb}];
             deps.push_back(dd);
             o.nmsg = 1;
             o.ndeps = static_cast<int16_t>(o.ndeps + 1);
@@ -1246,6 +1260,7 @@ struct CallPlan {
   bool uniform = false;  // every thread block on the base lanes (LL with per-connection lanes)
   int64_t small_elems = 0, n_head = 0, n_big = 0;  // tapered tiles (see plan_call)
   int stage_bytes = 16 << 10;
+  bool wq = false;  // work-queue mode (interp_wq)
   int weight = 0;        // units per lane: sum of multipliers, or thread blocks when uniform
 };
 
@@ -1397,6 +1412,31 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     if (f->second) break;
   }
   cp.group = std::max(G, 1);
+  // work-queue mode: every co-resident unit claims (thread block, tile) items until none is left
+  cp.wq = false;
+  const bool wq_ok = ds.plans.size() > static_cast<size_t>(id) && ds.plans[id].wq_ok;
+  // (chains of receive-and-forward ops run better on static lanes: measured on ring AllGather /
+  // ReduceScatter; phase-structured programs such as the two-step AllToAll gain: C2 0.31 -> 0.29 ms)
+  if (c->cfg.wq && wq_ok && (!ir.has_chain || c->cfg.wq > 1) && !cp.ll && !sys_scope && c->cfg.lanes <= 0 &&
+      capacity >= ntbs_local && chunk_bytes > 0) {
+    cp.wq = true;
+    cp.uniform = true;
+    const int units = capacity;
+    int64_t tb_bytes = c->cfg.tile_bytes > 0 ? c->cfg.tile_bytes / 16 * 16
+                                              : chunk_bytes * ntbs_local / (static_cast<int64_t>(std::max(1, c->cfg.wq_items)) * units);
+    tb_bytes = std::min<int64_t>(std::max<int64_t>(tb_bytes, 32 << 10), 1 << 20);
+    tb_bytes = align_up(static_cast<size_t>(tb_bytes), 16);
+    if (chunk_bytes <= tb_bytes) tb_bytes = chunk_bytes;
+    cp.tile_elems = std::max<int64_t>(tb_bytes / cp.kesize, 1);
+    cp.ntiles = (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems;
+    cp.small_elems = cp.tile_elems;
+    cp.n_head = 0;
+    cp.n_big = cp.ntiles;
+    cp.lanes = 1;
+    cp.weight = units;
+    cp.group = 1;
+    cp.grid = (units + units_per_block - 1) / units_per_block;
+  }
   return ncclSuccess;
 }
 
@@ -1457,6 +1497,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.ntbs = plan.ntbs;
   a.weight = cp.weight;
   a.uniform = cp.uniform ? 1 : 0;
+  a.wq = cp.wq ? 1 : 0;
   a.lanes = cp.lanes;
   a.unit_warps = cp.unit_warps;
   a.group = cp.group;
@@ -1590,6 +1631,22 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][1] = out;
     a.bufs[slot][2] = c->scratch;
     a.bufs[slot][kSource] = source ? source : in;
+  }
+  if (cp.wq) {  // claim counter reset + progress table (epoch-tagged, never reset)
+    DeviceGuard gw(dev);
+    const size_t need = static_cast<size_t>(plan.ntbs) * cp.ntiles * sizeof(uint64_t);
+    if (!ds->d_wq_next) CUDA_TRY(cudaMalloc(&ds->d_wq_next, 256));
+    if (need > ds->prog_bytes) {
+      if (ds->d_prog) CUDA_TRY(cudaFree(ds->d_prog));
+      ds->d_prog = nullptr;
+      ds->prog_bytes = 0;
+      CUDA_TRY(cudaMalloc(&ds->d_prog, need));
+      CUDA_TRY(cudaMemset(ds->d_prog, 0, need));
+      ds->prog_bytes = need;
+    }
+    CUDA_TRY(cudaMemsetAsync(ds->d_wq_next, 0, sizeof(int32_t), stream));
+    a.wq_next = ds->d_wq_next;
+    a.prog = ds->d_prog;
   }
   CUDA_TRY(interp_launch(cp.fn, a, cp.grid, cp.smem, stream));
   for (const PostCopy& pc : post)
@@ -1783,6 +1840,8 @@ static void release_comm(Comm* c) {
       }
       cudaFree(ds.d_abort);
       if (ds.d_trace) cudaFree(ds.d_trace);
+      if (ds.d_wq_next) cudaFree(ds.d_wq_next);
+      if (ds.d_prog) cudaFree(ds.d_prog);
       cudaFreeHost(ds.h_err);
     }
     g_cliques.erase(cl->key);
@@ -1989,6 +2048,8 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "mult_cap") c.mult_cap = static_cast<int>(value);
   else if (k == "taper") c.taper = static_cast<int>(value);
   else if (k == "l2hint") c.l2hint = static_cast<int>(value);
+  else if (k == "wq") c.wq = static_cast<int>(value);
+  else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;

@@ -260,3 +260,13 @@ def test_tapered_tiles(name, count, dtype):
     where it is active, vs uniform tiles: same bits as the oracle."""
     _check(name, count, dtype, lanes=2, balance=0, taper=1)
     _check(name, count, dtype, lanes=2, balance=0, taper=0)
+
+
+@pytest.mark.parametrize("name,count,dtype", [("twostep_a2a_2x4", 1 << 18, "float32"), ("ring_ag_8", 1 << 17, "bfloat16"),
+                                              ("ring_rs_8", 1 << 17, "int32"), ("twostep_a2a_1x8", 12345, "float16")])
+@pytest.mark.parametrize("wq", [0, 2])
+def test_work_queue_mode(name, count, dtype, wq):
+    """Programs whose messages are all direct or pulled run as a work queue of (thread block, tile)
+    items (interp_wq) or on static lanes: same bits either way."""
+    _check(name, count, dtype, wq=wq)
+    _check(name, count, dtype, wq=wq, wq_items=1)

@@ -1,3 +1,3 @@
-o=gpurun_out/r01t; mkdir -p $o
+o=gpurun_out/r01w; mkdir -p $o
 timeout 900 python -m pytest tests -m gpu -x -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
-for c in c1 c2 c3 c4 c5rs c5ag c2d; do timeout 120 python bench.py --config $c --quick --steps 20 >> $o/quick.jsonl 2>&1; done
+bash tools/ab.sh "wqnoinl:-DGC3_WQ_NOINLINE=1;wqinl:-DGC3_WQ_NOINLINE=0" "c2 c3 c4 c5rs c5ag c1" > $o/ab.txt 2>&1
