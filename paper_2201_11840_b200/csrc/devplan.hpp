@@ -113,6 +113,7 @@ struct LaunchArgs {
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
+  int64_t tma_min;      // bytes below which an op takes the register path
   int32_t uniform;      // 1: every thread block runs `lanes` lanes (LL launches: FIFOs need matched lanes)
   int32_t wq;           // 1: work-queue mode (see interp.cuh interp_wq)
   int32_t* wq_next;     // work-queue claim counter (zeroed before the launch)

@@ -661,10 +661,21 @@ __device__ bool ll_op(int opcode, int count, char* src0, const char* srcr0, char
 // the register path. `in` is the incoming message (FIFO slot or pulled span; segment j at
 // + j * in_stride; null when already in place or absent), `out` the outgoing one (FIFO slot or the
 // receiver's span; null when pulled or absent). Reads of the op's spans go through srcr / dstr.
+#ifndef GC3_TRANSFER_NOINLINE
+#define GC3_TRANSFER_NOINLINE 0
+#endif
+#if GC3_TRANSFER_NOINLINE
+#define GC3_TRANSFER_ATTR __noinline__
+#else
+#define GC3_TRANSFER_ATTR __forceinline__
+#endif
 template <class R>
-__device__ __forceinline__ void transfer(const DevOp& op, bool in_d, char* src, char* dst, const char* srcr, const char* dstr,
+__device__ GC3_TRANSFER_ATTR void transfer(const DevOp& op, bool in_d, char* src, char* dst, const char* srcr, const char* dstr,
                                          const char* in, int64_t in_stride, char* out, int64_t out_stride, int64_t tbytes,
-                                         int64_t chunk_bytes, int tma_ops, Tma& tma, int t, int n, int uw, int bar_id) {
+                                         int64_t chunk_bytes, int tma_ops, Tma& tma, int t, int n, int uw, int bar_id,
+                                         int64_t tma_min) {
+  // small transfers take the register path: one round trip, no bulk-engine setup latency
+  if (tbytes * op.count < tma_min) tma_ops = 0;
   if (R::kReduce && (tma_ops & 2) && tma.stages >= 2 && in &&
              (op.opcode == kOpRrc || op.opcode == kOpRrcs || op.opcode == kOpRrs) &&
              ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(srcr) | reinterpret_cast<uintptr_t>(dst) |
@@ -773,7 +784,7 @@ __device__ __forceinline__ void unit_sync(int uw, int bar_id, int n) {
 // word; every dependency of an item is on the same tile, and with at least ntbs co-resident units all
 // items of a tile are claimed before any unit can block on one of them: no deadlock.
 #ifndef GC3_WQ_NOINLINE
-#define GC3_WQ_NOINLINE 1
+#define GC3_WQ_NOINLINE 0
 #endif
 #if GC3_WQ_NOINLINE
 #define GC3_WQ_ATTR __noinline__
@@ -792,6 +803,7 @@ struct WqArgs {  // the launch arguments the work queue reads (by value: no loca
   int64_t chunk_elems, tile_elems, ntiles;
   uint64_t epoch;
   int ntbs, tma_ops;
+  int64_t tma_min;
 };
 
 template <class R>
@@ -837,7 +849,7 @@ __device__ GC3_WQ_ATTR void interp_wq(const WqArgs a, char* const* s_bufs, Tma& 
       const char* in = in_p ? rpeer[op.in_buf] + op.in_off * chunk_bytes + t0_bytes : nullptr;
       char* out = out_d ? peer[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes : nullptr;
       transfer<R>(op, in_d, src, dst, srcr, dstr, in, chunk_bytes, out, chunk_bytes, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw,
-                  bar_id);
+                  bar_id, a.tma_min);
       if (!unit_and(true, uw, bar_id, n)) return;
       if (t == 0 && (op.has_dep || (op.direct & kPubSem))) {
         fence_acq_rel(false);
@@ -871,18 +883,6 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   __shared__ uint32_t s_seq[kThreads / 32];
   Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0};
   const uint64_t pol_last = l2_evict_last_policy();
-  if (!LL && a.wq) {
-    if (t == 0) s_seq[uib] = 0;
-    if (t == 0 && a.tma_stages > 0) {
-      for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    unit_sync(uw, bar_id, n);
-    const WqArgs w{a.tbs, a.ops, a.deps, a.wq_next, a.prog, a.abort_flag, a.err_info, a.timeout_ns,
-                   a.chunk_elems, a.tile_elems, a.ntiles, a.epoch, a.ntbs, a.tma_ops};
-    interp_wq<R>(w, s_bufs, tma, pol_last, t, n, uw, uib, bar_id);
-    return;
-  }
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
     for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
@@ -1014,7 +1014,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
                       static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);
       } else {
         transfer<R>(op, in_d, src, dst, srcr, dstr, in, in_stride, out, out_stride, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw,
-                    bar_id);
+                    bar_id, a.tma_min);
       }
       if (t == 0) stamp(q, 2);
       if (!unit_and(ok, uw, bar_id, n)) return;
@@ -1050,6 +1050,36 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
     if (has_in) *cin->mine = rcvd;
     if (has_out) *cout->mine = sent;
   }
+}
+
+// Work-queue entry point (copy-only programs; see interp_wq). A separate kernel, so the static-lane
+// interpreter's register allocation is unaffected.
+template <class R>
+__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(const LaunchArgs a) {
+  __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
+#pragma unroll
+  for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
+    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  __syncthreads();
+  const int uw = a.unit_warps;
+  const int n = uw * 32;
+  const int uib = threadIdx.x / n;
+  const int t = threadIdx.x - uib * n;
+  const int bar_id = 1 + uib;
+  extern __shared__ __align__(128) char s_stage[];
+  __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
+  __shared__ uint32_t s_seq[kThreads / 32];
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0};
+  const uint64_t pol_last = l2_evict_last_policy();
+  if (t == 0) s_seq[uib] = 0;
+  if (t == 0 && a.tma_stages > 0) {
+    for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unit_sync(uw, bar_id, n);
+  const WqArgs w{a.tbs, a.ops, a.deps, a.wq_next, a.prog, a.abort_flag, a.err_info, a.timeout_ns,
+                 a.chunk_elems, a.tile_elems, a.ntiles, a.epoch, a.ntbs, a.tma_ops, a.tma_min};
+  interp_wq<R>(w, s_bufs, tma, pol_last, t, n, uw, uib, bar_id);
 }
 
 }  // namespace dev

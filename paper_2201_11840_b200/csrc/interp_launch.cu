@@ -12,12 +12,15 @@ namespace gc3 {
 
 using KernelFn = void (*)(LaunchArgs);
 KernelFn interp_kernel_copy(bool ll);
+KernelFn interp_kernel_copy_wq();
 KernelFn interp_kernel_sum(int dtype, bool ll);
 KernelFn interp_kernel_prod(int dtype, bool ll);
 KernelFn interp_kernel_max(int dtype, bool ll);
 KernelFn interp_kernel_min(int dtype, bool ll);
 
 constexpr int kMaxDynamicSmem = 200 << 10;  // TMA staging budget per block
+
+KernelFn interp_kernel_wq(int redop) { return redop == -1 ? interp_kernel_copy_wq() : nullptr; }
 
 // dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs.
 KernelFn interp_kernel(int dtype, int redop, bool ll) {

@@ -45,6 +45,7 @@ namespace gc3 {
 
 using KernelFn = void (*)(LaunchArgs);
 KernelFn interp_kernel(int dtype, int redop, bool ll);
+KernelFn interp_kernel_wq(int redop);  // work-queue kernel (copy-only programs), nullptr otherwise
 cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, size_t smem, cudaStream_t stream);
 int interp_blocks_per_sm(KernelFn fn, size_t smem);
 constexpr int kStageBytesHost = 16 << 10;  // interp.cuh kStageBytes
@@ -105,7 +106,8 @@ struct Config {
   int taper = 0;                     // quarter tiles in the first and last round of every lane (measured: no gain)
   int l2hint = 1;                    // evict_last stores for data the receiver reads soon
   int wq = 1;                        // work-queue mode where possible (interp_wq)
-  int wq_items = 6;                  // work items per unit targeted by the work-queue tile size
+  int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
+  int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
@@ -129,6 +131,7 @@ Config config_from_env() {
   c.taper = static_cast<int>(env_int("GC3_TAPER", c.taper));
   c.l2hint = static_cast<int>(env_int("GC3_L2HINT", c.l2hint));
   c.wq = static_cast<int>(env_int("GC3_WQ", c.wq));
+  c.tma_min = env_int("GC3_TMA_MIN", c.tma_min);
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
@@ -1417,9 +1420,11 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   const bool wq_ok = ds.plans.size() > static_cast<size_t>(id) && ds.plans[id].wq_ok;
   // (chains of receive-and-forward ops run better on static lanes: measured on ring AllGather /
   // ReduceScatter; phase-structured programs such as the two-step AllToAll gain: C2 0.31 -> 0.29 ms)
-  if (c->cfg.wq && wq_ok && (!ir.has_chain || c->cfg.wq > 1) && !cp.ll && !sys_scope && c->cfg.lanes <= 0 &&
-      capacity >= ntbs_local && chunk_bytes > 0) {
+  KernelFn wq_fn = interp_kernel_wq(cp.redop);
+  if (c->cfg.wq && wq_ok && wq_fn && (!ir.has_chain || c->cfg.wq > 1) && !cp.ll && !sys_scope && c->cfg.lanes <= 0 &&
+      capacity >= ntbs_local && chunk_bytes > 0 && interp_blocks_per_sm(wq_fn, cp.smem) >= bps) {
     cp.wq = true;
+    cp.fn = wq_fn;
     cp.uniform = true;
     const int units = capacity;
     int64_t tb_bytes = c->cfg.tile_bytes > 0 ? c->cfg.tile_bytes / 16 * 16
@@ -1504,6 +1509,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.tma_stages = cp.tma_stages;
   a.stage_bytes = cp.stage_bytes;
   a.tma_ops = c0->cfg.tma;
+  a.tma_min = c0->cfg.tma_min;
   a.discard = c0->cfg.discard;
   // LL: every message travels as flagged lines through the receiver's FIFO (lowest latency, no
   // fences); Simple: direct and pulled messages where the plan found them safe
@@ -2049,6 +2055,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "taper") c.taper = static_cast<int>(value);
   else if (k == "l2hint") c.l2hint = static_cast<int>(value);
   else if (k == "wq") c.wq = static_cast<int>(value);
+  else if (k == "tma_min") c.tma_min = value;
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);

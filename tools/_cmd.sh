@@ -1,3 +1,4 @@
-o=gpurun_out/r01w; mkdir -p $o
-timeout 900 python -m pytest tests -m gpu -x -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
-bash tools/ab.sh "wqnoinl:-DGC3_WQ_NOINLINE=1;wqinl:-DGC3_WQ_NOINLINE=0" "c2 c3 c4 c5rs c5ag c1" > $o/ab.txt 2>&1
+o=gpurun_out/r01aa; mkdir -p $o
+bash tools/envsweep.sh "c1 c5ag c5rs c4" "GC3_TMA_MIN=0;GC3_TMA_MIN=16384;GC3_TMA_MIN=32768;GC3_TMA_MIN=65536" > $o/env.txt 2>&1
+timeout 600 python bench.py --config c4 --sweep --sweep-min 1024 --sweep-max 16777216 --sweep-protos simple --steps 20 > $o/sweep.jsonl 2>&1
+GC3_TMA_MIN=0 timeout 600 python bench.py --config c4 --sweep --sweep-min 1024 --sweep-max 16777216 --sweep-protos simple --steps 20 > $o/sweep0.jsonl 2>&1
