@@ -114,6 +114,8 @@ struct LaunchArgs {
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
   int64_t tma_min;      // bytes below which an op takes the register path
+  int32_t l2hint;       // bit 0: evict_last stores of hot data (DevOp::hot), bit 1: evict_first bulk loads
+  int32_t pad4_;
   int32_t uniform;      // 1: every thread block runs `lanes` lanes (LL launches: FIFOs need matched lanes)
   int32_t wq;           // 1: work-queue mode (see interp.cuh interp_wq)
   int32_t* wq_next;     // work-queue claim counter (zeroed before the launch)

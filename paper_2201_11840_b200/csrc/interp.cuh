@@ -345,10 +345,23 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+__device__ __forceinline__ void bulk_load_plain(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_addr(smem)),
                "l"(gmem), "r"(bytes), "r"(smem_addr(bar))
                : "memory");
+}
+// every span this runtime bulk-loads is read once (inputs, pulled spans, forwarded spans, FIFO slots):
+// with a policy (L2 evict_first) the lines make room for data still to be read
+__device__ __forceinline__ void bulk_load_hint(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+  if (pol) bulk_load_hint(smem, gmem, bytes, bar, pol);
+  else bulk_load_plain(smem, gmem, bytes, bar);
 }
 __device__ __forceinline__ void bulk_store(void* gmem, const void* smem, uint32_t bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
@@ -357,6 +370,11 @@ __device__ __forceinline__ void bulk_store_hint(void* gmem, const void* smem, ui
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem), "r"(smem_addr(smem)),
                "r"(bytes), "l"(pol)
                : "memory");
+}
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
   uint64_t pol;
@@ -387,7 +405,8 @@ struct Tma {
   int stages;
   uint32_t* seq;  // (shared) pieces issued so far: stage = seq % stages, parity = (seq / stages) & 1;
                   // written by thread 0 at the end of an op, read by the unit's threads in a later one
-  uint64_t pol;   // L2 policy for the stores of the current op (0: none)
+  uint64_t pol;     // L2 policy for the stores of the current op (0: none)
+  uint64_t pol_rd;  // L2 policy for the bulk loads (0: none)
 };
 
 // Copies `count` segments of `nbytes` (segment j: a + j*sa -> o0 + j*s0 [, o1 + j*s1]).
@@ -416,7 +435,7 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     const uint32_t g = base + static_cast<uint32_t>(p);
     uint64_t* bar = m.bar + g % m.stages;
     mbar_expect_tx(bar, bytes);
-    bulk_load(m.stage + static_cast<size_t>(g % m.stages) * SB, src, bytes, bar);
+    bulk_load(m.stage + static_cast<size_t>(g % m.stages) * SB, src, bytes, bar, m.pol_rd);
   }
   for (int64_t p = 0; p < total; ++p) {
     const char* src;
@@ -447,7 +466,7 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
       piece(np, nsrc, n0, n1, nbytes_p);
       uint64_t* bar = m.bar + rg % m.stages;
       mbar_expect_tx(bar, nbytes_p);
-      bulk_load(m.stage + static_cast<size_t>(rg % m.stages) * SB, nsrc, nbytes_p, bar);
+      bulk_load(m.stage + static_cast<size_t>(rg % m.stages) * SB, nsrc, nbytes_p, bar, m.pol_rd);
     }
   }
   bulk_wait_all();
@@ -483,8 +502,8 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
     char* st = m.stage + static_cast<size_t>(g % m.stages) * SB;
     uint64_t* bar = m.bar + g % m.stages;
     mbar_expect_tx(bar, RED ? 2 * bytes : bytes);
-    bulk_load(st, a + j * sa + off, bytes, bar);
-    if (RED) bulk_load(st + P, b + j * sb + off, bytes, bar);
+    bulk_load(st, a + j * sa + off, bytes, bar, m.pol_rd);
+    if (RED) bulk_load(st + P, b + j * sb + off, bytes, bar, m.pol_rd);
   };
   if (t == 0) {
     fence_proxy_async_global();  // generic-proxy acquires (deps, flags) -> async-proxy reads
@@ -881,7 +900,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   extern __shared__ __align__(128) char s_stage[];
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
   __shared__ uint32_t s_seq[kThreads / 32];
-  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0};
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0,
+          (a.l2hint & 2) ? l2_evict_first_policy() : 0};
   const uint64_t pol_last = l2_evict_last_policy();
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
@@ -1069,7 +1089,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(cons
   extern __shared__ __align__(128) char s_stage[];
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
   __shared__ uint32_t s_seq[kThreads / 32];
-  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0};
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0,
+          (a.l2hint & 2) ? l2_evict_first_policy() : 0};
   const uint64_t pol_last = l2_evict_last_policy();
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {

@@ -104,7 +104,8 @@ struct Config {
   int balance = 1;                   // per-component lane multipliers (lane_multipliers; 2: rounded up)
   int mult_cap = 4;                  // largest lane multiplier
   int taper = 0;                     // quarter tiles in the first and last round of every lane (measured: no gain)
-  int l2hint = 1;                    // evict_last stores for data the receiver reads soon
+  int l2hint = 3;                    // bit 0: evict_last stores for data the receiver reads soon; bit 1:
+                                     // evict_first bulk loads (every span is read once)
   int wq = 1;                        // work-queue mode where possible (interp_wq)
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
   int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
@@ -975,7 +976,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
             o.in_buf = kSource;
         }
         if (pub_sem.count({r, static_cast<int>(t), static_cast<int>(s)})) o.direct |= kPubSem;
-        if (c0->cfg.l2hint && op_sends(op.op)) {  // its receiver reads what it writes: keep it in L2
+        if ((c0->cfg.l2hint & 1) && op_sends(op.op)) {  // its receiver reads what it writes: keep it in L2
           const auto rcv = receiver_of.find({r, static_cast<int>(t), static_cast<int>(s)});
           if (!(o.direct & kOutDirect)) {
             o.hot = 1;  // FIFO slot or pulled span: read by the receive
@@ -1510,6 +1511,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.stage_bytes = cp.stage_bytes;
   a.tma_ops = c0->cfg.tma;
   a.tma_min = c0->cfg.tma_min;
+  a.l2hint = c0->cfg.l2hint;
   a.discard = c0->cfg.discard;
   // LL: every message travels as flagged lines through the receiver's FIFO (lowest latency, no
   // fences); Simple: direct and pulled messages where the plan found them safe
