@@ -109,7 +109,19 @@ def main():
             s["publish"] += p
             data += d
         busy.append(data / max((last - first) / 1e3, 1e-9))
-    out = {"config": args.config, "plan": plan, "span_us": span, "blocks": int(tr.shape[0]),
+    # per thread block: when its units finish (median / max)
+    per_tb = []
+    if blocks is not None:
+        groups = {}
+        for i, (rank, tb) in enumerate(blocks):
+            groups.setdefault((rank, tb["id"]), []).extend(range(i * lanes, (i + 1) * lanes))
+        for (rank, tid), units in groups.items():
+            ends = [(tr[b, :int((tr[b, :, 3] > 0).sum()), 3].max() - t0) / 1e3 for b in units
+                    if b < tr.shape[0] and (tr[b, :, 3] > 0).any()]
+            if ends:
+                per_tb.append({"rank": rank, "tb": tid, "units": len(units), "end_med_us": float(np.median(ends)),
+                               "end_max_us": float(max(ends))})
+    out = {"config": args.config, "plan": plan, "span_us": span, "blocks": int(tr.shape[0]), "per_tb": per_tb,
            "mean_block_data_fraction": float(np.mean(busy)) if busy else None,
            "per_opcode_us": {k: {"n": v["n"], "wait": v["wait"] / v["n"], "data": v["data"] / v["n"],
                                  "publish": v["publish"] / v["n"]} for k, v in stats.items()}}
