@@ -184,6 +184,9 @@ ncclResult_t gc3BootstrapExchange(const ncclUniqueId* id, int rank, int nranks, 
  * buffer, 2: reduce's dst read does); *complete = 1 when every first read of `input` is covered, so
  * in-place IRs need no pre-copy of sendbuff (SURVEY.md §7 hard part 6). */
 ncclResult_t gc3IrSourceReads(gc3Ir_t ir, int* complete, char** json);
+/* [rank][tb][step] flags (1: the op's final write of the rank's owned ReduceScatter block goes
+ * straight to recvbuff); *complete = 1 when they cover every owned block (no copy-out). */
+ncclResult_t gc3IrResultWrites(gc3Ir_t ir, int* complete, char** json);
 /* per [rank][thread block] lane multipliers of the work balance (JSON); with balance on, thread block
  * i of a launch runs lanes x mult lanes (units in launch order). */
 ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);

@@ -26,8 +26,9 @@ enum : uint8_t { kInDirect = 1, kOutDirect = 2, kInPull = 4, kOutPull = 8,
                  kPubSem = 64,      // publish this op's semaphore (a receive waits on it)
                  kNoCtrOut = 128 }; // the send connection carries no FIFO message
 enum : uint8_t { kSrcFromSource = 1, kDstFromSource = 2 };
-constexpr int kBufs = 4;      // per rank: input, output, scratch, source (see LaunchArgs::bufs)
+constexpr int kBufs = 5;      // per rank: input, output, scratch, source, result (see LaunchArgs::bufs)
 constexpr int kSource = 3;
+constexpr int kResult = 4;
 
 struct DevOp {  // 32 bytes
   uint8_t opcode;
@@ -120,7 +121,9 @@ struct LaunchArgs {
   int32_t wq;           // 1: work-queue mode (see interp.cuh interp_wq)
   int32_t* wq_next;     // work-queue claim counter (zeroed before the launch)
   uint64_t* prog;       // work-queue progress: [thread block][tile] = (epoch << 32) | steps done
-  char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source (the caller's
+  char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source, result (the
+                                     // caller's recvbuff shifted so that an owned ReduceScatter chunk
+                                     // keeps its input offset; see result_writes), source (the caller's
                                      // const data the in-place IR's first reads see; = input when
                                      // the working buffer was pre-copied)
 };

@@ -275,6 +275,7 @@ struct DevicePlan {  // one registered IR on one device
   bool built = false;
   bool wq_ok = false;  // work-queue mode possible (no FIFO message, one launch)
   bool source_complete = false;  // every first read of `input` reads the source buffer (source_reads)
+  bool result_complete = false;  // ReduceScatter owned blocks are written straight to recvbuff (result_writes)
   std::vector<int> ranks;  // local ranks in launch order (rank_slot -> rank)
   int ntbs = 0;
   int weight = 0;          // sum of lane multipliers: units = lanes x weight
@@ -760,6 +761,81 @@ std::vector<std::vector<std::vector<uint8_t>>> source_reads(const Program& p, bo
   return flags;
 }
 
+// Final writes of a ReduceScatter's owned block straight into recvbuff. The IR is in place over
+// R x c chunks and rank r owns [r*c, (r+1)*c) (core.hpp:351-375); the runtime used to copy the owned
+// block out of its working buffer after the kernel. A local op (recv / copy / reduce / rrc) that
+// writes part of the owned block may write it into the result buffer instead when every other
+// write of that span happens before it and every read of it happens before it too (no one reads
+// the final value from the working buffer). Returns flags[rank][tb][step] (1 = write to the result
+// buffer); `complete` = on every rank such writes cover the whole owned block (the copy is dropped).
+std::vector<std::vector<std::vector<uint8_t>>> result_writes(const Program& p, bool& complete) {
+  const int R = p.ranks();
+  std::vector<std::vector<std::vector<uint8_t>>> flags(R);
+  for (int r = 0; r < R; ++r) {
+    flags[r].resize(p.gpus[r].tbs.size());
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) flags[r][t].assign(p.gpus[r].tbs[t].ops.size(), 0);
+  }
+  complete = false;
+  if (!p.inplace || R < 2 || p.collective != "reducescatter" || p.nchunks[0] % R) return flags;
+  const int c = p.nchunks[0] / R;
+  const HbGraph g(p);
+  if (!g.ok) return flags;
+  auto is_input = [&](Buf b) { return b == Buf::input || b == Buf::output; };
+  struct Acc {
+    int node, off, cnt;
+    bool write;
+  };
+  complete = true;
+  for (int r = 0; r < R; ++r) {
+    std::vector<Acc> acc;  // every local access of `input` on this rank
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t)
+      for (size_t s = 0; s < p.gpus[r].tbs[t].ops.size(); ++s) {
+        const Op& op = p.gpus[r].tbs[t].ops[s];
+        const int u = g.node(r, static_cast<int>(t), static_cast<int>(s));
+        switch (op.op) {
+          case Opcode::send: case Opcode::rrs:
+            if (is_input(op.src_buf)) acc.push_back({u, op.src_off, op.count, false});
+            break;
+          case Opcode::recv:
+            if (is_input(op.dst_buf)) acc.push_back({u, op.dst_off, op.count, true});
+            break;
+          case Opcode::copy: case Opcode::reduce: case Opcode::rrc:
+            if (is_input(op.src_buf)) acc.push_back({u, op.src_off, op.count, false});
+            if (is_input(op.dst_buf)) acc.push_back({u, op.dst_off, op.count, true});
+            if (op.op == Opcode::reduce && is_input(op.dst_buf)) acc.push_back({u, op.dst_off, op.count, false});
+            break;
+          case Opcode::rcs: case Opcode::rrcs:
+            if (is_input(op.src_buf)) {
+              acc.push_back({u, op.src_off, op.count, true});
+              acc.push_back({u, op.src_off, op.count, false});  // forwards (or is pulled from) its span
+            }
+            break;
+          default: break;
+        }
+      }
+    std::vector<bool> covered(c, false);
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t)
+      for (size_t s = 0; s < p.gpus[r].tbs[t].ops.size(); ++s) {
+        const Op& op = p.gpus[r].tbs[t].ops[s];
+        const bool local_writer = op.op == Opcode::recv || op.op == Opcode::copy || op.op == Opcode::reduce || op.op == Opcode::rrc;
+        if (!local_writer || !is_input(op.dst_buf)) continue;
+        if (op.dst_off < r * c || op.dst_off + op.count > (r + 1) * c) continue;  // not inside the owned block
+        const int u = g.node(r, static_cast<int>(t), static_cast<int>(s));
+        bool final_write = true;
+        for (const Acc& a : acc) {
+          if (a.node == u || !(a.off < op.dst_off + op.count && op.dst_off < a.off + a.cnt)) continue;
+          if (!g.reaches(a.node, u)) final_write = false;  // another access is not before this write
+        }
+        if (final_write) {
+          flags[r][t][s] = 1;
+          for (int k = op.dst_off; k < op.dst_off + op.count; ++k) covered[k - r * c] = true;
+        }
+      }
+    for (bool b : covered) complete = complete && b;
+  }
+  return flags;
+}
+
 // Work balance. Thread blocks joined by FIFO connections must run the same number of lanes (lane
 // l of a sender talks to lane l of its receiver), but separate components need not: a component
 // whose thread blocks move more bytes per tile (e.g. the coalesced count-G exchange of the two-step
@@ -858,6 +934,9 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   bool source_complete = false;
   const auto source = c0->cfg.source ? source_reads(p, source_complete) : std::vector<std::vector<std::vector<uint8_t>>>();
   plan.source_complete = c0->cfg.source && source_complete;
+  bool result_complete = false;
+  const auto result = c0->cfg.source ? result_writes(p, result_complete) : std::vector<std::vector<std::vector<uint8_t>>>();
+  plan.result_complete = c0->cfg.source && result_complete;
   auto direct = c0->cfg.direct ? direct_messages(p, (c0->cfg.direct & 2) != 0, &pull_src)
                                : std::vector<std::vector<std::vector<uint8_t>>>();
   if (!(c0->cfg.direct & 1))  // pulls only: drop the direct flags
@@ -995,6 +1074,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         o.dst_buf = static_cast<uint8_t>(op.dst_buf);
         o.src_rbuf = plan.source_complete && (source[r][t][s] & kSrcFromSource) ? kSource : o.src_buf;
         o.dst_rbuf = plan.source_complete && (source[r][t][s] & kDstFromSource) ? kSource : o.dst_buf;
+        if (plan.result_complete && result[r][t][s]) o.dst_buf = kResult;  // final owned write -> recvbuff
         o.has_dep = op.has_dep ? 1 : 0;
         o.src_off = op.src_off;
         o.dst_off = op.dst_off;
@@ -1583,6 +1663,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     char* send = const_cast<char*>(static_cast<const char*>(q->send));
     char* recv = static_cast<char*>(q->recv);
     char* source = nullptr;  // what the in-place IR's first reads see (source_reads); null: `in`
+    char* result = nullptr;  // ReduceScatter: recvbuff shifted to the owned block's offset (result_writes)
     switch (p0.coll) {
       case kAllReduce:  // in-place IR on `input` (core.hpp:305-327)
         if (ragged) {
@@ -1617,7 +1698,9 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
         else if (!ragged) CUDA_TRY(cudaMemcpyAsync(c->work, send, blk * R, cudaMemcpyDeviceToDevice, stream));
         else CUDA_TRY(cudaMemcpy2DAsync(c->work, pblk, send, blk, blk, R, cudaMemcpyDeviceToDevice, stream));
         in = out = c->work;
-        post.push_back({recv, blk, c->work + static_cast<size_t>(c->rank) * pblk, pblk, blk, 1});
+        // the owned block's final writes land in recvbuff: its chunk k sits at recvbuff + (k - r*c)*ce
+        if (!ragged && plan.result_complete) result = recv - static_cast<ptrdiff_t>(c->rank) * static_cast<ptrdiff_t>(pblk);
+        else post.push_back({recv, blk, c->work + static_cast<size_t>(c->rank) * pblk, pblk, blk, 1});
         break;
       case kAllToAll:
         if (q->send == q->recv) return set_error(ncclInvalidArgument, "in-place AllToAll is not supported");
@@ -1639,6 +1722,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][1] = out;
     a.bufs[slot][2] = c->scratch;
     a.bufs[slot][kSource] = source ? source : in;
+    a.bufs[slot][kResult] = result ? result : in;
   }
   if (cp.wq) {  // claim counter reset + progress table (epoch-tagged, never reset)
     DeviceGuard gw(dev);
@@ -2264,6 +2348,24 @@ ncclResult_t gc3IrSourceReads(gc3Ir_t ir, int* complete, char** json) {
   if (!ir || !json || !complete) return ncclInvalidArgument;
   bool c = false;
   const auto f = source_reads(ir->p, c);
+  *complete = c ? 1 : 0;
+  std::string o = "[";
+  for (size_t r = 0; r < f.size(); ++r) {
+    o += r ? ",[" : "[";
+    for (size_t t = 0; t < f[r].size(); ++t) {
+      o += t ? ",[" : "[";
+      for (size_t k = 0; k < f[r][t].size(); ++k) o += (k ? "," : "") + std::to_string(f[r][t][k]);
+      o += "]";
+    }
+    o += "]";
+  }
+  *json = dup_cstr(o + "]");
+  return ncclSuccess;
+}
+ncclResult_t gc3IrResultWrites(gc3Ir_t ir, int* complete, char** json) {
+  if (!ir || !json || !complete) return ncclInvalidArgument;
+  bool c = false;
+  const auto f = result_writes(ir->p, c);
   *complete = c ? 1 : 0;
   std::string o = "[";
   for (size_t r = 0; r < f.size(); ++r) {

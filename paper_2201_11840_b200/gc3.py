@@ -90,6 +90,7 @@ def lib():
         "gc3IrToXml": [vp, ctypes.POINTER(vp)],
         "gc3IrLaneMultipliers": [vp, ctypes.POINTER(vp)],
         "gc3IrSourceReads": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
+        "gc3IrResultWrites": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -199,6 +200,13 @@ class IR:
         import json
         out, comp = ctypes.c_void_p(), ctypes.c_int()
         check(lib().gc3IrSourceReads(self._h, ctypes.byref(comp), ctypes.byref(out)))
+        return bool(comp.value), json.loads(_take(out.value))
+
+    def result_writes(self):
+        """(complete, flags[rank][tb][step]) of the ReduceScatter result-buffer analysis."""
+        import json
+        out, comp = ctypes.c_void_p(), ctypes.c_int()
+        check(lib().gc3IrResultWrites(self._h, ctypes.byref(comp), ctypes.byref(out)))
         return bool(comp.value), json.loads(_take(out.value))
 
     def lane_multipliers(self):

@@ -28,7 +28,7 @@ SENDS = {"send", "rcs", "rrcs", "rrs"}
 RECVS = {"recv", "rrc", "rcs", "rrcs", "rrs"}
 
 
-def run(irj, flags, seed, use_flags=True, source=None):
+def run(irj, flags, seed, use_flags=True, source=None, result=None):
     """source: flags of the const-source analysis; the working input then starts as garbage and
     flagged reads see the caller's (initial) data instead."""
     R = len(irj["gpus"])
@@ -42,6 +42,7 @@ def run(irj, flags, seed, use_flags=True, source=None):
             inp[:] = 77777  # the working buffer is not initialised
         out = inp if irj["inplace"] else np.zeros(max(nout, 1), np.int64)
         bufs.append([inp, out, np.zeros(max(nsc, 1), np.int64)])
+    res = [np.full(max(nin, 1), 55555, np.int64) for _ in range(R)]  # the result buffers (recvbuff)
 
     def span(r, b, off, cnt):
         return bufs[r][BUFS[b]][off:off + cnt]
@@ -81,6 +82,8 @@ def run(irj, flags, seed, use_flags=True, source=None):
         oc, cnt = op["opcode"], op["count"]
         src = span(r, op["src_buf"], op["src_off"], cnt)
         dst = span(r, op["dst_buf"], op["dst_off"], cnt)
+        if result is not None and result[r][t][s]:  # final owned write: straight to recvbuff
+            dst = res[r][op["dst_off"]:op["dst_off"] + cnt]
         srcr = rspan(r, op["src_buf"], op["src_off"], cnt, t, s, 1)
         dstr = rspan(r, op["dst_buf"], op["dst_off"], cnt, t, s, 2)
         msg = None
@@ -127,6 +130,8 @@ def run(irj, flags, seed, use_flags=True, source=None):
                 fifo.setdefault(key, []).append(out)
         pc[(r, t)] += 1
     assert all(pc[(r, t)] == len(tb["ops"]) for r, t, tb in tbs), "deadlock"
+    if result is not None:
+        return [x.copy() for x in res]
     return [b[1].copy() for b in bufs]
 
 
@@ -223,3 +228,25 @@ def test_const_source_reads_need_no_precopy(name):
             if irj["collective"] == "reducescatter":  # only the owned block is the result
                 a, b = a[r * c:(r + 1) * c], b[r * c:(r + 1) * c]
             assert np.array_equal(a, b), f"seed {seed} rank {r}"
+
+
+@pytest.mark.parametrize("name", ["ring_rs_8", "ring_rs_4@2", "ring_rs_2"])
+def test_reducescatter_final_writes_to_recvbuff(name):
+    """ReduceScatter owned blocks written straight into recvbuff (runtime.cpp result_writes) with an
+    uninitialised working buffer and the chosen transports: every interleaving leaves the reduced
+    owned block in the result buffer."""
+    spec, _, k = name.partition("@")
+    ir = gc3.IR(read_ir(spec))
+    if k:
+        ir = ir.replicate(int(k))
+    irj, flags = json.loads(ir.serialize()), ir.direct_messages()
+    complete, source = ir.source_reads()
+    rcomplete, result = ir.result_writes()
+    assert complete and rcomplete
+    ref = run(irj, flags, 0, use_flags=False)
+    R = len(irj["gpus"])
+    c = irj["nchunks"]["input"] // R
+    for seed in range(30):
+        got = run(irj, flags, seed, source=source, result=result)
+        for r in range(R):
+            assert np.array_equal(ref[r][r * c:(r + 1) * c], got[r][r * c:(r + 1) * c]), f"seed {seed} rank {r}"

@@ -1,2 +1,3 @@
-o=gpurun_out/r01ab; mkdir -p $o
-bash tools/envsweep.sh "c2 c2d c5ag c5rs c3 c4" "GC3_L2HINT=3;GC3_L2HINT=1" > $o/env.txt 2>&1
+o=gpurun_out/r01ad; mkdir -p $o
+timeout 900 python -m pytest tests -m gpu -x -q > $o/pytest_gpu.log 2>&1; echo "rc=$?" >> $o/pytest_gpu.log
+for c in c2 c3 c4 c5rs c5ag c1 c2d; do timeout 120 python bench.py --config $c --quick --steps 20 >> $o/quick.jsonl 2>&1; done
