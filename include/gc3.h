@@ -134,9 +134,14 @@ typedef struct {
 /* collective: 0 allreduce, 1 allgather, 2 reducescatter, 3 alltoall; count as in the NCCL call. */
 ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDataType_t datatype, gc3PlanInfo* info);
 
-/* Runtime knobs (defaults from GC3_SLOTS, GC3_SLOT_BYTES, GC3_MAX_LANES, GC3_LANES,
- * GC3_TILE_BYTES, GC3_TIMEOUT_MS). key: "slots", "slot_bytes", "max_lanes" (apply to IRs registered
- * afterwards), "lanes", "tile_bytes", "timeout_ms" (apply to the next launch; 0 = automatic). */
+/* Runtime knobs; defaults from the GC3_<KEY> environment variables (upper case). Registration-time
+ * keys (apply to IRs registered afterwards): "slots", "slot_bytes", "max_lanes", "direct" (bit 0
+ * direct messages, bit 1 pulled messages), "source" (const-source reads and result writes),
+ * "balance" (lane multipliers; 2 = rounded up), "mult_cap", "l2hint" (bit 0 evict_last stores, bit 1
+ * evict_first loads). Launch-time keys: "lanes", "tile_bytes", "timeout_ms", "unit_warps", "group"
+ * (0 = automatic), "tma" (bit 0 bulk copies, bit 1 staged reductions, bit 2 register-store copies),
+ * "tma_min", "discard", "wq" (work-queue mode; 2 = also for chain programs), "wq_items", "taper",
+ * "ll_max_bytes" (Simple IRs run LL up to this many bytes per rank), "trace". */
 ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value);
 
 /* In-kernel event log of the last launch on comm's device when config "trace" (GC3_TRACE) is set

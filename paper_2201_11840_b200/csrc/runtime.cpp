@@ -108,6 +108,7 @@ struct Config {
                                      // evict_first bulk loads (every span is read once)
   int wq = 1;                        // work-queue mode where possible (interp_wq)
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
+  int64_t ll_max_bytes = 0;          // Simple IRs run LL up to this many bytes per rank (0: never)
   int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
@@ -133,6 +134,7 @@ Config config_from_env() {
   c.l2hint = static_cast<int>(env_int("GC3_L2HINT", c.l2hint));
   c.wq = static_cast<int>(env_int("GC3_WQ", c.wq));
   c.tma_min = env_int("GC3_TMA_MIN", c.tma_min);
+  c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
@@ -1364,7 +1366,12 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.kesize = ir.has_reduce ? static_cast<int>(esize) : 1;
   const int64_t chunk_bytes = ce * static_cast<int64_t>(esize);
   cp.chunk_elems = chunk_bytes / cp.kesize;
-  const int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
+  // protocol: the override, else the IR's tag; a Simple IR runs LL for messages up to ll_max_bytes
+  // per rank (no fences on the data path: measured ~2x lower latency below ~1 MiB)
+  int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
+  if (ir.proto_override < 0 && proto == 0 && c->cfg.ll_max_bytes > 0 &&
+      selection_bytes(coll, count, esize, c->nranks) <= static_cast<uint64_t>(c->cfg.ll_max_bytes))
+    proto = 1;
   cp.ll = proto == 1 && chunk_bytes % 8 == 0;
   // an LL launch sends every message through lane-matched FIFOs: with per-connection lane counts
   // (lane_mask) it runs every thread block on the base lanes instead
@@ -2142,6 +2149,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "l2hint") c.l2hint = static_cast<int>(value);
   else if (k == "wq") c.wq = static_cast<int>(value);
   else if (k == "tma_min") c.tma_min = value;
+  else if (k == "ll_max_bytes") c.ll_max_bytes = value;
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
