@@ -195,6 +195,9 @@ ncclResult_t gc3IrResultWrites(gc3Ir_t ir, int* complete, char** json);
 /* per [rank][thread block] lane multipliers of the work balance (JSON); with balance on, thread block
  * i of a launch runs lanes x mult lanes (units in launch order). */
 ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);
+/* The built-in program the runtime uses for `collective` ("allreduce", "allgather", "reducescatter",
+ * "alltoall") on nranks ranks when no registered IR matches a call (see gc3RegisterIR). */
+ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir);
 ncclResult_t gc3IrFree(gc3Ir_t ir);
 void gc3Free(void* p);
 

@@ -502,4 +502,90 @@ Program replicate_instances(const Program& p, int k) {
   return q;
 }
 
+bool builtin_program(const std::string& collective, int R, Program& out) {
+  if (R < 2) return false;
+  auto mod = [R](int x) { return ((x % R) + R) % R; };
+  Program p;
+  p.collective = collective;
+  p.proto = Proto::simple;
+  auto op = [](int step, Opcode o, Buf sb, int so, Buf db, int dof) {
+    Op x;
+    x.step = step;
+    x.op = o;
+    x.src_buf = sb;
+    x.src_off = so;
+    x.dst_buf = db;
+    x.dst_off = dof;
+    x.count = 1;
+    return x;
+  };
+  for (int r = 0; r < R; ++r) {
+    Gpu g;
+    g.rank = r;
+    if (collective == "alltoall") {  // direct: one thread block per peer, own chunk copied locally
+      int id = 0;
+      for (int q = 0; q < R; ++q) {
+        if (q == r) continue;
+        ThreadBlock tb;
+        tb.id = id;
+        tb.send_peer = tb.recv_peer = q;
+        tb.channel = 0;
+        int s = 0;
+        tb.ops.push_back(op(s++, Opcode::send, Buf::input, q, Buf::output, r));
+        if (id == 0) tb.ops.push_back(op(s++, Opcode::copy, Buf::input, r, Buf::output, r));
+        tb.ops.push_back(op(s++, Opcode::recv, Buf::input, r, Buf::output, q));
+        g.tbs.push_back(tb);
+        ++id;
+      }
+    } else {  // ring: send to r+1, receive from r-1
+      ThreadBlock tb;
+      tb.id = 0;
+      tb.send_peer = mod(r + 1);
+      tb.recv_peer = mod(r - 1);
+      tb.channel = 0;
+      int s = 0;
+      auto same = [&](Opcode o, Buf b, int c) { tb.ops.push_back(op(s++, o, b, mod(c), b, mod(c))); };
+      if (collective == "allreduce") {
+        // chunk c: sent raw by rank c+1, reduced along the ring (the rank before its owner forwards the
+        // sum without storing it: rrs), completed by rank c, then forwarded around to every rank
+        same(Opcode::send, Buf::input, r - 1);
+        if (R == 2) {
+          same(Opcode::rrcs, Buf::input, r);
+        } else {
+          for (int k = 1; k <= R - 3; ++k) same(Opcode::rrcs, Buf::input, r - 1 - k);
+          same(Opcode::rrs, Buf::input, r + 1);
+          same(Opcode::rrcs, Buf::input, r);
+          for (int k = 0; k <= R - 3; ++k) same(Opcode::rcs, Buf::input, r - 1 - k);
+        }
+        same(Opcode::recv, Buf::input, r + 1);
+      } else if (collective == "allgather") {
+        tb.ops.push_back(op(s++, Opcode::copy, Buf::input, 0, Buf::output, r));
+        same(Opcode::send, Buf::output, r);
+        for (int k = 1; k <= R - 2; ++k) same(Opcode::rcs, Buf::output, r - k);
+        same(Opcode::recv, Buf::output, r + 1);
+      } else if (collective == "reducescatter") {
+        same(Opcode::send, Buf::input, r - 1);
+        for (int k = 1; k <= R - 2; ++k) same(Opcode::rrcs, Buf::input, r - 1 - k);
+        same(Opcode::rrc, Buf::input, r);
+      } else {
+        return false;
+      }
+      g.tbs.push_back(tb);
+    }
+    p.gpus.push_back(std::move(g));
+  }
+  if (collective == "allreduce" || collective == "reducescatter") {
+    p.inplace = true;
+    p.nchunks[0] = p.nchunks[1] = R;
+  } else if (collective == "allgather") {
+    p.nchunks[0] = 1;
+    p.nchunks[1] = R;
+  } else {
+    p.nchunks[0] = p.nchunks[1] = R;
+  }
+  p.name = "builtin_" + collective + "_" + std::to_string(R);
+  out = std::move(p);
+  return true;
+}
+
 }  // namespace gc3

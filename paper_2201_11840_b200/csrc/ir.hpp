@@ -119,4 +119,12 @@ std::vector<SlotViolation> check_slots(const Program& p, int slots);
 Program replicate_instances(const Program& p, int k);
 bool uniform_counts(const Program& p);
 
+// Built-in programs the runtime uses when no registered IR matches a call (drop-in NCCL use without
+// gc3RegisterIR): ring AllReduce / AllGather / ReduceScatter on one channel and the direct AlltoAll,
+// for any rank count >= 2. They are the reference compiler's programs for these algorithms
+// (ring_allreduce / ring allgather / ring reducescatter / alltoall with one node):
+// op for op identical to its output (tests/test_builtin_irs.py). collective: "allreduce",
+// "allgather", "reducescatter" or "alltoall"; returns false for anything else.
+bool builtin_program(const std::string& collective, int nranks, Program& out);
+
 }  // namespace gc3

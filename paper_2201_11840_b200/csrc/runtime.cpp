@@ -109,6 +109,7 @@ struct Config {
   int wq = 1;                        // work-queue mode where possible (interp_wq)
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
   int64_t ll_max_bytes = 0;          // Simple IRs run LL up to this many bytes per rank (0: never)
+  int builtin = 1;                   // calls no registered IR matches run the built-in programs
   int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
@@ -135,6 +136,7 @@ Config config_from_env() {
   c.wq = static_cast<int>(env_int("GC3_WQ", c.wq));
   c.tma_min = env_int("GC3_TMA_MIN", c.tma_min);
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
+  c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
@@ -263,6 +265,7 @@ struct RankIR {
   bool has_reduce = false;
   bool has_chain = false;  // an op both receives and sends (rcs / rrcs / rrs): multi-hop chains
   uint8_t lane_mask = 0;   // transports assumed by the lane multipliers (transport_mask)
+  bool builtin = false;    // registered by the runtime (builtin_program), selected after user IRs
   int max_count = 1;
   std::vector<std::vector<int>> mult;  // lane multiplier per (rank, tb) (lane_multipliers)
   ArenaLayout lay;
@@ -1243,15 +1246,19 @@ uint64_t selection_bytes(int coll, size_t count, size_t esize, int nranks) {
   return 0;
 }
 
+// The first registered IR whose collective and size_range match (ir.hpp:112-116);
+// the runtime's built-in programs only when no user IR does.
 int select_ir(Comm* c, int coll, size_t count, int dtype) {
   const uint64_t bytes = selection_bytes(coll, count, dtype_size(dtype), c->nranks);
-  for (size_t i = 0; i < c->irs.size(); ++i) {
-    const Program& p = c->irs[i]->prog;
-    if (p.collective != coll_name(coll)) continue;
-    if (bytes < p.min_bytes || bytes > p.max_bytes) continue;
-    if (chunk_elems_for(p, coll, count, c->nranks) < 0) continue;
-    return static_cast<int>(i);
-  }
+  for (int pass = 0; pass < 2; ++pass)
+    for (size_t i = 0; i < c->irs.size(); ++i) {
+      if (c->irs[i]->builtin != (pass == 1)) continue;
+      const Program& p = c->irs[i]->prog;
+      if (p.collective != coll_name(coll)) continue;
+      if (bytes < p.min_bytes || bytes > p.max_bytes) continue;
+      if (chunk_elems_for(p, coll, count, c->nranks) < 0) continue;
+      return static_cast<int>(i);
+    }
   return -1;
 }
 
@@ -1760,9 +1767,96 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   return ncclSuccess;
 }
 
+// Validates a program against the communicator, sizes and allocates its arena and publishes it to
+// the other processes of the clique (the part of gc3RegisterIR after parsing).
+ncclResult_t register_program(Comm* comm, std::unique_ptr<RankIR> ir, int* ir_id) {
+  Topology topo;
+  topo.nodes = 1;
+  topo.gpus_per_node = comm->nranks;
+  topo.max_threadblocks = 148;
+  topo.max_channels = 1 << 20;
+  const auto issues = validate(ir->prog, topo);
+  if (!issues.empty()) return set_error(ncclInvalidUsage, "IR %s fails validation: %s", ir->prog.name.c_str(), issues[0].c_str());
+  if (ir->prog.collective != "allreduce" && ir->prog.collective != "allgather" && ir->prog.collective != "reducescatter" &&
+      ir->prog.collective != "alltoall")
+    return set_error(ncclInvalidUsage, "collective %s has no NCCL entry point", ir->prog.collective.c_str());
+  for (const auto& g : ir->prog.gpus)
+    for (const auto& tb : g.tbs)
+      for (const auto& op : tb.ops) {
+        if (op_reduces(op.op)) ir->has_reduce = true;
+        if (op_receives(op.op) && op_sends(op.op)) ir->has_chain = true;
+        if (op_sends(op.op) || op_receives(op.op)) ir->max_count = std::max(ir->max_count, op.count);
+      }
+  ir->slots = std::max(1, comm->cfg.slots);
+  ir->slot_bytes = std::max<int64_t>(comm->cfg.slot_bytes / 256 * 256, 256);
+  {  // lanes provisioned: enough for ~2 CUDA blocks per SM when one rank owns a device
+    int max_tbs = 1;
+    for (const auto& g : ir->prog.gpus) max_tbs = std::max(max_tbs, static_cast<int>(g.tbs.size()));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
+    ir->lanes = std::max(1, std::min(comm->cfg.max_lanes, (2 * sms + max_tbs - 1) / max_tbs));
+  }
+  {  // direct / pulled messages (and lanes that differ across their connections) only when every
+     // rank runs in one launch: all ranks hosted here, on one device
+    bool one_launch = true;
+    for (int r = 0; r < comm->nranks; ++r)
+      one_launch = one_launch && comm->clique->local[r] && comm->clique->local[r]->device == comm->device;
+    ir->lane_mask = one_launch ? transport_mask(comm->cfg.direct) : 0;
+  }
+  ir->mult = comm->cfg.balance ? lane_multipliers(ir->prog, comm->cfg.balance, comm->cfg.mult_cap, ir->lane_mask)
+                               : std::vector<std::vector<int>>();
+  if (ir->mult.empty())
+    for (const auto& g : ir->prog.gpus) ir->mult.emplace_back(g.tbs.size(), 1);
+  ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes, ir->mult);
+  {
+    DeviceGuard g(comm->device);
+    CUDA_TRY(cudaMalloc(&ir->arena, ir->lay.bytes));
+    CUDA_TRY(cudaMemset(ir->arena, 0, ir->lay.bytes));
+    CUDA_TRY(cudaDeviceSynchronize());
+    // publish the arena to the other processes of the clique
+    bool remote_peers = false;
+    for (int r = 0; r < comm->nranks; ++r) remote_peers = remote_peers || !comm->clique->local[r];
+    if (remote_peers) {
+      CUDA_TRY(cudaIpcGetMemHandle(&ir->handle, ir->arena));
+      const std::string rec(reinterpret_cast<const char*>(&ir->handle), sizeof(ir->handle));
+      const int id = static_cast<int>(comm->irs.size());
+      if (!post_record(shm_dir(comm->clique->key), "ir" + std::to_string(id) + ".rank" + std::to_string(comm->rank), rec))
+        return set_error(ncclSystemError, "cannot publish arena handle");
+    }
+  }
+  comm->irs.push_back(std::move(ir));
+  if (ir_id) *ir_id = static_cast<int>(comm->irs.size()) - 1;
+  return ncclSuccess;
+}
+
+// A call no registered IR matches runs the runtime's built-in program for its collective
+// (builtin_program): registered here, before any launch of the group, on every communicator this
+// process hosts in the clique, in rank order — every process meets the first such call of a
+// collective at the same point of the call sequence, so IR ids stay aligned across ranks.
+ncclResult_t register_builtins(std::vector<Pending>& pend) {
+  for (Pending& q : pend) {
+    Comm* c = q.comm;
+    if (!c->cfg.builtin || select_ir(c, q.coll, q.count, q.dtype) >= 0) continue;
+    const std::string coll = coll_name(q.coll);
+    for (int r = 0; r < c->nranks; ++r) {
+      Comm* lc = c->clique->local[r];
+      if (!lc) continue;
+      bool have = false;
+      for (const auto& ir : lc->irs) have = have || (ir->builtin && ir->prog.collective == coll);
+      if (have) continue;
+      auto ir = std::make_unique<RankIR>();
+      if (!builtin_program(coll, lc->nranks, ir->prog)) break;
+      ir->builtin = true;
+      NCCL_TRY(register_program(lc, std::move(ir), nullptr));
+    }
+  }
+  return ncclSuccess;
+}
+
 ncclResult_t flush_group() {
   std::vector<Pending> pend;
   pend.swap(g_pending);
+  NCCL_TRY(register_builtins(pend));
   std::map<std::pair<Clique*, int>, std::vector<Pending*>> by_dev;
   for (Pending& q : pend) by_dev[{q.comm->clique, q.comm->device}].push_back(&q);
   ncclResult_t rc = ncclSuccess;
@@ -2061,64 +2155,9 @@ ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instan
       return set_error(ncclInvalidUsage, "instances=%d: the runtime rewrite needs ops of one count (SURVEY.md Finding 5)", instances);
     ir->prog = replicate_instances(ir->prog, instances);
   }
-  Topology topo;
-  topo.nodes = 1;
-  topo.gpus_per_node = comm->nranks;
-  topo.max_threadblocks = 148;
-  topo.max_channels = 1 << 20;
-  const auto issues = validate(ir->prog, topo);
-  if (!issues.empty()) return set_error(ncclInvalidUsage, "IR %s fails validation: %s", ir->prog.name.c_str(), issues[0].c_str());
-  if (ir->prog.collective != "allreduce" && ir->prog.collective != "allgather" && ir->prog.collective != "reducescatter" &&
-      ir->prog.collective != "alltoall")
-    return set_error(ncclInvalidUsage, "collective %s has no NCCL entry point", ir->prog.collective.c_str());
-  for (const auto& g : ir->prog.gpus)
-    for (const auto& tb : g.tbs)
-      for (const auto& op : tb.ops) {
-        if (op_reduces(op.op)) ir->has_reduce = true;
-        if (op_receives(op.op) && op_sends(op.op)) ir->has_chain = true;
-        if (op_sends(op.op) || op_receives(op.op)) ir->max_count = std::max(ir->max_count, op.count);
-      }
-  ir->slots = std::max(1, comm->cfg.slots);
-  ir->slot_bytes = std::max<int64_t>(comm->cfg.slot_bytes / 256 * 256, 256);
-  {  // lanes provisioned: enough for ~2 CUDA blocks per SM when one rank owns a device
-    int max_tbs = 1;
-    for (const auto& g : ir->prog.gpus) max_tbs = std::max(max_tbs, static_cast<int>(g.tbs.size()));
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, comm->device);
-    ir->lanes = std::max(1, std::min(comm->cfg.max_lanes, (2 * sms + max_tbs - 1) / max_tbs));
-  }
-  {  // direct / pulled messages (and lanes that differ across their connections) only when every
-     // rank runs in one launch: all ranks hosted here, on one device
-    bool one_launch = true;
-    for (int r = 0; r < comm->nranks; ++r)
-      one_launch = one_launch && comm->clique->local[r] && comm->clique->local[r]->device == comm->device;
-    ir->lane_mask = one_launch ? transport_mask(comm->cfg.direct) : 0;
-  }
-  ir->mult = comm->cfg.balance ? lane_multipliers(ir->prog, comm->cfg.balance, comm->cfg.mult_cap, ir->lane_mask)
-                               : std::vector<std::vector<int>>();
-  if (ir->mult.empty())
-    for (const auto& g : ir->prog.gpus) ir->mult.emplace_back(g.tbs.size(), 1);
-  ir->lay = make_layout(ir->prog, comm->rank, ir->lanes, ir->slots, ir->slot_bytes, ir->mult);
-  {
-    DeviceGuard g(comm->device);
-    CUDA_TRY(cudaMalloc(&ir->arena, ir->lay.bytes));
-    CUDA_TRY(cudaMemset(ir->arena, 0, ir->lay.bytes));
-    CUDA_TRY(cudaDeviceSynchronize());
-    // publish the arena to the other processes of the clique
-    bool remote_peers = false;
-    for (int r = 0; r < comm->nranks; ++r) remote_peers = remote_peers || !comm->clique->local[r];
-    if (remote_peers) {
-      CUDA_TRY(cudaIpcGetMemHandle(&ir->handle, ir->arena));
-      const std::string rec(reinterpret_cast<const char*>(&ir->handle), sizeof(ir->handle));
-      const int id = static_cast<int>(comm->irs.size());
-      if (!post_record(shm_dir(comm->clique->key), "ir" + std::to_string(id) + ".rank" + std::to_string(comm->rank), rec))
-        return set_error(ncclSystemError, "cannot publish arena handle");
-    }
-  }
-  comm->irs.push_back(std::move(ir));
-  if (ir_id) *ir_id = static_cast<int>(comm->irs.size()) - 1;
-  return ncclSuccess;
+  return register_program(comm, std::move(ir), ir_id);
 }
+
 
 ncclResult_t gc3SetProtocolOverride(ncclComm_t comm, int ir_id, int proto) {
   if (!comm || ir_id < 0 || ir_id >= static_cast<int>(comm->irs.size()) || proto < -1 || proto > 2)
@@ -2150,6 +2189,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "wq") c.wq = static_cast<int>(value);
   else if (k == "tma_min") c.tma_min = value;
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
+  else if (k == "builtin") c.builtin = static_cast<int>(value);
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
@@ -2398,6 +2438,13 @@ ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json) {
     o += "]";
   }
   *json = dup_cstr(o + "]");
+  return ncclSuccess;
+}
+ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir) {
+  if (!collective || !ir) return ncclInvalidArgument;
+  auto h = std::make_unique<gc3Ir>();
+  if (!builtin_program(collective, nranks, h->p)) return ncclInvalidArgument;
+  *ir = h.release();
   return ncclSuccess;
 }
 ncclResult_t gc3IrFree(gc3Ir_t ir) {

@@ -91,6 +91,7 @@ def lib():
         "gc3IrLaneMultipliers": [vp, ctypes.POINTER(vp)],
         "gc3IrSourceReads": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrResultWrites": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
+        "gc3IrBuiltin": [cp, i, ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -141,6 +142,13 @@ class IR:
             e.path, e.message = path, msg
             raise e
         self._h = h
+
+    @classmethod
+    def builtin(cls, collective, nranks):
+        """The runtime's built-in program for `collective` on nranks ranks."""
+        h = ctypes.c_void_p()
+        check(lib().gc3IrBuiltin(collective.encode(), nranks, ctypes.byref(h)))
+        return cls._wrap(h)
 
     @classmethod
     def from_xml(cls, text, fold_nops=True):
