@@ -157,10 +157,14 @@ __device__ __forceinline__ F float_apply(F a, F b) {
 }
 
 // Element-wise reduction functor over raw storage. kEsize = element bytes.
+// kBulkAdd: the L2 can apply this reduction to a bulk copy bit-exactly (cp.reduce.async.bulk .add):
+// 1 u32, 2 u64 (wrapping integer sums), 3 bf16, 4 f16 (.noftz, round to nearest even); 0 none (f32 is
+// excluded: the L2's f32 add flushes subnormals, the oracle keeps them)
 template <typename T, int OP>
 struct RedInt {
   static constexpr int kEsize = sizeof(T);
   static constexpr bool kReduce = true;
+  static constexpr int kBulkAdd = OP == kSum ? (sizeof(T) == 4 ? 1 : (sizeof(T) == 8 ? 2 : 0)) : 0;
   __device__ static void elem(const char* a, const char* b, char* o) {
     *reinterpret_cast<T*>(o) = IntOp<T, OP>::apply(*reinterpret_cast<const T*>(a), *reinterpret_cast<const T*>(b));
   }
@@ -179,6 +183,7 @@ template <typename F, int OP>
 struct RedFloat {
   static constexpr int kEsize = sizeof(F);
   static constexpr bool kReduce = true;
+  static constexpr int kBulkAdd = 0;
   __device__ static void elem(const char* a, const char* b, char* o) {
     *reinterpret_cast<F*>(o) = float_apply<F, OP>(*reinterpret_cast<const F*>(a), *reinterpret_cast<const F*>(b));
   }
@@ -197,6 +202,7 @@ template <bool BF, int OP>
 struct RedHalf {
   static constexpr int kEsize = 2;
   static constexpr bool kReduce = true;
+  static constexpr int kBulkAdd = OP == kSum ? (BF ? 3 : 4) : 0;
   __device__ static uint16_t one(uint16_t a, uint16_t b) {
     const float p = BF ? bf16_to_f32(a) : f16_to_f32(a);
     const float q = BF ? bf16_to_f32(b) : f16_to_f32(b);
@@ -225,6 +231,7 @@ struct RedHalf {
 struct RedNone {
   static constexpr int kEsize = 1;
   static constexpr bool kReduce = false;
+  static constexpr int kBulkAdd = 0;
   __device__ static void elem(const char* a, const char*, char* o) { *o = *a; }
   template <typename V>
   __device__ static V vec(V a, V) {
@@ -385,6 +392,17 @@ __device__ __forceinline__ void st_vec_hint(uint4* p, uint4 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1,%2,%3,%4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
                : "memory");
 }
+template <int K>
+__device__ __forceinline__ void bulk_reduce_add(void* gmem, const void* smem, uint32_t bytes) {
+  if (K == 1)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u32 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
+  if (K == 2)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.u64 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
+  if (K == 3)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.noftz.bf16 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
+  if (K == 4)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.noftz.f16 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
@@ -412,6 +430,8 @@ struct Tma {
 // Copies `count` segments of `nbytes` (segment j: a + j*sa -> o0 + j*s0 [, o1 + j*s1]).
 // Called by thread 0 of the unit; returns after every store has completed (async-proxy writes
 // ordered for the generic proxy by the caller's fence.proxy.async).
+// K > 0: the stores are L2 reductions (o0 += piece, see kBulkAdd) instead of copies
+template <int K = 0>
 static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int64_t s0, char* o1, int64_t s1, int64_t nbytes,
                          int count) {
   const int SB = m.sb;
@@ -445,7 +465,9 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
     const uint32_t g = base + static_cast<uint32_t>(p);
     char* sm = m.stage + static_cast<size_t>(g % m.stages) * SB;
     mbar_wait(m.bar + g % m.stages, (g / m.stages) & 1);
-    if (m.pol) {
+    if (K) {
+      bulk_reduce_add<K>(d0, sm, bytes);
+    } else if (m.pol) {
       bulk_store_hint(d0, sm, bytes, m.pol);
       if (d1) bulk_store_hint(d1, sm, bytes, m.pol);
     } else {
@@ -695,7 +717,18 @@ __device__ GC3_TRANSFER_ATTR void transfer(const DevOp& op, bool in_d, char* src
                                          int64_t tma_min) {
   // small transfers take the register path: one round trip, no bulk-engine setup latency
   if (tbytes * op.count < tma_min) tma_ops = 0;
-  if (R::kReduce && (tma_ops & 2) && tma.stages >= 2 && in &&
+  if (R::kBulkAdd && (tma_ops & 8) && tma.stages > 0 && in && !out && srcr == src &&
+      (op.opcode == kOpRrcs || (op.opcode == kOpRrc && dst == src)) &&
+      ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(in) | static_cast<uintptr_t>(tbytes) |
+        static_cast<uintptr_t>(chunk_bytes) | static_cast<uintptr_t>(in_stride)) & 15) == 0) {
+    // in-place sum: the message streams through shared memory and the L2 adds it into the local
+    // span (cp.reduce.async.bulk); the SM never loads the local operand
+    if (t == 0 && tbytes > 0) {
+      fence_proxy_async_global();
+      tma_copy<R::kBulkAdd>(tma, in, in_stride, src, chunk_bytes, nullptr, 0, tbytes, op.count);
+      fence_proxy_async_global();
+    }
+  } else if (R::kReduce && (tma_ops & 2) && tma.stages >= 2 && in &&
              (op.opcode == kOpRrc || op.opcode == kOpRrcs || op.opcode == kOpRrs) &&
              ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(srcr) | reinterpret_cast<uintptr_t>(dst) |
                reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(tbytes) |

@@ -100,7 +100,8 @@ struct Config {
   int direct = 3;                    // bit 0: direct messages, bit 1: pulled messages (direct_messages)
   int source = 1;                    // in-place IRs read the caller's const buffer (source_reads)
   int unit_warps = 0;                // warps per (thread block, lane) unit; 0 = automatic
-  int tma = 3;                       // bulk (TMA) engine on same-device peers: bit 0 copies, bit 1 reductions
+  int tma = 11;                      // bulk (TMA) engine on same-device peers: bit 0 copies, bit 1 staged
+                                     // reductions, bit 3 in-place sums reduced by the L2
   int balance = 1;                   // per-component lane multipliers (lane_multipliers; 2: rounded up)
   int mult_cap = 4;                  // largest lane multiplier
   int taper = 0;                     // quarter tiles in the first and last round of every lane (measured: no gain)

@@ -302,3 +302,45 @@ def test_builtin_programs_without_registration(coll, count, dtype):
     finally:
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("name", ["hier_ar_2x4_par1", "ring_ar_8_ch1"])
+@pytest.mark.parametrize("dtype", ["bfloat16", "float16", "int32", "int64", "uint64", "float32"])
+def test_large_sums_with_special_values(name, dtype):
+    """Sums big enough for the bulk-engine paths (staged reductions, and for 16-bit floats and
+    integers the in-place L2 reduction, cp.reduce.async.bulk), with subnormals, infinities, NaNs and
+    rounding ties among the inputs: bit-exact vs the oracle."""
+    from paper_2201_11840_b200 import gc3
+    from gpu_util import TORCH_DT, make_input, oracle_collective, run_collective, to_np_bits
+    irj = json.loads(read_ir(name))
+    R, count = 8, 8 * 65536
+    comms = gc3.init_all([0] * R)
+    try:
+        for c in comms:
+            c.register_ir(ir_path(name))
+        inputs = []
+        for r in range(R):
+            x = make_input(count, dtype, 40 + r)
+            if dtype in ("bfloat16", "float16", "float32"):
+                bits = {"bfloat16": torch.int16, "float16": torch.int16, "float32": torch.int32}[dtype]
+                v = x.view(bits)
+                v[r::97] = 1                      # smallest subnormal
+                v[r + 5::389] = -32767 if dtype != "float32" else -2147483647  # negative subnormal
+                x[r + 11::1009] = float("inf")
+                x[r + 13::4099] = float("-inf")
+                x[r + 17::8191] = float("nan")
+            inputs.append(x)
+        expected = oracle_collective(irj, "allreduce", [x.clone() for x in inputs], count, dtype)
+        outs = run_collective(comms, "allreduce", inputs, count, dtype, inplace=True)
+        torch.cuda.synchronize()
+        assert comms[0].async_error()[0] == 0
+        for r in range(R):  # compare bit patterns (NaN payloads included)
+            got = to_np_bits(outs[r], dtype)
+            exp = expected[r]
+            ut = {1: np.uint8, 2: np.uint16, 4: np.uint32, 8: np.uint64}[exp.dtype.itemsize]
+            g, e = got.view(ut), exp.view(ut)
+            bad = np.nonzero(g != e)[0]
+            assert bad.size == 0, (r, bad[:8], g[bad[:4]], e[bad[:4]])
+    finally:
+        for c in comms:
+            c.destroy()

@@ -1,3 +1,5 @@
-o=gpurun_out/r01af; mkdir -p $o
-bash tools/ab.sh "llb1:-DGC3_LL_BATCH=1;llb2:-DGC3_LL_BATCH=2;llb4:-DGC3_LL_BATCH=4" "c1 c4" "--proto ll" > $o/ab.txt 2>&1
-for L in 1 4; do GC3_LIB_PATH=/tmp/libgc3_llb$L.so timeout 300 python bench.py --config c4 --sweep --sweep-min 1024 --sweep-max 8388608 --sweep-protos ll --steps 20 > $o/sweep_b$L.jsonl 2>&1; done
+o=gpurun_out/r01ah; mkdir -p $o
+timeout 900 python -m pytest tests -m gpu -q -k "special_values or dtypes or allreduce_f32" > $o/pytest_sel.log 2>&1; echo "rc=$?" >> $o/pytest_sel.log
+GC3_TMA=3 timeout 900 python -m pytest tests -m gpu -q -k "special_values" > $o/pytest_sel_notma8.log 2>&1; echo "rc=$?" >> $o/pytest_sel_notma8.log
+bash tools/envsweep.sh "c3 c4 c5rs" "GC3_TMA=11;GC3_TMA=3" > $o/env.txt 2>&1
+bash tools/envsweep.sh "c2" "GC3_UNIT_WARPS=2;GC3_UNIT_WARPS=4;GC3_WQ_ITEMS=5" >> $o/env.txt 2>&1
