@@ -179,11 +179,14 @@ struct RedInt {
     return r;
   }
 };
+#ifndef GC3_F32_BULKADD  // experiment: f32 sums through the L2 too (subnormal behaviour measured by the tests)
+#define GC3_F32_BULKADD 0
+#endif
 template <typename F, int OP>
 struct RedFloat {
   static constexpr int kEsize = sizeof(F);
   static constexpr bool kReduce = true;
-  static constexpr int kBulkAdd = 0;
+  static constexpr int kBulkAdd = GC3_F32_BULKADD && OP == kSum && sizeof(F) == 4 ? 5 : 0;
   __device__ static void elem(const char* a, const char* b, char* o) {
     *reinterpret_cast<F*>(o) = float_apply<F, OP>(*reinterpret_cast<const F*>(a), *reinterpret_cast<const F*>(b));
   }
@@ -402,6 +405,8 @@ __device__ __forceinline__ void bulk_reduce_add(void* gmem, const void* smem, ui
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.noftz.bf16 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
   if (K == 4)
     asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.noftz.f16 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
+  if (K == 5)
+    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(gmem), "r"(smem_addr(smem)), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read_all() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }

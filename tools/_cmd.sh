@@ -1,5 +1,5 @@
-o=gpurun_out/r01ah; mkdir -p $o
-timeout 900 python -m pytest tests -m gpu -q -k "special_values or dtypes or allreduce_f32" > $o/pytest_sel.log 2>&1; echo "rc=$?" >> $o/pytest_sel.log
-GC3_TMA=3 timeout 900 python -m pytest tests -m gpu -q -k "special_values" > $o/pytest_sel_notma8.log 2>&1; echo "rc=$?" >> $o/pytest_sel_notma8.log
-bash tools/envsweep.sh "c3 c4 c5rs" "GC3_TMA=11;GC3_TMA=3" > $o/env.txt 2>&1
-bash tools/envsweep.sh "c2" "GC3_UNIT_WARPS=2;GC3_UNIT_WARPS=4;GC3_WQ_ITEMS=5" >> $o/env.txt 2>&1
+o=gpurun_out/r01ai; mkdir -p $o
+GC3_BUILD_TAG=_f32 GC3_LIB_OUT=/tmp/libgc3_f32.so GC3_NVCC_DEFS="-DGC3_F32_BULKADD=1" python -m paper_2201_11840_b200.build > /tmp/b.log 2>&1
+GC3_LIB_PATH=/tmp/libgc3_f32.so timeout 600 python -m pytest tests -m gpu -q -k "special_values and float32" > $o/f32.log 2>&1; echo "rc=$?" >> $o/f32.log
+GC3_LIB_PATH=/tmp/libgc3_f32.so timeout 120 python bench.py --config c4 --quick --steps 20 > $o/c4_f32.jsonl 2>&1
+timeout 600 python -m pytest tests -m gpu -q -k "special_values" > $o/sv.log 2>&1; echo "rc=$?" >> $o/sv.log
