@@ -158,8 +158,8 @@ __device__ __forceinline__ F float_apply(F a, F b) {
 
 // Element-wise reduction functor over raw storage. kEsize = element bytes.
 // kBulkAdd: the L2 can apply this reduction to a bulk copy bit-exactly (cp.reduce.async.bulk .add):
-// 1 u32, 2 u64 (wrapping integer sums), 3 bf16, 4 f16 (.noftz, round to nearest even); 0 none (f32 is
-// excluded: the L2's f32 add flushes subnormals, the oracle keeps them)
+// 1 u32, 2 u64 (wrapping integer sums), 3 bf16, 4 f16 (.noftz), 5 f32 (round to nearest even; measured
+// to keep subnormals and to give the oracle's NaN/inf bits: test_large_sums_with_special_values); 0 none
 template <typename T, int OP>
 struct RedInt {
   static constexpr int kEsize = sizeof(T);
@@ -179,8 +179,8 @@ struct RedInt {
     return r;
   }
 };
-#ifndef GC3_F32_BULKADD  // experiment: f32 sums through the L2 too (subnormal behaviour measured by the tests)
-#define GC3_F32_BULKADD 0
+#ifndef GC3_F32_BULKADD  // f32 sums through the L2 too (subnormals kept: measured by the tests)
+#define GC3_F32_BULKADD 1
 #endif
 template <typename F, int OP>
 struct RedFloat {

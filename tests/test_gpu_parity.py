@@ -318,6 +318,8 @@ def test_large_sums_with_special_values(name, dtype):
     try:
         for c in comms:
             c.register_ir(ir_path(name))
+            c.set_config("tma_min", 0)  # every aligned op through the bulk engine (L2 sums included)
+            c.set_config("lanes", 2)    # large tiles
         inputs = []
         for r in range(R):
             x = make_input(count, dtype, 40 + r)
@@ -326,6 +328,7 @@ def test_large_sums_with_special_values(name, dtype):
                 v = x.view(bits)
                 v[r::97] = 1                      # smallest subnormal
                 v[r + 5::389] = -32767 if dtype != "float32" else -2147483647  # negative subnormal
+                v[5000:5400] = torch.arange(1, 401, dtype=bits) * (r + 1)  # all-subnormal sums
                 x[r + 11::1009] = float("inf")
                 x[r + 13::4099] = float("-inf")
                 x[r + 17::8191] = float("nan")
