@@ -295,7 +295,10 @@ def e2e_run(args, cfg, comms, ins, outs, count, stream, step, barrier, dist):
     h2d = sum(x.numel() * x.element_size() for x in host_in)
     d2h = sum(y.numel() * y.element_size() for y in host_out)
     sets = [(ins, outs), ([torch.empty_like(x) for x in ins], [torch.empty_like(y) for y in outs])]
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    # each direction over E_STREAMS copy streams (several DMA engines in flight on the PCIe link)
+    ns = int(os.environ.get("GC3_E2E_STREAMS", "2"))
+    s_ins, s_outs = [torch.cuda.Stream() for _ in range(ns)], [torch.cuda.Stream() for _ in range(ns)]
+    s_in, s_out = s_ins[0], s_outs[0]
     steps = max(1, min(args.steps, 8))
     done = [torch.cuda.Event(), torch.cuda.Event()]      # collective of the set finished
     drained = [torch.cuda.Event(), torch.cuda.Event()]   # download of the set finished
@@ -305,20 +308,27 @@ def e2e_run(args, cfg, comms, ins, outs, count, stream, step, barrier, dist):
     def one(k):
         xs, ys = sets[k % 2]
         res = xs if inplace else ys
-        up = torch.cuda.Event()
-        s_in.wait_event(drained[k % 2])                  # the set's previous result is on the host
-        with torch.cuda.stream(s_in):
-            for h, d in zip(host_in, xs):
+        for si in s_ins:
+            si.wait_event(drained[k % 2])                # the set's previous result is on the host
+        for i, (h, d) in enumerate(zip(host_in, xs)):
+            with torch.cuda.stream(s_ins[i % ns]):
                 d.copy_(h, non_blocking=True)
-            up.record(s_in)
-        stream.wait_event(up)
+        for si in s_ins:
+            up = torch.cuda.Event()
+            up.record(si)
+            stream.wait_event(up)
         run_step(xs, ys)
         done[k % 2].record(stream)
-        s_out.wait_event(done[k % 2])
-        with torch.cuda.stream(s_out):
-            for d, h in zip(res, host_out):
+        for so in s_outs:
+            so.wait_event(done[k % 2])
+        for i, (d, h) in enumerate(zip(res, host_out)):
+            with torch.cuda.stream(s_outs[i % ns]):
                 h.copy_(d, non_blocking=True)
-            drained[k % 2].record(s_out)
+        for so in s_outs[1:]:
+            ev = torch.cuda.Event()
+            ev.record(so)
+            s_out.wait_event(ev)
+        drained[k % 2].record(s_out)
 
     def run_step(xs, ys):
         from paper_2201_11840_b200 import gc3
@@ -338,6 +348,8 @@ def e2e_run(args, cfg, comms, ins, outs, count, stream, step, barrier, dist):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s_in)
+    for si in s_ins[1:]:
+        si.wait_event(e0)
     for k in range(steps):
         one(k)
     e1.record(s_out)
