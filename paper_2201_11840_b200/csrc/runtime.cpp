@@ -111,6 +111,8 @@ struct Config {
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
   int64_t ll_max_bytes = 0;          // Simple IRs run LL up to this many bytes per rank (0: never)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
+  int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
+  int64_t stage_kb = 0;              // bytes per stage (0: automatic, 3+ stages per unit)
   int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
@@ -138,6 +140,8 @@ Config config_from_env() {
   c.tma_min = env_int("GC3_TMA_MIN", c.tma_min);
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
   c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
+  c.smem_kb = env_int("GC3_SMEM_KB", c.smem_kb);
+  c.stage_kb = env_int("GC3_STAGE_KB", c.stage_kb);
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
@@ -1419,8 +1423,14 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.tma_stages = 0;
   // three or more stages per unit: 16 KiB stages for wide units, smaller ones (>= 4 KiB) when
   // many narrow units share the SM's shared memory
-  cp.stage_bytes = std::max(4 << 10, std::min(kStageBytesHost, kSmemBudget / (units_per_block * 3) / 1024 * 1024));
-  if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, kSmemBudget / (units_per_block * cp.stage_bytes));
+  // reductions stream two operands per piece: fewer, larger stages (2 x 24 KiB per 4-warp unit in
+  // 216 KiB) measured 3-4% faster on C3/C4/C5-RS; copies keep 3 x 16 KiB in 192 KiB
+  const bool wide = ir.has_reduce && c->cfg.smem_kb == 192 && c->cfg.stage_kb <= 0 && units_per_block == 4;
+  const int budget = static_cast<int>(std::min<int64_t>(wide ? 216 : c->cfg.smem_kb, 220)) << 10;
+  cp.stage_bytes = c->cfg.stage_kb > 0 ? static_cast<int>(c->cfg.stage_kb) << 10
+                   : wide             ? 24 << 10
+                                      : std::max(4 << 10, std::min(kStageBytesHost, budget / (units_per_block * 3) / 1024 * 1024));
+  if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, budget / (units_per_block * cp.stage_bytes));
   cp.smem = static_cast<size_t>(units_per_block) * cp.tma_stages * cp.stage_bytes;
   int bps = occupancy(cp.smem);
   if (bps * ds.num_sms * units_per_block < weight && cp.smem) {  // staging would break co-residency
@@ -2191,6 +2201,8 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "tma_min") c.tma_min = value;
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
   else if (k == "builtin") c.builtin = static_cast<int>(value);
+  else if (k == "smem_kb") c.smem_kb = value;
+  else if (k == "stage_kb") c.stage_kb = value;
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
