@@ -198,6 +198,10 @@ ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);
 /* The built-in program the runtime uses for `collective` ("allreduce", "allgather", "reducescatter",
  * "alltoall") on nranks ranks when no registered IR matches a call (see gc3RegisterIR). */
 ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir);
+/* Timed model (SPEC.md:464-481 run_timed, as an alpha-beta model over the happens-before graph,
+ * calibrated on a B200 in loopback): predicted microseconds of one launch of the program with chunks
+ * of chunk_bytes, protocol (0 simple, 1 ll) and `lanes` lanes per thread block. */
+ncclResult_t gc3IrPredict(gc3Ir_t ir, int64_t chunk_bytes, int protocol, int lanes, double* us);
 ncclResult_t gc3IrFree(gc3Ir_t ir);
 void gc3Free(void* p);
 

