@@ -1649,6 +1649,12 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     cp.group = 1;
     cp.grid = (units + units_per_block - 1) / units_per_block;
   }
+  // every op below the bulk-engine threshold takes the register path: launch without staging memory
+  // (measured: small LL calls 37 -> 33 us)
+  if (cp.tile_elems * cp.kesize * ir.max_count < c->cfg.tma_min) {
+    cp.tma_stages = 0;
+    cp.smem = 0;
+  }
   return ncclSuccess;
 }
 
