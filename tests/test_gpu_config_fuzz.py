@@ -17,6 +17,7 @@ REG = {"direct": [0, 1, 2, 3], "balance": [0, 1, 2], "l2hint": [0, 1, 3], "sourc
 LAUNCH = {"unit_warps": [0, 1, 2, 4, 8], "lanes": [0, 0, 1, 3, 8], "tile_bytes": [0, 0, 4096, 16384, 65536],
           "tma": [0, 1, 3, 11], "tma_min": [0, 32768], "wq": [0, 1, 2], "group": [0, 1, 2], "taper": [0, 1],
           "wq_items": [1, 4]}
+RAN, REFUSED = [], []
 CASES = [("ring_ar_8_ch8_inst1", "allreduce", 8 * 70001, "float32"), ("hier_ar_2x4_par1", "allreduce", 8 * 65536, "bfloat16"),
          ("twostep_a2a_2x4", "alltoall", 40000, "float32"), ("ring_rs_8", "reducescatter", 33333, "int32"),
          ("ring_ag_4", "allgather", 50000, "float16"), ("allpairs_ar_8", "allreduce", 8 * 20000, "float32")]
@@ -50,7 +51,9 @@ def test_config_fuzz(case, seed):
             outs = run_collective(comms, coll, inputs, count, dtype)
         except gc3.NcclError as e:  # an infeasible combination is refused up front
             assert "co-resident" in str(e) or "invalid usage" in str(e), (reg, launch, proto, str(e))
+            REFUSED.append((case, seed))
             return
+        RAN.append((case, seed))
         torch.cuda.synchronize()
         err = comms[0].async_error()
         assert err[0] == 0, (reg, launch, proto, err)
@@ -61,3 +64,10 @@ def test_config_fuzz(case, seed):
     finally:
         for c in comms:
             c.destroy()
+
+
+def test_zz_most_combinations_run():
+    """(runs after the fuzz cases in the same session) the fuzz is not vacuous"""
+    if not RAN and not REFUSED:
+        pytest.skip("fuzz cases not run in this session")
+    assert len(RAN) >= 2 * len(REFUSED), (len(RAN), len(REFUSED))
