@@ -110,7 +110,8 @@ struct Config {
                                      // evict_first bulk loads (every span is read once)
   int wq = 1;                        // work-queue mode where possible (interp_wq)
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
-  int64_t ll_max_bytes = 0;          // Simple IRs run LL up to this many bytes per rank (0: never)
+  int64_t ll_max_bytes = 512 << 10;  // Simple IRs run LL up to this many bytes per rank (0: never;
+                                     // measured: LL ~2x faster than Simple below ~1 MiB, BASELINE §5.2)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
   int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
   int select = 0;                    // among matching IRs pick the lowest timed-model prediction

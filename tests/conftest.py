@@ -7,6 +7,9 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if REPO not in sys.path:
     sys.path.insert(0, REPO)
 
+# the parity tests pin each protocol explicitly: no size-based switch of Simple IRs to LL
+os.environ.setdefault("GC3_LL_MAX_BYTES", "0")
+
 GOLDEN = os.path.join(REPO, "tests", "golden")
 IR_DIR = os.path.join(GOLDEN, "ir")
 REF_LIB = os.path.join(REPO, "oracle", "_ref", "libref.so")

@@ -378,3 +378,18 @@ def test_select_by_timed_model():
         for c in comms:
             c.destroy()
     assert preds  # (predictions exercised on the host as well)
+
+
+def test_small_messages_switch_to_ll():
+    """ll_max_bytes: a Simple IR runs the LL protocol for messages up to the threshold (per rank),
+    Simple above it; both bit-exact."""
+    from paper_2201_11840_b200 import gc3
+    comms, irj = _setup("ring_ar_8_ch8_inst4", ll_max_bytes=256 << 10)
+    try:
+        assert comms[0].query_plan("allreduce", 32 * 1024, "float32")["protocol"] == 1   # 128 KiB per rank
+        assert comms[0].query_plan("allreduce", 32 * 65536, "float32")["protocol"] == 0  # 8 MiB per rank
+    finally:
+        for c in comms:
+            c.destroy()
+    _check("ring_ar_8_ch8_inst4", 32 * 1024, ll_max_bytes=256 << 10)
+    _check("ring_ar_8_ch8_inst4", 32 * 65536, ll_max_bytes=256 << 10)
