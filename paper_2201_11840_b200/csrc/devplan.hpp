@@ -120,6 +120,7 @@ struct LaunchArgs {
   int32_t uniform;      // 1: every thread block runs `lanes` lanes (LL launches: FIFOs need matched lanes)
   int32_t wq;           // 1: work-queue mode (see interp.cuh interp_wq)
   int32_t* wq_next;     // work-queue claim counter (zeroed before the launch)
+  const int32_t* wq_order;  // claim position -> item (tile * ntbs + thread block); null: identity
   uint64_t* prog;       // work-queue progress: [thread block][tile] = (epoch << 32) | steps done
   char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source, result (the
                                      // caller's recvbuff shifted so that an owned ReduceScatter chunk

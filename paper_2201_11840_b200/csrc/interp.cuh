@@ -853,6 +853,7 @@ struct WqArgs {  // the launch arguments the work queue reads (by value: no loca
   const DevOp* ops;
   const DevDep* deps;
   int32_t* wq_next;
+  const int32_t* wq_order;
   uint64_t* prog;
   int32_t* abort_flag;
   uint64_t* err_info;
@@ -874,8 +875,9 @@ __device__ GC3_WQ_ATTR void interp_wq(const WqArgs a, char* const* s_bufs, Tma& 
   for (;;) {
     if (t == 0) s_item[uib] = static_cast<int>(atomicAdd(a.wq_next, 1));
     unit_sync(uw, bar_id, n);
-    const int64_t item = s_item[uib];
-    if (item >= nitems) return;
+    const int64_t claim = s_item[uib];
+    if (claim >= nitems) return;
+    const int64_t item = a.wq_order ? a.wq_order[claim] : claim;
     const int tbi = static_cast<int>(item % a.ntbs);
     const int64_t tile = item / a.ntbs;
     const DevTb tb = a.tbs[tbi];
@@ -1136,7 +1138,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(cons
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   unit_sync(uw, bar_id, n);
-  const WqArgs w{a.tbs, a.ops, a.deps, a.wq_next, a.prog, a.abort_flag, a.err_info, a.timeout_ns,
+  const WqArgs w{a.tbs, a.ops, a.deps, a.wq_next, a.wq_order, a.prog, a.abort_flag, a.err_info, a.timeout_ns,
                  a.chunk_elems, a.tile_elems, a.ntiles, a.epoch, a.ntbs, a.tma_ops, a.tma_min};
   interp_wq<R>(w, s_bufs, tma, pol_last, t, n, uw, uib, bar_id);
 }

@@ -117,6 +117,7 @@ struct Config {
   int select = 0;                    // among matching IRs pick the lowest timed-model prediction
   int64_t stage_kb = 0;              // bytes per stage (0: automatic, 3+ stages per unit)
   int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
+  int wq_lag = 0;                    // claim deeper thread blocks' items this many tiles later (0: off)
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
 };
@@ -147,6 +148,7 @@ Config config_from_env() {
   c.select = static_cast<int>(env_int("GC3_SELECT", c.select));
   c.stage_kb = env_int("GC3_STAGE_KB", c.stage_kb);
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
+  c.wq_lag = static_cast<int>(env_int("GC3_WQ_LAG", c.wq_lag));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
   return c;
 }
@@ -289,6 +291,8 @@ struct RankIR {
 struct DevicePlan {  // one registered IR on one device
   bool built = false;
   bool wq_ok = false;  // work-queue mode possible (no FIFO message, one launch)
+  std::vector<int> wq_level;  // per launch thread block: 1 + max level of the thread blocks its deps name
+  std::map<std::pair<int64_t, int>, int32_t*> wq_order;  // (ntiles, lag) -> device claim-order table
   bool source_complete = false;  // every first read of `input` reads the source buffer (source_reads)
   bool result_complete = false;  // ReduceScatter owned blocks are written straight to recvbuff (result_writes)
   std::vector<int> ranks;  // local ranks in launch order (rank_slot -> rank)
@@ -1035,6 +1039,20 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   }
   // work-queue mode needs every message direct or pulled (no FIFO) and every rank in this launch
   plan.wq_ok = ir0.lane_mask != 0 && fifo_conn.empty();
+  plan.wq_level.assign(launch_index.size(), 0);
+  for (int pass = 0; pass < static_cast<int>(launch_index.size()); ++pass)  // longest dep chain, by relaxation
+    for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
+      const int r = plan.ranks[slot];
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+        int& lv = plan.wq_level[launch_index[{r, static_cast<int>(t)}]];
+        for (const Op& op : p.gpus[r].tbs[t].ops)
+          for (const Dep& d : op.deps) {
+            const int ti = tb_index(p, r, d.tb);
+            if (ti >= 0 && ti != static_cast<int>(t)) lv = std::max(lv, 1 + plan.wq_level[launch_index[{r, ti}]]);
+          }
+        lv = std::min(lv, 64);
+      }
+    }
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
     const int r = plan.ranks[slot];
     Comm* c = cl->local[r];
@@ -1872,6 +1890,28 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     CUDA_TRY(cudaMemsetAsync(ds->d_wq_next, 0, sizeof(int32_t), stream));
     a.wq_next = ds->d_wq_next;
     a.prog = ds->d_prog;
+    a.wq_order = nullptr;
+    const int lag = c0->cfg.wq_lag;
+    if (lag > 0) {  // items of a deeper thread block are claimed `lag` tiles later: fewer blocked units
+      auto key = std::make_pair(cp.ntiles, lag);
+      auto f = plan.wq_order.find(key);
+      if (f == plan.wq_order.end()) {
+        const int nt = plan.ntbs;
+        std::vector<std::pair<int64_t, int32_t>> items;
+        items.reserve(static_cast<size_t>(nt) * cp.ntiles);
+        for (int64_t tile = 0; tile < cp.ntiles; ++tile)
+          for (int tb = 0; tb < nt; ++tb)
+            items.push_back({(tile + static_cast<int64_t>(plan.wq_level[tb]) * lag) * nt + tb, static_cast<int32_t>(tile * nt + tb)});
+        std::stable_sort(items.begin(), items.end());
+        std::vector<int32_t> order(items.size());
+        for (size_t i = 0; i < items.size(); ++i) order[i] = items[i].second;
+        int32_t* d = nullptr;
+        CUDA_TRY(cudaMalloc(&d, std::max<size_t>(order.size(), 1) * sizeof(int32_t)));
+        CUDA_TRY(cudaMemcpy(d, order.data(), order.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        f = plan.wq_order.emplace(key, d).first;
+      }
+      a.wq_order = f->second;
+    }
   }
   CUDA_TRY(interp_launch(cp.fn, a, cp.grid, cp.smem, stream));
   for (const PostCopy& pc : post)
@@ -2149,6 +2189,7 @@ static void release_comm(Comm* c) {
         cudaFree(p.d_deps);
         cudaFree(p.d_chans);
         cudaFree(p.d_sems);
+        for (auto& [k, d] : p.wq_order) cudaFree(d);
       }
       cudaFree(ds.d_abort);
       if (ds.d_trace) cudaFree(ds.d_trace);
@@ -2314,6 +2355,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "select") c.select = static_cast<int>(value);
   else if (k == "stage_kb") c.stage_kb = value;
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
+  else if (k == "wq_lag") c.wq_lag = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;

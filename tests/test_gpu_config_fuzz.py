@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 REG = {"direct": [0, 1, 2, 3], "balance": [0, 1, 2], "l2hint": [0, 1, 3], "source": [0, 1], "slots": [2, 3]}
 LAUNCH = {"unit_warps": [0, 1, 2, 4, 8], "lanes": [0, 0, 1, 3, 8], "tile_bytes": [0, 0, 4096, 16384, 65536],
           "tma": [0, 1, 3, 11], "tma_min": [0, 32768], "wq": [0, 1, 2], "group": [0, 1, 2], "taper": [0, 1],
-          "wq_items": [1, 4]}
+          "wq_items": [1, 4], "wq_lag": [0, 1, 3]}
 RAN, REFUSED = [], []
 CASES = [("ring_ar_8_ch8_inst1", "allreduce", 8 * 70001, "float32"), ("hier_ar_2x4_par1", "allreduce", 8 * 65536, "bfloat16"),
          ("twostep_a2a_2x4", "alltoall", 40000, "float32"), ("ring_rs_8", "reducescatter", 33333, "int32"),

@@ -271,6 +271,7 @@ def test_work_queue_mode(name, count, dtype, wq):
     items (interp_wq) or on static lanes: same bits either way."""
     _check(name, count, dtype, wq=wq)
     _check(name, count, dtype, wq=wq, wq_items=1)
+    _check(name, count, dtype, wq=wq, wq_items=2, wq_lag=2)  # lagged claim order
 
 
 @pytest.mark.parametrize("coll,count,dtype", [("allreduce", 8 * 1000 + 5, "float32"), ("allgather", 4096, "bfloat16"),
