@@ -42,7 +42,17 @@ CONFIGS = {
                  desc="Ring AllGather GC3-IR, 8 ranks"),
     "c5rs": dict(ir="ring_rs_8", coll="reducescatter", dtype="float32", bytes=64 << 20, proto=None,
                  desc="Ring ReduceScatter GC3-IR, 8 ranks"),
+    # C5 at 2 and 4 ranks (sweep / quick only; the 8-rank bench line stays the default contract)
+    "c5ag4": dict(ir="ring_ag_4", coll="allgather", dtype="float32", bytes=64 << 20, proto=None, desc="Ring AllGather, 4 ranks"),
+    "c5ag2": dict(ir="ring_ag_2", coll="allgather", dtype="float32", bytes=64 << 20, proto=None, desc="Ring AllGather, 2 ranks"),
+    "c5rs4": dict(ir="ring_rs_4", coll="reducescatter", dtype="float32", bytes=64 << 20, proto=None, desc="Ring ReduceScatter, 4 ranks"),
+    "c5rs2": dict(ir="ring_rs_2", coll="reducescatter", dtype="float32", bytes=64 << 20, proto=None, desc="Ring ReduceScatter, 2 ranks"),
 }
+
+
+def ir_ranks(cfg):
+    with open(os.path.join(IR_DIR, cfg["ir"] + ".ir.json")) as f:
+        return len(json.load(f)["gpus"])
 ESIZE = {"float32": 4, "bfloat16": 2, "float16": 2, "int32": 4}
 
 
@@ -439,7 +449,7 @@ def run_sweep(args, cfg):
     import torch
     from paper_2201_11840_b200 import gc3
     torch.cuda.set_device(0)
-    R = 8
+    R = ir_ranks(cfg)
     comms = setup_comms(dict(cfg, proto=None), args, R, 0, 1, 0, None)
     peaks, _ = load_peaks()
     stream = torch.cuda.Stream()
@@ -484,7 +494,7 @@ def run_sweep(args, cfg):
             ms = e0.elapsed_time(e1) / steps
             err = comms[0].async_error()
             plan = comms[0].query_plan(cfg["coll"], count, cfg["dtype"])
-            print(json.dumps({"config": args.config, "ir": cfg["ir"], "proto": proto, "bytes": nbytes, "us": round(ms * 1e3, 2),
+            print(json.dumps({"config": args.config, "ir": cfg["ir"], "ranks": R, "proto": proto, "bytes": nbytes, "us": round(ms * 1e3, 2),
                               "algbw_gbs": round(nbytes / (ms * 1e-3) / 1e9, 2),
                               "busbw_gbs": round(nbytes / (ms * 1e-3) / 1e9 * bus_factor(cfg["coll"], R), 2),
                               "hbm_frac": round(plan["hbm_bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
