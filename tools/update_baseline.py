@@ -98,6 +98,10 @@ for 8 data bytes and cannot use the direct/pulled transports); register one IR p
 """
     p = os.path.join(REPO, "BASELINE.md")
     s = open(p).read()
+    keep = ""  # sections measured separately (e.g. 5.2b, the C5 rank sweeps) survive a refresh
+    if "### 5.2b" in s:
+        keep = s[s.index("### 5.2b"):s.index("### 5.3")]
+        sec = sec.replace("### 5.3 Progress", keep + "### 5.3 Progress")
     s = s[:s.index("## 5. Results")] + sec
     open(p, "w").write(s)
     print(sec[:400])
