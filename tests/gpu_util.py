@@ -46,15 +46,17 @@ def oracle_collective(ir_json, coll, inputs, count, dtype, op="sum"):
                       [to_np_bits(x, dtype) for x in inputs], count, odt, op)
 
 
-def run_collective(comms, coll, inputs, count, dtype, op="sum", inplace=False, stream=None):
-    """Issues one grouped collective over the comms; returns the recv tensors."""
+def run_collective(comms, coll, inputs, count, dtype, op="sum", inplace=False, stream=None, nranks=None, first_rank=0):
+    """Issues one grouped collective over the comms (ranks first_rank.. of an nranks-rank clique,
+    all of it by default); returns the recv tensors."""
     from paper_2201_11840_b200 import gc3
-    R = len(comms)
+    R = nranks or len(comms)
     tdt = TORCH_DT[dtype]
     outs = []
     with gc3.group():
-        for r, c in enumerate(comms):
-            x = inputs[r]
+        for k, c in enumerate(comms):
+            r = first_rank + k
+            x = inputs[k]
             if coll == "allreduce":
                 recv = x if inplace else torch.empty(count, dtype=tdt, device=x.device)
                 c.all_reduce(x, recv, count, dtype, op, stream)

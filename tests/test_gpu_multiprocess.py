@@ -1,0 +1,88 @@
+"""The multi-process path on one B200: two processes host four ranks each (ncclCommInitRank inside
+a group, /dev/shm bootstrap, CUDA IPC arenas), so every message between the processes goes through
+the receiver-resident FIFOs with .sys-scope flags — the code the N-GPU runs use — and the results
+must be bit-exact vs the oracle."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import ir_path, read_ir
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(proc, nproc, port, name, coll, count, dtype, q):
+    import torch.distributed as dist
+    from paper_2201_11840_b200 import gc3
+    from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=proc, world_size=nproc)
+    try:
+        torch.cuda.set_device(0)
+        irj = json.loads(read_ir(name))
+        R = len(irj["gpus"])
+        per = R // nproc
+        uid = [gc3.get_unique_id() if proc == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        with gc3.group():
+            comms = [gc3.init_rank(R, uid[0], proc * per + k) for k in range(per)]
+        for c in comms:
+            c.register_ir(ir_path(name))
+        inputs = [make_input(input_len(coll, count, R), dtype, 90 + r) for r in range(R)]
+        expected = oracle_collective(irj, coll, [x.clone() for x in inputs], count, dtype)
+        mine = [inputs[proc * per + k] for k in range(per)]
+        ok, why = True, []
+        for it in range(2):
+            outs = run_collective(comms, coll, [x.clone() for x in mine], count, dtype, nranks=R, first_rank=proc * per)
+            torch.cuda.synchronize()
+            err = comms[0].async_error()
+            if err[0] != 0:
+                ok = False
+                why.append(f"it {it}: async error {err}")
+            for k in range(per):
+                r = proc * per + k
+                got, exp = to_np_bits(outs[k], dtype), expected[r]
+                if not np.array_equal(got, exp):
+                    ok = False
+                    bad = np.nonzero(got != exp)[0]
+                    why.append(f"it {it} rank {r}: {bad.size} mismatches, first {bad[:6].tolist()}")
+            dist.barrier()
+        for c in comms:
+            c.destroy()
+        q.put((proc, ok, "; ".join(why)))
+    except Exception as e:  # reported to the parent
+        q.put((proc, False, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,coll,count,dtype", [("ring_ar_8_ch1", "allreduce", 8 * 40000, "float32"),
+                                                   ("twostep_a2a_2x4", "alltoall", 30000, "bfloat16"),
+                                                   ("ring_rs_8", "reducescatter", 20000, "int32"),
+                                                   ("hier_ar_2x4_par1", "allreduce", 8 * 30000, "bfloat16"),
+                                                   ("ring_ag_8", "allgather", 25000, "float32")])
+def test_two_processes_share_a_gpu(name, coll, count, dtype):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, q)) for p in range(2)]
+    for p in procs:
+        p.start()
+    results = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for proc, ok, err in results:
+        assert ok, (proc, err)
