@@ -23,7 +23,7 @@ def _free_port():
     return p
 
 
-def _worker(proc, nproc, port, name, coll, count, dtype, q):
+def _worker(proc, nproc, port, name, coll, count, dtype, proto, q):
     import torch.distributed as dist
     from paper_2201_11840_b200 import gc3
     from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
@@ -39,7 +39,9 @@ def _worker(proc, nproc, port, name, coll, count, dtype, q):
         with gc3.group():
             comms = [gc3.init_rank(R, uid[0], proc * per + k) for k in range(per)]
         for c in comms:
-            c.register_ir(ir_path(name))
+            i = c.register_ir(ir_path(name))
+            if proto:
+                c.set_protocol(i, proto)
         inputs = [make_input(input_len(coll, count, R), dtype, 90 + r) for r in range(R)]
         expected = oracle_collective(irj, coll, [x.clone() for x in inputs], count, dtype)
         mine = [inputs[proc * per + k] for k in range(per)]
@@ -68,17 +70,22 @@ def _worker(proc, nproc, port, name, coll, count, dtype, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("name,coll,count,dtype", [("ring_ar_8_ch1", "allreduce", 8 * 40000, "float32"),
-                                                   ("twostep_a2a_2x4", "alltoall", 30000, "bfloat16"),
-                                                   ("ring_rs_8", "reducescatter", 20000, "int32"),
-                                                   ("hier_ar_2x4_par1", "allreduce", 8 * 30000, "bfloat16"),
-                                                   ("ring_ag_8", "allgather", 25000, "float32")])
-def test_two_processes_share_a_gpu(name, coll, count, dtype):
+@pytest.mark.parametrize("name,coll,count,dtype,proto", [
+    ("ring_ar_8_ch1", "allreduce", 8 * 40000, "float32", None),
+    ("twostep_a2a_2x4", "alltoall", 30000, "bfloat16", None),
+    ("ring_rs_8", "reducescatter", 20000, "int32", None),
+    ("hier_ar_2x4_par1", "allreduce", 8 * 30000, "bfloat16", None),
+    ("ring_ag_8", "allgather", 25000, "float32", None),
+    # LL lines across processes (.sys-scope line flags), and a ragged count (padded chunks)
+    ("ring_ar_8_ch1", "allreduce", 8 * 5000, "float32", "ll"),
+    ("twostep_a2a_2x4", "alltoall", 7000, "float16", "ll"),
+    ("ring_ar_8_ch1", "allreduce", 8 * 40000 + 13, "float32", None)])
+def test_two_processes_share_a_gpu(name, coll, count, dtype, proto):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, q)) for p in range(2)]
+    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, proto, q)) for p in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=240) for _ in procs]

@@ -94,7 +94,7 @@ for 8 data bytes and cannot use the direct/pulled transports); register one IR p
   `{tag}_c4ll.md` (LL), `{tag}_c3.md`; earlier iterations `r01a`–`r01r`, `r01f1`, `r01f2`.
 * NVLink (N > 1) numbers: not measurable this round (one GPU per box). The multi-process path (CUDA
   IPC arenas, FIFO messages between processes) is validated on one B200 with two processes of four
-  ranks each (`tests/test_gpu_multiprocess.py`, 5 programs bit-exact), and its host logic by
+  ranks each (`tests/test_gpu_multiprocess.py`: 5 programs, Simple and LL, a ragged count; bit-exact), and its host logic by
   2-process gloo tests on CPU (`tests/test_multiproc.py`).
 * Stock NCCL context: not available at N = 1 (NCCL does not run 8 ranks on one GPU).
 """
