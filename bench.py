@@ -72,6 +72,19 @@ def input_elems(coll, count, R):
     return count if coll in ("allreduce", "allgather") else R * count
 
 
+PROTO_NAMES = {0: "simple", 1: "ll", 2: "ll128"}
+NVLINK_PEER_GBS = 770.0  # measured peer copy per direction per GPU (B200_PROFILING.md; 900 nominal)
+
+
+def workload_config(cfg, S, R, world):
+    """The `config` object of the JSON line: identical in both arms (gc3 and reference)."""
+    return {"workload": cfg["desc"], "ir": cfg["ir"], "collective": cfg["coll"], "dtype": cfg["dtype"], "ranks": R,
+            "bytes_per_rank": S, "count": per_rank_count(cfg, S, R),
+            "placement": "loopback: 8 IR ranks on 1 GPU" if world == 1 else f"{R // world} IR ranks per GPU",
+            "l2": f"inputs larger than L2 ({R * S >> 20} MiB per step)" if R * S > (126 << 20) else "L2-resident inputs",
+            "value_definition": "sum over the R ranks of nccl-tests busBW"}
+
+
 def load_peaks():
     try:
         with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
@@ -239,37 +252,41 @@ def run_gc3(args, cfg):
     bf = bus_factor(cfg["coll"], R)
     S = nbytes
     busbw = S / (ms * 1e-3) * bf / 1e9
+    verified = verify_outputs(cfg, comms, count, stream, dist)
     result = {
         "metric": METRIC, "value": round(busbw * R, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms, 5), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": {"float32": "f32", "bfloat16": "bf16"}.get(cfg["dtype"], cfg["dtype"]),
         "data": "synthetic (seeded N(0,1), seed 0x6C33+rank)",
-        "config": {"workload": cfg["desc"], "ir": cfg["ir"], "collective": cfg["coll"], "ranks": R,
-                   "bytes_per_rank": S, "count": count,
-                   "placement": "loopback: 8 IR ranks on 1 GPU" if world == 1 else f"{R // world} IR ranks per GPU",
-                   "protocol": "ll" if plan["protocol"] else "simple", "lanes": plan["lanes"], "grid": plan["grid"],
-                   "tile_bytes": plan["tile_elems"] * ESIZE[cfg["dtype"]], "slots": plan["slots"],
-                   "l2": f"inputs larger than L2 ({R * S >> 20} MiB per step)" if R * S > (126 << 20) else "L2-resident inputs",
-                   "value_definition": "sum over the R ranks of nccl-tests busBW"},
+        "config": workload_config(cfg, S, R, world),
+        "plan": {"protocol": PROTO_NAMES.get(plan["protocol"], plan["protocol"]), "lanes": plan["lanes"], "grid": plan["grid"],
+                 "tile_bytes": plan["tile_elems"] * ESIZE[cfg["dtype"]], "slots": plan["slots"]},
         "busbw_per_rank_gbs": round(busbw, 2),
         "algbw_per_rank_gbs": round(S / (ms * 1e-3) / 1e9, 2),
+        "verified": verified,
         "impl": "gc3",
     }
     peaks, kind = load_peaks()
-    hbm_ms = ms  # the launch is the only kernel of the step (no pre-copies for this call shape)
-    achieved = plan["hbm_bytes"] / (hbm_ms * 1e-3) / 1e9 if world == 1 else None
-    result["roofline"] = {
-        "bound": "hbm", "achieved": round(achieved, 1) if achieved else None, "peak": peaks["hbm_gbs"],
-        "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4) if achieved else None,
-        "traffic": load_traffic(cfg, S, world), "peak_kind": kind,
-        "algorithmic_bytes_per_launch": plan["hbm_bytes"],
-        "note": "algorithmic bytes = local reads+writes of user/scratch buffers per op (send 1R, recv 1W, "
-                "copy 1R1W, rrc 1R1W, rcs 1W, rrcs 1R1W, rrs 1R, reduce 2R1W) x count x chunk bytes, all ranks of the launch",
-    }
-    if world > 1:
+    if world == 1:
+        # loopback: every message is HBM traffic; the launch is the only kernel of the step
+        achieved = plan["hbm_bytes"] / (ms * 1e-3) / 1e9
+        result["roofline"] = {
+            "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": load_traffic(cfg, S, world), "peak_kind": kind,
+            "algorithmic_bytes_per_launch": plan["hbm_bytes"],
+            "note": "algorithmic bytes = local reads+writes of user/scratch buffers per op (send 1R, recv 1W, "
+                    "copy 1R1W, rrc 1R1W, rcs 1W, rrcs 1R1W, rrs 1R, reduce 2R1W) x count x chunk bytes, all ranks of the launch",
+        }
+    else:
+        # across GPUs: the bytes that must cross NVLink (max over ranks of bytes sent or received) per
+        # launch over the measured peer-copy bandwidth
         wire = plan["wire_bytes"] / (ms * 1e-3) / 1e9
-        result["nvlink"] = {"achieved_wire_gbs": round(wire, 1), "peak": 770.0, "nominal": 900.0,
-                            "frac_of_measured": round(wire / 770.0, 4)}
+        result["roofline"] = {
+            "bound": "nvlink", "achieved": round(wire, 1), "peak": NVLINK_PEER_GBS, "unit": "GB/s",
+            "frac": round(wire / NVLINK_PEER_GBS, 4), "traffic": None, "peak_kind": "measured peer copy (B200_PROFILING.md)",
+            "algorithmic_bytes_per_launch": plan["wire_bytes"],
+            "note": "wire bytes = max over ranks of chunks sent or received x chunk bytes; 900 GB/s nominal",
+        }
     result["e2e"] = {"value": round(S / (e2e_ms * 1e-3) * bf / 1e9 * R, 2), "unit": "GB/s",
                      "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(e2e_ms, 4)}
     result["clocks"] = clocks.summary()
@@ -277,11 +294,16 @@ def run_gc3(args, cfg):
     if args.quick and rank == 0:
         print(json.dumps({"config": args.config, "bytes": S, "ms": round(ms, 4), "agg_busbw": result["value"],
                           "hbm_frac": result["roofline"]["frac"], "lanes": plan["lanes"], "grid": plan["grid"],
-                          "tile": result["config"]["tile_bytes"], "proto": result["config"]["protocol"],
+                          "tile": result["plan"]["tile_bytes"], "proto": result["plan"]["protocol"], "verified": verified,
                           "uw": plan["unit_warps"], "group": plan["group"], "ntiles": plan["ntiles"]}), flush=True)
         for c in comms:
             c.destroy()
         return
+    if world == 1 and not args.no_more:
+        for c in comms:
+            c.destroy()
+        comms = []
+        result["more"] = [more_config(name, args) for name in args.more.split(",") if name]
     if rank == 0 and not args.no_cpu_baseline:
         result["cpu_baseline"] = cpu_baseline(cfg, S, R, budget_s=args.cpu_seconds)
     if rank == 0:
@@ -290,6 +312,134 @@ def run_gc3(args, cfg):
         c.destroy()
     if dist:
         dist.destroy_process_group()
+
+
+def verify_outputs(cfg, comms, count, stream=None, dist=None, seed=0x5EED):
+    """Parity gate of a timed configuration: one more collective on fresh seeded inputs, checked
+    exactly. AllToAll / AllGather outputs must be the exact permutation of the inputs; reductions
+    must equal the CPU oracle's result (oracle/, used here only as the checker) bit for bit.
+    Returns True, or raises."""
+    import json as _json
+    import numpy as np
+    import torch
+    from paper_2201_11840_b200 import gc3
+    R = comms[0].nranks
+    coll, dt = cfg["coll"], cfg["dtype"]
+    tdt = getattr(torch, dt)
+    n_in = input_elems(coll, count, R)
+
+    def host_input(r):
+        g = torch.Generator(device="cpu").manual_seed(seed + r)
+        return torch.randn(n_in, generator=g, dtype=torch.float32).to(tdt)
+
+    hins = {c.rank: host_input(c.rank) for c in comms}
+    ins = {r: x.cuda() for r, x in hins.items()}
+    outs = {}
+    with gc3.group():
+        for c in comms:
+            x = ins[c.rank]
+            if coll == "allreduce":
+                outs[c.rank] = torch.empty(count, device="cuda", dtype=tdt)
+                c.all_reduce(x, outs[c.rank], count, dt, "sum", stream)
+            elif coll == "alltoall":
+                outs[c.rank] = torch.empty(R * count, device="cuda", dtype=tdt)
+                c.all_to_all(x, outs[c.rank], count, dt, stream)
+            elif coll == "allgather":
+                outs[c.rank] = torch.empty(R * count, device="cuda", dtype=tdt)
+                c.all_gather(x, outs[c.rank], count, dt, stream)
+            else:
+                outs[c.rank] = torch.empty(count, device="cuda", dtype=tdt)
+                c.reduce_scatter(x, outs[c.rank], count, dt, "sum", stream)
+    torch.cuda.synchronize()
+    err = comms[0].async_error()
+    if err[0]:
+        raise SystemExit(f"verification run failed: {err[1]}")
+    if coll in ("alltoall", "allgather"):
+        allin = [hins[r] if r in hins else host_input(r) for r in range(R)]
+        for d, y in outs.items():
+            y = y.cpu()
+            for s_ in range(R):
+                want = allin[s_][d * count:(d + 1) * count] if coll == "alltoall" else allin[s_]
+                if not torch.equal(y[s_ * count:(s_ + 1) * count].view(torch.int16 if tdt != torch.float32 else torch.int32),
+                                   want.view(torch.int16 if tdt != torch.float32 else torch.int32)):
+                    raise SystemExit(f"verification failed: rank {d} block {s_} differs")
+        return True
+    from oracle.oracle import collective
+
+    def bits(t):
+        t = t.contiguous()
+        return t.view(torch.int16).numpy().view(np.uint16) if t.element_size() == 2 else t.view(torch.int32).numpy().view(np.uint32)
+
+    with open(os.path.join(IR_DIR, cfg["ir"] + ".ir.json")) as f:
+        irj = _json.load(f)
+    odt = {"bfloat16": 9, "float16": 6}.get(dt, dt)
+    want = collective(irj, coll, [bits(hins[r] if r in hins else host_input(r)) for r in range(R)], count, odt, "sum",
+                      mode="threaded")
+    for r, y in outs.items():
+        if not np.array_equal(bits(y.cpu()), want[r]):
+            raise SystemExit(f"verification failed: rank {r} differs from the oracle")
+    return True
+
+
+def more_config(name, args):
+    """Device time of another BASELINE configuration (the AllReduce half of the metric), verified
+    like the headline: {config, ms, aggregate busBW, HBM roofline fraction}."""
+    import torch
+    from paper_2201_11840_b200 import gc3
+    cfg = CONFIGS[name]
+    R = ir_ranks(cfg)
+    comms = setup_comms(dict(cfg), args, R, 0, 1, 0, None)
+    try:
+        S = cfg["bytes"]
+        count = per_rank_count(cfg, S, R)
+        tdt = getattr(torch, cfg["dtype"])
+        n_in = input_elems(cfg["coll"], count, R)
+        g = torch.Generator(device="cuda")
+        ins = []
+        for c in comms:
+            g.manual_seed(0x6C33 + c.rank)
+            ins.append(torch.randn(n_in, device="cuda", generator=g, dtype=torch.float32).to(tdt))
+        outs = [torch.empty(R * count if cfg["coll"] in ("allgather", "alltoall") else count, device="cuda", dtype=tdt)
+                for _ in comms]
+        stream = torch.cuda.Stream()
+
+        def step():
+            with gc3.group():
+                for c, x, y in zip(comms, ins, outs):
+                    if cfg["coll"] == "allreduce":
+                        c.all_reduce(x, x, count, cfg["dtype"], "sum", stream)
+                    elif cfg["coll"] == "alltoall":
+                        c.all_to_all(x, y, count, cfg["dtype"], stream)
+                    elif cfg["coll"] == "allgather":
+                        c.all_gather(x, y, count, cfg["dtype"], stream)
+                    else:
+                        c.reduce_scatter(x, y, count, cfg["dtype"], "sum", stream)
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        steps = max(5, min(args.steps, 20))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(steps):
+            step()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        err = comms[0].async_error()
+        if err[0]:
+            raise SystemExit(f"{name} failed: {err[1]}")
+        plan = comms[0].query_plan(cfg["coll"], count, cfg["dtype"])
+        del ins, outs
+        verified = verify_outputs(cfg, comms, count, stream)
+        peaks, _ = load_peaks()
+        busbw = S / (ms * 1e-3) * bus_factor(cfg["coll"], R) / 1e9
+        return {"config": name, "ir": cfg["ir"], "collective": cfg["coll"], "dtype": cfg["dtype"], "bytes_per_rank": S,
+                "protocol": PROTO_NAMES.get(plan["protocol"]), "ms_per_step": round(ms, 5), "value": round(busbw * R, 2),
+                "unit": "GB/s", "hbm_frac": round(plan["hbm_bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
+                "verified": verified}
+    finally:
+        for c in comms:
+            c.destroy()
 
 
 def e2e_run(args, cfg, comms, ins, outs, count, stream, step, barrier, dist):
@@ -385,48 +535,66 @@ def load_traffic(cfg, S, world):
 
 
 # ------------------------------------------------------------------------------------------- CPU
-def cpu_run(cfg, S, R, budget_s, threads=True):
-    """The CPU oracle (restated reference interpreter) on the same IR; returns (GB/s agg, sample, cores)."""
-    import numpy as np
-    from oracle.oracle import FlatIR
-    ir = FlatIR(os.path.join(IR_DIR, cfg["ir"] + ".ir.json"))
-    e = ESIZE[cfg["dtype"]]
-    count = per_rank_count(cfg, S, R)
-    nin, nout, nsc = ir.nchunks
-    ce = count // nin if cfg["coll"] in ("allreduce", "allgather") else count // (nin // R)
-    np_dt = {"float32": np.float32, "bfloat16": np.uint16}[cfg["dtype"]]
-    rng = np.random.default_rng(0)
-    bufs = []
-    for r in range(R):
-        inp = rng.standard_normal(nin * ce).astype(np.float32)
-        if np_dt is np.uint16:
-            inp = (inp.view(np.uint32) >> 16).astype(np.uint16)
-        out = inp if ir.inplace else np.zeros(nout * ce, dtype=np_dt)
-        sc = np.zeros(max(nsc, 1) * ce, dtype=np_dt)
-        bufs.append([inp, out, sc])
-    ntbs = sum(len(g["threadblocks"]) for g in ir.json["gpus"])
-    times, t_start = [], time.time()
-    mode = "threaded" if threads else "deterministic"
-    dt = {"float32": 7, "bfloat16": 9}[cfg["dtype"]]
-    tile = max(1, (256 << 10) // e // max(1, max(o["count"] for g in ir.json["gpus"] for t in g["threadblocks"] for o in t["ops"])))
-    while True:
+class CpuWorkload:
+    """The CPU oracle (restated reference interpreter) on the same IR and sizes: buffers allocated
+    and first-touched once (no page faults inside the timed runs), inputs restored before every
+    run outside the timed region (the in-place reductions would otherwise feed their own output)."""
+
+    def __init__(self, cfg, S, R, threads=True):
+        import numpy as np
+        from oracle.oracle import FlatIR
+        self.cfg, self.S, self.R, self.threads = cfg, S, R, threads
+        self.ir = ir = FlatIR(os.path.join(IR_DIR, cfg["ir"] + ".ir.json"))
+        e = ESIZE[cfg["dtype"]]
+        count = per_rank_count(cfg, S, R)
+        nin, nout, nsc = ir.nchunks
+        self.ce = count // nin if cfg["coll"] in ("allreduce", "allgather") else count // (nin // R)
+        np_dt = {"float32": np.float32, "bfloat16": np.uint16}[cfg["dtype"]]
+        rng = np.random.default_rng(0)
+        self.bufs, self.pristine = [], []
+        for r in range(R):
+            inp = rng.standard_normal(nin * self.ce).astype(np.float32)
+            if np_dt is np.uint16:
+                inp = (inp.view(np.uint32) >> 16).astype(np.uint16)
+            out = inp if ir.inplace else np.zeros(nout * self.ce, dtype=np_dt)
+            sc = np.zeros(max(nsc, 1) * self.ce, dtype=np_dt)
+            self.bufs.append([inp, out, sc])
+            self.pristine.append(inp.copy())
+        self.ntbs = sum(len(g["threadblocks"]) for g in ir.json["gpus"])
+        self.mode = "threaded" if threads else "deterministic"
+        self.dt = {"float32": 7, "bfloat16": 9}[cfg["dtype"]]
+        maxc = max(o["count"] for g in ir.json["gpus"] for t in g["threadblocks"] for o in t["ops"])
+        self.tile = max(1, (256 << 10) // e // max(1, maxc))
+        self.cores = min(self.ntbs, os.cpu_count() or 1) if threads else 1
+
+    def run(self):
+        """One full run of the IR over all ranks; returns seconds (inputs restored first, untimed)."""
+        import numpy as np
+        for b, p in zip(self.bufs, self.pristine):
+            np.copyto(b[0], p)
         t0 = time.perf_counter()
-        rc, err = ir.run(bufs, ce, dt, "sum", mode=mode, slots=2, tile_elems=tile)
-        times.append(time.perf_counter() - t0)
+        rc, err = self.ir.run(self.bufs, self.ce, self.dt, "sum", mode=self.mode, slots=2, tile_elems=self.tile)
+        t = time.perf_counter() - t0
         if rc != 0:
             raise RuntimeError(err)
-        if time.time() - t_start > budget_s or len(times) >= 20:
-            break
-    t = sum(times) / len(times)
-    agg = S / t * bus_factor(cfg["coll"], R) / 1e9 * R
-    cores = min(ntbs, os.cpu_count() or 1) if threads else 1
-    sample = f"{len(times)} full runs of {cfg['ir']} ({R} ranks x {S >> 20} MiB), oracle {mode} mode, {ntbs} threads"
-    return agg, sample, cores, t
+        return t
+
+    def gbs(self, t):
+        return self.S / t * bus_factor(self.cfg["coll"], self.R) / 1e9 * self.R
+
+    def sample(self, n):
+        return (f"{n} full runs of {self.cfg['ir']} ({self.R} ranks x {self.S >> 20} MiB, buffers allocated and touched once), "
+                f"oracle {self.mode} mode, {self.ntbs} threads")
 
 
 def cpu_baseline(cfg, S, R, budget_s=10.0):
-    agg, sample, cores, _ = cpu_run(cfg, S, R, budget_s)
-    return {"value": round(agg, 3), "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample,
+    w = CpuWorkload(cfg, S, R)
+    w.run()  # warm: page-in, thread creation paths
+    times, t_start = [], time.time()
+    while time.time() - t_start < budget_s and len(times) < 20:
+        times.append(w.run())
+    t = sum(times) / len(times)
+    return {"value": round(w.gbs(t), 3), "unit": "GB/s", "cores": w.cores, "kind": "port", "sample": w.sample(len(times)),
             "host_cpu": host_cpu()}
 
 
@@ -441,11 +609,42 @@ def host_cpu():
     return f"{os.cpu_count()} logical cpus"
 
 
+def verify_int_sum(cfg, comms, nbytes, stream):
+    """Parity property for reductions too large for the oracle: int32 data (wrapping sum: the
+    association does not matter) must equal the torch sum exactly."""
+    import torch
+    from paper_2201_11840_b200 import gc3
+    R = comms[0].nranks
+    icfg = dict(cfg, dtype="int32")
+    count = per_rank_count(icfg, nbytes, R)
+    n_in = input_elems(cfg["coll"], count, R)
+    g = torch.Generator(device="cuda").manual_seed(7)
+    ins = [torch.randint(-2 ** 20, 2 ** 20, (n_in,), device="cuda", dtype=torch.int32, generator=g) for _ in comms]
+    want = torch.stack(ins).sum(0, dtype=torch.int64).to(torch.int32)
+    outs = [torch.empty(count, device="cuda", dtype=torch.int32) for _ in comms]
+    with gc3.group():
+        for c, x, y in zip(comms, ins, outs):
+            if cfg["coll"] == "allreduce":
+                c.all_reduce(x, y, count, "int32", "sum", stream)
+            else:
+                c.reduce_scatter(x, y, count, "int32", "sum", stream)
+    torch.cuda.synchronize()
+    if comms[0].async_error()[0]:
+        raise SystemExit("verification run failed")
+    for c, y in zip(comms, outs):
+        w = want if cfg["coll"] == "allreduce" else want[c.rank * count:(c.rank + 1) * count]
+        if not torch.equal(y, w):
+            raise SystemExit(f"verification failed: rank {c.rank} int32 sum differs")
+    return True
+
+
 def run_sweep(args, cfg):
-    """Message-size sweep (BASELINE config C4: 1 KiB - 1 GiB, Simple vs LL): one JSON line per
+    """Message-size sweep (BASELINE configs C4 / C5: 1 KiB - 1 GiB per protocol): one JSON line per
     (protocol, size) with the device time of one collective (CUDA events, mean of the timed steps,
     inputs re-used: small sizes are L2-resident), algBW / busBW per rank and the HBM roofline
-    fraction of the launch's algorithmic bytes."""
+    fraction of the launch's algorithmic bytes. Every point is verified before it is printed:
+    permutations exactly, reductions against the oracle up to 64 MiB per rank and by an exact int32
+    sum above."""
     import torch
     from paper_2201_11840_b200 import gc3
     torch.cuda.set_device(0)
@@ -466,6 +665,10 @@ def run_sweep(args, cfg):
         for nbytes in sizes:
             count = per_rank_count(cfg, nbytes, R)
             n_in = input_elems(cfg["coll"], count, R)
+            if cfg["coll"] in ("alltoall", "allgather") or nbytes <= (64 << 20):
+                verified = verify_outputs(cfg, comms, count, stream)
+            else:
+                verified = verify_int_sum(cfg, comms, nbytes, stream)
             ins = [torch.randn(n_in, device="cuda").to(tdt) for _ in comms]
             outs = [torch.empty(R * count if cfg["coll"] in ("allgather", "alltoall") else count, device="cuda", dtype=tdt)
                     for _ in comms]
@@ -492,47 +695,101 @@ def run_sweep(args, cfg):
             e1.record(stream)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / steps
+            graph_us = graph_time_us(step, stream) if args.graph and nbytes <= args.graph_max else None
             err = comms[0].async_error()
             plan = comms[0].query_plan(cfg["coll"], count, cfg["dtype"])
             print(json.dumps({"config": args.config, "ir": cfg["ir"], "ranks": R, "proto": proto, "bytes": nbytes, "us": round(ms * 1e3, 2),
+                              "graph_us": graph_us,
                               "algbw_gbs": round(nbytes / (ms * 1e-3) / 1e9, 2),
                               "busbw_gbs": round(nbytes / (ms * 1e-3) / 1e9 * bus_factor(cfg["coll"], R), 2),
                               "hbm_frac": round(plan["hbm_bytes"] / (ms * 1e-3) / 1e9 / peaks["hbm_gbs"], 4),
-                              "lanes": plan["lanes"], "tile": plan["tile_elems"] * ESIZE[cfg["dtype"]], "ok": err[0] == 0}),
+                              "ran": PROTO_NAMES.get(plan["protocol"]), "lanes": plan["lanes"],
+                              "tile": plan["tile_elems"] * ESIZE[cfg["dtype"]], "ok": err[0] == 0, "verified": verified}),
                   flush=True)
             del ins, outs
     for c in comms:
         c.destroy()
 
 
+def graph_time_us(step, stream, reps=20):
+    """Per-collective device time with `reps` collectives captured in one CUDA graph (launch cost
+    amortised: the small-message floor without host enqueue overhead)."""
+    import torch
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        step()  # warm on the capture stream
+        stream.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            for _ in range(reps):
+                step()
+    g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    with torch.cuda.stream(stream):
+        for _ in range(5):
+            g.replay()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    return round(e0.elapsed_time(e1) * 1e3 / (5 * reps), 2)
+
+
 def run_reference(args, cfg):
     """The reference arm: the reference's interpreter semantics on the host cores (oracle port;
-    the reference ships no runtime)."""
+    the reference ships no runtime), with warm buffers like the gc3 arm's
+    cpu_baseline: W untimed runs, then K timed runs of the whole workload."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     S = args.bytes or cfg["bytes"]
-    R = 8
-    times = []
+    R = ir_ranks(cfg)
+    w = CpuWorkload(cfg, S, R)
     for _ in range(args.warmup):
-        cpu_run(cfg, S, R, budget_s=0.0)
-    for _ in range(args.steps):
-        agg, sample, cores, t = cpu_run(cfg, S, R, budget_s=0.0)
-        times.append(t)
+        w.run()
+    times = [w.run() for _ in range(args.steps)]
     t = sum(times) / len(times)
-    agg = S / t * bus_factor(cfg["coll"], R) / 1e9 * R
+    agg = w.gbs(t)
     out = {
         "metric": METRIC, "value": round(agg, 3), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": {"float32": "f32", "bfloat16": "bf16"}.get(cfg["dtype"]), "data": "synthetic",
-        "config": {"workload": cfg["desc"], "ir": cfg["ir"], "collective": cfg["coll"], "ranks": R,
-                   "bytes_per_rank": S},
+        "vs_baseline": None, "dtype": {"float32": "f32", "bfloat16": "bf16"}.get(cfg["dtype"]),
+        "data": "synthetic (seeded N(0,1))",
+        "config": workload_config(cfg, S, R, world),
         "impl": "reference",
-        "cpu_baseline": {"value": round(agg, 3), "unit": "GB/s", "cores": cores, "kind": "port",
-                         "sample": f"each step: {sample}", "host_cpu": host_cpu()},
+        "cpu_baseline": {"value": round(agg, 3), "unit": "GB/s", "cores": w.cores, "kind": "port",
+                         "sample": f"each step: {w.sample(1)}", "host_cpu": host_cpu()},
         "e2e": {"value": round(agg, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out), flush=True)
+
+
+def enforce_world(args):
+    """--gpus N means N processes, one per GPU: under torchrun WORLD_SIZE must be N; without it the
+    bench re-executes itself under torch.distributed.run. Never a silent loopback fallback."""
+    rank, world, _ = dist_env()
+    if args.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if "WORLD_SIZE" in os.environ:
+        if world != args.gpus:
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    elif args.gpus > 1:
+        if args.impl == "gc3":
+            import torch
+            n = torch.cuda.device_count()
+            if n < args.gpus:
+                raise SystemExit(f"--gpus {args.gpus}: only {n} GPU(s) visible")
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        os.execvp(sys.executable, [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+                                   "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:])
+    if args.impl == "gc3" and world > 1:
+        import torch
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"WORLD_SIZE={world} but only {torch.cuda.device_count()} GPU(s) visible")
+        if 8 % world:
+            raise SystemExit(f"--gpus {world} must divide the 8 IR ranks")
 
 
 def main():
@@ -549,13 +806,19 @@ def main():
     ap.add_argument("--instances", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--more", default="c3,c4", help="other configurations timed (device only) and verified at N=1")
+    ap.add_argument("--no-more", action="store_true")
     ap.add_argument("--quick", action="store_true", help="kernel timing only: one compact JSON line")
     ap.add_argument("--sweep", action="store_true", help="message-size sweep (one JSON line per protocol and size)")
     ap.add_argument("--sweep-min", type=int, default=1 << 10)
     ap.add_argument("--sweep-max", type=int, default=1 << 30)
-    ap.add_argument("--sweep-protos", default="simple,ll")
+    ap.add_argument("--sweep-protos", default="simple,ll,ll128")
+    ap.add_argument("--graph", action="store_true", help="sweep: also time collectives captured in a CUDA graph")
+    ap.add_argument("--graph-max", type=int, default=8 << 20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if not args.sweep:
+        enforce_world(args)
     cfg = dict(CONFIGS[args.config])
     if args.proto:
         cfg["proto"] = args.proto

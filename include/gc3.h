@@ -111,12 +111,12 @@ ncclResult_t ncclGroupEnd(void);
  * a 1 x nranks topology with the B200 budget (148 thread blocks), staged in device memory, and its
  * FIFOs are exchanged with the peers. *ir_id receives the registration index. */
 ncclResult_t gc3RegisterIR(ncclComm_t comm, const char* path_or_json, int instances, int* ir_id);
-/* proto: -1 = as tagged in the IR, 0 = simple, 1 = ll, 2 = ll128 (runs with the simple transport) */
+/* proto: -1 = as tagged in the IR, 0 = simple, 1 = ll (16-byte lines, 8 payload bytes), 2 = ll128 (128-byte lines, 120 payload bytes) */
 ncclResult_t gc3SetProtocolOverride(ncclComm_t comm, int ir_id, int proto);
 
 typedef struct {
   int ir_id;          /* selected IR, -1 if none matches */
-  int protocol;       /* effective protocol: 0 simple, 1 ll */
+  int protocol;       /* effective protocol: 0 simple, 1 ll, 2 ll128 */
   int lanes;          /* CUDA blocks per IR thread block */
   int grid;           /* CUDA blocks in the launch on this rank's device */
   int local_ranks;    /* ranks executed by that launch */

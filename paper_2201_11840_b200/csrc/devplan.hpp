@@ -74,14 +74,17 @@ struct DevTb {
   int32_t recv_slot;  // rank slot of the receive peer when it runs in the same launch, else -1
 };
 
-// One side of one connection for one lane.  The FIFO and `head` live in the receiver's memory,
-// `tail` in the sender's memory (NVLink buffers on the receiving GPU).
+// One side of one connection for one lane.  The FIFOs and `head` live in the receiver's memory,
+// `tail` in the sender's memory (NVLink buffers on the receiving GPU). Every
+// protocol has its own slots (NCCL keeps per-protocol buffers for the same reason): a line protocol
+// validates a slot by flags embedded in the data, so it must never see another protocol's payload.
+enum : int { kProtoSimple = 0, kProtoLL = 1, kProtoLL128 = 2, kNumProtos = 3 };
 struct DevChan {
-  char* fifo;          // slots x slot_bytes
-  uint64_t* head;      // messages posted (written by the sender)
-  uint64_t* tail;      // messages consumed (written by the receiver)
-  uint64_t* mine;      // this side's persistent message counter
-  int64_t slot_bytes;  // bytes of one slot: tile unit x the connection's largest count
+  char* fifo[kNumProtos];            // per protocol: slots x slot_bytes[p]
+  uint64_t* head;                    // messages posted (written by the sender; Simple only)
+  uint64_t* tail;                    // messages consumed (written by the receiver)
+  uint64_t* mine;                    // this side's persistent message counter
+  int64_t slot_bytes[kNumProtos];    // bytes of one slot: tile unit x the connection's largest count
 };
 
 struct LaunchArgs {

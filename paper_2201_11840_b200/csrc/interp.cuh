@@ -703,6 +703,125 @@ __device__ bool ll_op(int opcode, int count, char* src0, const char* srcr0, char
   return true;
 }
 
+// ------------------------------------------------------------------ LL128 op body
+// LL128 (NCCL's 128-byte-line protocol): a message travels as 128-byte lines of
+// 15 payload words (8 bytes each) and one 8-byte flag word, the 64-bit message sequence number.
+// Eight consecutive threads of a warp own one line and write it with one 16-byte store each (the
+// eighth thread carries the flag in its upper half), so a warp-wide store puts whole lines in one
+// memory transaction; a receiver whose eight threads load the line together and see the flag has
+// the whole payload. Lines whose flag does not match yet are re-loaded by their eight threads
+// together. 120 of every 128 bytes are payload (LL: 8 of 16); no fences on the data path.
+// Line k of the message is segment k / lps, payload words (k % lps) * 15 ... + 14 of that segment.
+#ifndef GC3_LL128_BATCH  // lines in flight per 8-thread group
+#define GC3_LL128_BATCH 2
+#endif
+constexpr int kLL128Words = 15;
+__device__ __forceinline__ uint64_t ll128_flag(const uint4& v) { return (static_cast<uint64_t>(v.w) << 32) | v.z; }
+
+template <class R>
+__device__ bool ll128_op(int opcode, int count, char* src0, const char* srcr0, char* dst0, int64_t chunk_bytes, int64_t tbytes,
+                         const uint4* inl, uint4* outl, uint64_t in_flag, uint64_t out_flag, bool sys, const Ctx& c, int t, int n) {
+  constexpr int U = GC3_LL128_BATCH;
+  const int64_t words = tbytes >> 3;
+  const int64_t lps = (words + kLL128Words - 1) / kLL128Words;
+  const int64_t nlines = lps * count;
+  const bool send = is_send(opcode);
+  // ops that read their local span: send, rrc, rrcs, rrs, and rcs whose message is already in place
+  const bool reads_src = opcode == kOpSend || opcode == kOpRrc || opcode == kOpRrcs || opcode == kOpRrs || (opcode == kOpRcs && !inl);
+  const int lt = t & 31, g = lt >> 3, j8 = lt & 7;
+  const int w = t >> 5, nw = n >> 5;
+  const bool flag_thread = j8 == 7;
+  const int mywords = flag_thread ? 1 : 2;  // payload words of this thread in its line
+  const int64_t step = static_cast<int64_t>(nw) * 4 * U;
+  for (int64_t kb = static_cast<int64_t>(w) * 4 * U; kb < nlines; kb += step) {
+    uint4 l[U];
+    uint2 own[U][2];
+    int64_t off[U];
+    int nv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t k = kb + u * 4 + g;  // a warp covers 4 consecutive lines per u: 512 contiguous bytes
+      nv[u] = -1;
+      off[u] = 0;
+      if (k >= nlines) continue;
+      const int64_t seg = k / lps, line = k - seg * lps;
+      const int64_t wi = line * kLL128Words + 2 * j8;
+      const int64_t left = words - wi;
+      nv[u] = left <= 0 ? 0 : (left < mywords ? static_cast<int>(left) : mywords);
+      off[u] = seg * chunk_bytes + wi * 8;
+      if (inl) l[u] = ld_line(inl + k * 8 + j8, sys);
+      if (reads_src) {
+        const char* s = (opcode == kOpRcs ? src0 : srcr0) + off[u];
+        if (nv[u] > 0) own[u][0] = ld_cg8(s);
+        if (nv[u] > 1) own[u][1] = ld_cg8(s + 8);
+      }
+    }
+    if (inl) {
+      const uint64_t start = globaltimer();
+      for (int it = 0;; ++it) {
+        bool bad[U], any = false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          bad[u] = nv[u] >= 0 && flag_thread && ll128_flag(l[u]) != in_flag;
+          any = any || bad[u];
+        }
+        if (!__any_sync(0xffffffffu, any)) break;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          // the line's eight threads re-load it together (one transaction)
+          if (__shfl_sync(0xffffffffu, bad[u], lt | 7)) l[u] = ld_line(inl + (kb + u * 4 + g) * 8 + j8, sys);
+        }
+        if ((it & 255) == 255) {
+          if (*reinterpret_cast<volatile int*>(c.abort_flag)) return false;
+          if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
+            raise_timeout(c, 4);
+            return false;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (nv[u] < 0) continue;  // the whole 8-thread group is past the end
+      const uint2 msg[2] = {make_uint2(l[u].x, l[u].y), make_uint2(l[u].z, l[u].w)};
+      char* src = src0 + off[u];
+      char* dst = dst0 + off[u];
+      uint2 v[2] = {make_uint2(0, 0), make_uint2(0, 0)};
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        if (i >= nv[u]) break;
+        switch (opcode) {
+          case kOpSend: v[i] = own[u][i]; break;
+          case kOpRecv:
+            if (inl) st_vec8(dst + 8 * i, msg[i]);
+            break;
+          case kOpRrc: st_vec8(dst + 8 * i, R::template vec<uint2>(own[u][i], msg[i])); break;
+          case kOpRcs:
+            if (inl) {
+              v[i] = msg[i];
+              st_vec8(src + 8 * i, v[i]);
+            } else {
+              v[i] = own[u][i];
+            }
+            break;
+          case kOpRrcs:
+            v[i] = R::template vec<uint2>(own[u][i], msg[i]);
+            st_vec8(src + 8 * i, v[i]);
+            break;
+          case kOpRrs: v[i] = R::template vec<uint2>(own[u][i], msg[i]); break;
+          default: break;
+        }
+      }
+      if (send && outl) {
+        const uint4 line = flag_thread ? make_uint4(v[0].x, v[0].y, static_cast<uint32_t>(out_flag), static_cast<uint32_t>(out_flag >> 32))
+                                       : make_uint4(v[0].x, v[0].y, v[1].x, v[1].y);
+        st_line(outl + (kb + u * 4 + g) * 8 + j8, line, sys);
+      }
+    }
+  }
+  return true;
+}
+
 // The data movement of one op on one tile (Simple transports): staged reductions, bulk copies or
 // the register path. `in` is the incoming message (FIFO slot or pulled span; segment j at
 // + j * in_stride; null when already in place or absent), `out` the outgoing one (FIFO slot or the
@@ -919,7 +1038,7 @@ __device__ GC3_WQ_ATTR void interp_wq(const WqArgs a, char* const* s_bufs, Tma& 
   }
 }
 
-template <class R, bool LL>
+template <class R, int P>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
   // every rank's buffers of this launch, staged in shared memory once: ops index them by rank slot
   // and buffer id (a dynamically indexed kernel parameter would be copied to local memory)
@@ -1020,7 +1139,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       const bool in_d = (tr & kInDirect) != 0, out_d = (tr & kOutDirect) != 0;
       const bool in_p = (tr & kInPull) != 0, out_p = (tr & kOutPull) != 0;
       const bool in_fifo = recv && !in_d && !in_p, out_fifo = send && !out_d && !out_p;
-      const bool ll_in = LL && in_fifo, ll_out = LL && out_fifo;
+      const bool ll_in = P != kProtoSimple && in_fifo, ll_out = P != kProtoSimple && out_fifo;
       c.step = s;
       if (t == 0) stamp(q, 0);
       // (1) preconditions, polled in parallel
@@ -1056,19 +1175,22 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
       const char* dstr = mine[op.dst_rbuf] + op.dst_off * chunk_bytes + t0_bytes;
       const char* in = nullptr;
       int64_t in_stride = tbytes;
-      if (in_fifo) in = cin->fifo + static_cast<int64_t>(rcvd % slots) * cin->slot_bytes;
+      if (in_fifo) in = cin->fifo[P] + static_cast<int64_t>(rcvd % slots) * cin->slot_bytes[P];
       if (in_p) {
         in = rpeer[op.in_buf] + op.in_off * chunk_bytes + t0_bytes;
         in_stride = chunk_bytes;
       }
       char* out = nullptr;
       int64_t out_stride = tbytes;
-      if (out_fifo) out = cout->fifo + static_cast<int64_t>(sent % slots) * cout->slot_bytes;
+      if (out_fifo) out = cout->fifo[P] + static_cast<int64_t>(sent % slots) * cout->slot_bytes[P];
       if (out_d) {
         out = peer[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes;
         out_stride = chunk_bytes;
       }
-      if (ll_in || ll_out) {
+      if ((ll_in || ll_out) && P == kProtoLL128) {
+        ok = ll128_op<R>(op.opcode, op.count, src, srcr, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
+                         ll_out ? reinterpret_cast<uint4*>(out) : nullptr, rcvd + 1, sent + 1, sys, c, t, n);
+      } else if (ll_in || ll_out) {
         ok = ll_op<R>(op.opcode, op.count, src, srcr, dst, chunk_bytes, tbytes, ll_in ? reinterpret_cast<const uint4*>(in) : nullptr,
                       in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
                       static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);

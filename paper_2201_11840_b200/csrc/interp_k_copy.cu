@@ -5,7 +5,11 @@ namespace gc3 {
 
 using KernelFn = void (*)(LaunchArgs);
 
-KernelFn interp_kernel_copy(bool ll) { return ll ? dev::interp<dev::RedNone, true> : dev::interp<dev::RedNone, false>; }
+KernelFn interp_kernel_copy(int proto) {
+  return proto == kProtoLL128 ? dev::interp<dev::RedNone, kProtoLL128>
+         : proto == kProtoLL  ? dev::interp<dev::RedNone, kProtoLL>
+                              : dev::interp<dev::RedNone, kProtoSimple>;
+}
 KernelFn interp_kernel_copy_wq() { return dev::interp_wq_kernel<dev::RedNone>; }
 
 }  // namespace gc3

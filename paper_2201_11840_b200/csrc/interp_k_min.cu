@@ -6,11 +6,11 @@ namespace gc3 {
 using KernelFn = void (*)(LaunchArgs);
 
 template <class R>
-static KernelFn pick(bool ll) {
-  return ll ? dev::interp<R, true> : dev::interp<R, false>;
+static KernelFn pick(int proto) {
+  return proto == kProtoLL128 ? dev::interp<R, kProtoLL128> : proto == kProtoLL ? dev::interp<R, kProtoLL> : dev::interp<R, kProtoSimple>;
 }
 
-KernelFn interp_kernel_min(int dtype, bool ll) {
+KernelFn interp_kernel_min(int dtype, int ll) {
   constexpr int OP = dev::kMin;
   switch (dtype) {
     case 0: return pick<dev::RedInt<int8_t, OP>>(ll);

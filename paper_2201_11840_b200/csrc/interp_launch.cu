@@ -11,19 +11,19 @@
 namespace gc3 {
 
 using KernelFn = void (*)(LaunchArgs);
-KernelFn interp_kernel_copy(bool ll);
+KernelFn interp_kernel_copy(int proto);
 KernelFn interp_kernel_copy_wq();
-KernelFn interp_kernel_sum(int dtype, bool ll);
-KernelFn interp_kernel_prod(int dtype, bool ll);
-KernelFn interp_kernel_max(int dtype, bool ll);
-KernelFn interp_kernel_min(int dtype, bool ll);
+KernelFn interp_kernel_sum(int dtype, int proto);
+KernelFn interp_kernel_prod(int dtype, int proto);
+KernelFn interp_kernel_max(int dtype, int proto);
+KernelFn interp_kernel_min(int dtype, int proto);
 
 constexpr int kMaxDynamicSmem = 220 << 10;  // TMA staging budget per block (runtime smem_kb <= 220)
 
 KernelFn interp_kernel_wq(int redop) { return redop == -1 ? interp_kernel_copy_wq() : nullptr; }
 
-// dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs.
-KernelFn interp_kernel(int dtype, int redop, bool ll) {
+// dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs; ll: kProtoSimple / kProtoLL / kProtoLL128.
+KernelFn interp_kernel(int dtype, int redop, int ll) {
   switch (redop) {
     case -1: return interp_kernel_copy(ll);
     case 0: return interp_kernel_sum(dtype, ll);

@@ -45,7 +45,7 @@
 namespace gc3 {
 
 using KernelFn = void (*)(LaunchArgs);
-KernelFn interp_kernel(int dtype, int redop, bool ll);
+KernelFn interp_kernel(int dtype, int redop, int proto);
 KernelFn interp_kernel_wq(int redop);  // work-queue kernel (copy-only programs), nullptr otherwise
 cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, size_t smem, cudaStream_t stream);
 int interp_blocks_per_sm(KernelFn fn, size_t smem);
@@ -112,6 +112,7 @@ struct Config {
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
   int64_t ll_max_bytes = 512 << 10;  // Simple IRs run LL up to this many bytes per rank (0: never;
                                      // measured: LL ~2x faster than Simple below ~1 MiB, BASELINE §5.2)
+  int64_t ll128_max_bytes = 0;       // ... and LL128 above ll_max_bytes up to this many (0: never)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
   int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
   int select = 0;                    // among matching IRs pick the lowest timed-model prediction
@@ -143,6 +144,7 @@ Config config_from_env() {
   c.wq = static_cast<int>(env_int("GC3_WQ", c.wq));
   c.tma_min = env_int("GC3_TMA_MIN", c.tma_min);
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
+  c.ll128_max_bytes = env_int("GC3_LL128_MAX_BYTES", c.ll128_max_bytes);
   c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
   c.smem_kb = env_int("GC3_SMEM_KB", c.smem_kb);
   c.select = static_cast<int>(env_int("GC3_SELECT", c.select));
@@ -215,18 +217,25 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct ArenaLayout {
   std::vector<int> in_index, out_index;  // per tb: index among receiving / sending tbs, or -1
-  std::vector<size_t> fifo_off;          // per receiving tb: offset of its FIFOs (lanes x slots)
-  std::vector<int64_t> slot_stride;      // per receiving tb: bytes of one slot = unit x max count
+  std::vector<size_t> fifo_off[kNumProtos];      // per protocol, per receiving tb: offset of its FIFOs (lanes x slots)
+  std::vector<int64_t> slot_stride[kNumProtos];  // per protocol, per receiving tb: bytes of one slot = unit x max count
   std::vector<int> in_lane_base;         // per receiving tb: index of its first lane's head / counter
   std::vector<int> out_lane_base;        // per sending tb: index of its first lane's tail / counter
   int n_in = 0, n_out = 0;
   size_t off_head = 0, off_tail = 0, off_mine_in = 0, off_mine_out = 0, bytes = 0;
 };
 
+// Slot unit (bytes of one tile's message) per protocol for a Simple unit of `unit` bytes: Simple
+// and LL128 slots hold `unit` bytes (LL128: unit / 128 lines of 120 payload bytes), LL slots hold
+// unit / 2 bytes of 16-byte lines (unit / 4 payload bytes: LL is for small messages).
+int64_t proto_unit(int proto, int64_t unit) { return proto == kProtoLL ? std::max<int64_t>(unit / 2 / 256 * 256, 256) : unit; }
+
 // FIFO slots are sized per connection: one slot holds a message of `count` tiles, each at most
 // `unit` bytes, so the tile size does not shrink with the aggregation count.
-// Thread block t of `rank` runs lanes x mult[rank][t] lanes (work balance, see lane_multipliers);
-// `lane_base` gives each receiving / sending thread block's first lane in the counter arrays.
+// Every protocol has its own slots (a line protocol must never read another protocol's payload as
+// flags). Thread block t of `rank` runs lanes x mult[rank][t] lanes (work balance, see
+// lane_multipliers); `lane_base` gives each receiving / sending thread block's first lane in the
+// counter arrays.
 ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_t unit, const std::vector<std::vector<int>>& mult) {
   ArenaLayout a;
   const Gpu& g = p.gpus[rank];
@@ -241,11 +250,14 @@ ArenaLayout make_layout(const Program& p, int rank, int lanes, int slots, int64_
       int maxc = 1;
       for (const Op& op : g.tbs[t].ops)
         if (op_receives(op.op)) maxc = std::max(maxc, op.count);
-      a.fifo_off.push_back(off);
-      a.slot_stride.push_back(unit * maxc);
+      for (int pr = 0; pr < kNumProtos; ++pr) {
+        const int64_t u = proto_unit(pr, unit);
+        a.fifo_off[pr].push_back(off);
+        a.slot_stride[pr].push_back(u * maxc);
+        off += static_cast<size_t>(lt) * slots * u * maxc;
+      }
       a.in_lane_base.push_back(in_lanes);
       in_lanes += lt;
-      off += static_cast<size_t>(lt) * slots * unit * maxc;
     }
     if (g.tbs[t].send_peer >= 0) {
       a.out_index[t] = a.n_out++;
@@ -321,6 +333,12 @@ struct DeviceState {
   uint64_t* d_prog = nullptr;    // work-queue progress table
   size_t prog_bytes = 0;
   int trace_grid = 0, trace_ops = 0, trace_lanes = 0;
+  // every launch of this device waits for the previous one: launches share FIFO counters, scratch,
+  // work buffers and the work-queue tables, so collectives issued on different streams must not
+  // overlap (NCCL orders a communicator's kernels the same way)
+  cudaEvent_t last_done = nullptr;
+  cudaStream_t last_stream = nullptr;
+  bool has_last = false;
 };
 
 struct Clique {
@@ -1108,6 +1126,15 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         o.src_rbuf = plan.source_complete && (source[r][t][s] & kSrcFromSource) ? kSource : o.src_buf;
         o.dst_rbuf = plan.source_complete && (source[r][t][s] & kDstFromSource) ? kSource : o.dst_buf;
         if (plan.result_complete && result[r][t][s]) o.dst_buf = kResult;  // final owned write -> recvbuff
+        if (plan.result_complete && (o.direct & kOutDirect)) {
+          // a direct message whose receive is a final owned write: the sender stores it straight into
+          // the receiver's result buffer (the receive itself moves nothing)
+          const auto rcv = receiver_of.find({r, static_cast<int>(t), static_cast<int>(s)});
+          if (rcv != receiver_of.end()) {
+            const auto [rr, rt, rs] = rcv->second;
+            if (result[rr][rt][rs]) o.dst_buf = kResult;
+          }
+        }
         o.has_dep = op.has_dep ? 1 : 0;
         o.src_off = op.src_off;
         o.dst_off = op.dst_off;
@@ -1156,8 +1183,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         d.chan_in = static_cast<int>(chans.size());
         for (int l = 0; l < Lt; ++l) {
           DevChan ch{};
-          ch.fifo = ir.arena + ir.lay.fifo_off[k] + static_cast<size_t>(l) * ir.slots * ir.lay.slot_stride[k];
-          ch.slot_bytes = ir.lay.slot_stride[k];
+          for (int pr = 0; pr < kNumProtos; ++pr) {
+            ch.fifo[pr] = ir.arena + ir.lay.fifo_off[pr][k] + static_cast<size_t>(l) * ir.slots * ir.lay.slot_stride[pr][k];
+            ch.slot_bytes[pr] = ir.lay.slot_stride[pr][k];
+          }
           ch.head = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_head + (kb + l) * kCounterStride);
           ch.tail = reinterpret_cast<uint64_t*>(sender_arena + slay.off_tail + (mb + l) * kCounterStride);
           ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_in + (kb + l) * 8);
@@ -1178,8 +1207,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         d.chan_out = static_cast<int>(chans.size());
         for (int l = 0; l < Lt; ++l) {
           DevChan ch{};
-          ch.fifo = recv_arena + rlay.fifo_off[k] + static_cast<size_t>(l) * ir.slots * rlay.slot_stride[k];
-          ch.slot_bytes = rlay.slot_stride[k];
+          for (int pr = 0; pr < kNumProtos; ++pr) {
+            ch.fifo[pr] = recv_arena + rlay.fifo_off[pr][k] + static_cast<size_t>(l) * ir.slots * rlay.slot_stride[pr][k];
+            ch.slot_bytes[pr] = rlay.slot_stride[pr][k];
+          }
           ch.head = reinterpret_cast<uint64_t*>(recv_arena + rlay.off_head + (kb + l) * kCounterStride);
           ch.tail = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_tail + (mb + l) * kCounterStride);
           ch.mine = reinterpret_cast<uint64_t*>(ir.arena + ir.lay.off_mine_out + (mb + l) * 8);
@@ -1464,7 +1495,8 @@ bool order_is_deadlock_free(const Program& p, const std::vector<std::vector<std:
 
 struct CallPlan {
   int id = -1;
-  bool ll = false;
+  bool ll = false;  // a line protocol (LL or LL128): every message through the FIFO lines
+  int proto = kProtoSimple;
   int lanes = 1;
   int grid = 0;
   int unit_warps = 4;
@@ -1501,20 +1533,26 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   // protocol: the override, else the IR's tag; a Simple IR runs LL for messages up to ll_max_bytes
   // per rank (no fences on the data path: measured ~2x lower latency below ~1 MiB)
   int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
-  if (ir.proto_override < 0 && proto == 0 && c->cfg.ll_max_bytes > 0 &&
-      selection_bytes(coll, count, esize, c->nranks) <= static_cast<uint64_t>(c->cfg.ll_max_bytes))
-    proto = 1;
-  cp.ll = proto == 1 && chunk_bytes % 8 == 0;
+  if (ir.proto_override < 0 && proto == kProtoSimple) {
+    const uint64_t sb = selection_bytes(coll, count, esize, c->nranks);
+    if (c->cfg.ll_max_bytes > 0 && sb <= static_cast<uint64_t>(c->cfg.ll_max_bytes)) proto = kProtoLL;
+    else if (c->cfg.ll128_max_bytes > 0 && sb <= static_cast<uint64_t>(c->cfg.ll128_max_bytes)) proto = kProtoLL128;
+  }
+  // line protocols move 8-byte words: chunks of other sizes run Simple
+  cp.proto = proto != kProtoSimple && chunk_bytes % 8 == 0 ? proto : kProtoSimple;
+  cp.ll = cp.proto != kProtoSimple;
   // an LL launch sends every message through lane-matched FIFOs: with per-connection lane counts
   // (lane_mask) it runs every thread block on the base lanes instead
   int ntbs_local = 0;
   for (int r = 0; r < c->nranks; ++r)
     if (c->clique->local[r] && c->clique->local[r]->device == ds.device) ntbs_local += static_cast<int>(p.gpus[r].tbs.size());
   cp.uniform = cp.ll && ir.lane_mask != 0;
-  const int64_t cap_bytes = cp.ll ? ir.slot_bytes / 2 : ir.slot_bytes;  // per tile (slots scale with count)
+  // payload bytes of one tile that fit the protocol's slot unit (slots scale with count)
+  const int64_t unit = proto_unit(cp.proto, ir.slot_bytes);
+  const int64_t cap_bytes = cp.proto == kProtoLL ? unit / 2 : cp.proto == kProtoLL128 ? unit / 128 * 120 : unit;
   int64_t tile_bytes_cap = cap_bytes / 16 * 16;
   if (tile_bytes_cap < 16) return set_error(ncclInvalidUsage, "FIFO slot unit too small");
-  cp.fn = interp_kernel(cp.redop < 0 ? 0 : dtype, cp.redop, cp.ll);
+  cp.fn = interp_kernel(cp.redop < 0 ? 0 : dtype, cp.redop, cp.proto);
   if (!cp.fn) return set_error(ncclInvalidArgument, "no kernel for dtype %d op %d", dtype, redop);
   auto occupancy = [&](size_t smem) {
     auto f = ds.occupancy.find({cp.fn, smem});
@@ -1700,6 +1738,12 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     if (q->comm->async_error != ncclSuccess) return set_error(q->comm->async_error, "communicator is in an error state");
   }
   if (p0.count == 0) return ncclSuccess;
+  if (ds->h_err && reinterpret_cast<volatile uint64_t*>(ds->h_err)[0]) {
+    // a previous launch on this device hit the watchdog: its abort flag is still raised, so a new
+    // launch would exit early and leave recvbuff unwritten; fail the call instead
+    for (Pending* q : ops) q->comm->async_error = ncclSystemError;
+    return set_error(ncclSystemError, "a previous collective on device %d timed out (watchdog); abort the communicator", dev);
+  }
   const int id = select_ir(c0, p0.coll, p0.count, p0.dtype);
   if (id < 0)
     return set_error(ncclInvalidUsage, "no registered %s IR matches %zu elements of type %d (no NCCL fallback on this path)",
@@ -1795,6 +1839,12 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     CUDA_TRY(cudaStreamWaitEvent(stream, ev, 0));
     CUDA_TRY(cudaEventDestroy(ev));
   }
+  // serialise with the previous launch of this device when it went to another stream (same stream:
+  // stream order suffices). Under stream capture the graph's own edges order the launches.
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  CUDA_TRY(cudaStreamIsCapturing(stream, &cap));
+  const bool capturing = cap != cudaStreamCaptureStatusNone;
+  if (!capturing && ds->has_last && ds->last_stream != stream) CUDA_TRY(cudaStreamWaitEvent(stream, ds->last_done, 0));
   for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
     const int r = plan.ranks[slot];
     Pending* q = nullptr;
@@ -1916,6 +1966,12 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   CUDA_TRY(interp_launch(cp.fn, a, cp.grid, cp.smem, stream));
   for (const PostCopy& pc : post)
     CUDA_TRY(cudaMemcpy2DAsync(pc.dst, pc.dpitch, pc.src, pc.spitch, pc.width, pc.rows, cudaMemcpyDeviceToDevice, stream));
+  if (!capturing) {
+    if (!ds->last_done) CUDA_TRY(cudaEventCreateWithFlags(&ds->last_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ds->last_done, stream));
+    ds->last_stream = stream;
+    ds->has_last = true;
+  }
   for (cudaStream_t s : others) {
     cudaEvent_t ev;
     CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1939,6 +1995,21 @@ ncclResult_t register_program(Comm* comm, std::unique_ptr<RankIR> ir, int* ir_id
   if (ir->prog.collective != "allreduce" && ir->prog.collective != "allgather" && ir->prog.collective != "reducescatter" &&
       ir->prog.collective != "alltoall")
     return set_error(ncclInvalidUsage, "collective %s has no NCCL entry point", ir->prog.collective.c_str());
+  {  // buffer shapes the NCCL entry points map onto (core.hpp:305-397): AllReduce and
+     // ReduceScatter run in place on `input`, AllGather / AlltoAll out of place
+    const Program& p = ir->prog;
+    const int R = comm->nranks, cin = p.nchunks[0], cout = p.nchunks[1];
+    const std::string& coll = p.collective;
+    const char* bad = nullptr;
+    if (cin < 1) bad = "nchunks.input must be >= 1";
+    else if ((coll == "allreduce" || coll == "reducescatter") && !p.inplace) bad = "must be in place";
+    else if ((coll == "allreduce" || coll == "reducescatter") && cout != cin) bad = "needs nchunks.output == nchunks.input";
+    else if (coll == "reducescatter" && cin % R) bad = "needs nchunks.input divisible by the rank count";
+    else if ((coll == "allgather" || coll == "alltoall") && p.inplace) bad = "must be out of place";
+    else if (coll == "allgather" && cout != R * cin) bad = "needs nchunks.output == ranks x nchunks.input";
+    else if (coll == "alltoall" && (cout != cin || cin % R)) bad = "needs nchunks.output == nchunks.input, divisible by the rank count";
+    if (bad) return set_error(ncclInvalidUsage, "%s IR %s %s", coll.c_str(), p.name.c_str(), bad);
+  }
   for (const auto& g : ir->prog.gpus)
     for (const auto& tb : g.tbs)
       for (const auto& op : tb.ops) {
@@ -2195,6 +2266,7 @@ static void release_comm(Comm* c) {
       if (ds.d_trace) cudaFree(ds.d_trace);
       if (ds.d_wq_next) cudaFree(ds.d_wq_next);
       if (ds.d_prog) cudaFree(ds.d_prog);
+      if (ds.last_done) cudaEventDestroy(ds.last_done);
       cudaFreeHost(ds.h_err);
     }
     g_cliques.erase(cl->key);
@@ -2350,6 +2422,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "wq") c.wq = static_cast<int>(value);
   else if (k == "tma_min") c.tma_min = value;
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
+  else if (k == "ll128_max_bytes") c.ll128_max_bytes = value;
   else if (k == "builtin") c.builtin = static_cast<int>(value);
   else if (k == "smem_kb") c.smem_kb = value;
   else if (k == "select") c.select = static_cast<int>(value);
@@ -2396,7 +2469,7 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
     }
   CallPlan cp;
   NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1, ntbs, false, cp));
-  info->protocol = cp.ll ? 1 : 0;
+  info->protocol = cp.proto;
   info->lanes = cp.lanes;
   info->unit_warps = cp.unit_warps;
   info->group = cp.group;
@@ -2507,9 +2580,16 @@ ncclResult_t gc3IrArenaLayout(gc3Ir_t ir, int rank, int lanes, int slots, int64_
   os << "{\"n_in\": " << a.n_in << ", \"n_out\": " << a.n_out << ", \"bytes\": " << a.bytes << ", \"off_head\": " << a.off_head
      << ", \"off_tail\": " << a.off_tail << ", \"off_mine_in\": " << a.off_mine_in << ", \"off_mine_out\": " << a.off_mine_out
      << ", \"fifo_off\": [";
-  for (size_t i = 0; i < a.fifo_off.size(); ++i) os << (i ? ", " : "") << a.fifo_off[i];
+  for (size_t i = 0; i < a.fifo_off[0].size(); ++i) os << (i ? ", " : "") << a.fifo_off[0][i];
   os << "], \"slot_stride\": [";
-  for (size_t i = 0; i < a.slot_stride.size(); ++i) os << (i ? ", " : "") << a.slot_stride[i];
+  for (size_t i = 0; i < a.slot_stride[0].size(); ++i) os << (i ? ", " : "") << a.slot_stride[0][i];
+  static const char* pn[] = {"simple", "ll", "ll128"};
+  for (int pr = 1; pr < kNumProtos; ++pr) {
+    os << "], \"fifo_off_" << pn[pr] << "\": [";
+    for (size_t i = 0; i < a.fifo_off[pr].size(); ++i) os << (i ? ", " : "") << a.fifo_off[pr][i];
+    os << "], \"slot_stride_" << pn[pr] << "\": [";
+    for (size_t i = 0; i < a.slot_stride[pr].size(); ++i) os << (i ? ", " : "") << a.slot_stride[pr][i];
+  }
   os << "]}";
   *json = dup_cstr(os.str());
   return ncclSuccess;

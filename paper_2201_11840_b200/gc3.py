@@ -318,6 +318,12 @@ class Comm:
             check(lib().ncclCommDestroy(self.h))
             self.h = None
 
+    def abort(self):
+        """ncclCommAbort: raises the device abort flag (spinning blocks exit) and frees the comm."""
+        if self.h:
+            check(lib().ncclCommAbort(self.h))
+            self.h = None
+
 
 @contextlib.contextmanager
 def group():

@@ -87,3 +87,71 @@ def test_allreduce_int_full_size_equals_sum(name, mib):
     finally:
         for c in comms:
             c.destroy()
+
+
+# ---------------------------------------------------------------------------------------------
+# Bit-exact parity with the CPU oracle at BASELINE.json's own sizes and dtypes (the planner picks
+# different tiles, lane multipliers and bulk / L2 paths there than at the small parity sizes).
+
+def _oracle_full(name, coll, count, dtype, proto=None, seed=3, **cfg):
+    import numpy as np
+    from gpu_util import input_len, oracle_collective, run_collective, to_np_bits
+    comms = _comms(name, **cfg)
+    R = len(comms)
+    try:
+        if proto is not None:
+            for c in comms:
+                c.set_protocol(0, proto)
+        g = torch.Generator(device="cuda").manual_seed(seed)
+        n = input_len(coll, count, R)
+        inputs = [torch.randn(n, device="cuda", generator=g, dtype=torch.float32).to(getattr(torch, dtype)) for _ in range(R)]
+        host = [x.cpu() for x in inputs]
+        want_proto = {None: None, "simple": 0, "ll": 1, "ll128": 2}[proto]
+        if want_proto is not None:
+            assert comms[0].query_plan(coll, count, dtype)["protocol"] == want_proto
+        outs = run_collective(comms, coll, inputs, count, dtype, "sum")
+        torch.cuda.synchronize()
+        assert comms[0].async_error()[0] == 0
+        got = [to_np_bits(o, dtype) for o in outs]
+        del outs, inputs
+        from oracle.oracle import collective
+        odt = {"bfloat16": 9, "float16": 6}.get(dtype, dtype)
+        want = collective(json.loads(read_ir(name)), coll, [to_np_bits(x, dtype) for x in host], count, odt, "sum", mode="threaded")
+        for r in range(R):
+            if not np.array_equal(got[r], want[r]):
+                bad = np.nonzero(got[r] != want[r])[0]
+                raise AssertionError(f"{name} {proto} rank {r}: {bad.size} mismatches, first at {bad[:8]}")
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+def test_c3_hier_allreduce_bf16_256MiB_vs_oracle():
+    """C3: hierarchical 2x4 AllReduce with rrcs fusion, bf16, 256 MiB per rank."""
+    _oracle_full("hier_ar_2x4_par1", "allreduce", (256 << 20) // 2, "bfloat16")
+
+
+@pytest.mark.parametrize("proto", ["simple", "ll", "ll128"])
+@pytest.mark.parametrize("name", ["ring_ar_8_ch8_inst4", "ring_ar_8_inst4_auto"])
+def test_c4_ring_allreduce_f32_64MiB_vs_oracle(name, proto):
+    """C4: ring AllReduce instances=4 / channels=8 (and auto channels), f32, 64 MiB per rank, per protocol."""
+    _oracle_full(name, "allreduce", (64 << 20) // 4, "float32", proto)
+
+
+def test_c5_ring_reducescatter_f32_64MiB_vs_oracle():
+    """C5-RS: ring ReduceScatter over 8 ranks, f32, 64 MiB per rank (recvcount = 2 Mi elements)."""
+    _oracle_full("ring_rs_8", "reducescatter", (64 << 20) // 4 // 8, "float32")
+
+
+@pytest.mark.parametrize("proto", ["simple", "ll", "ll128"])
+def test_c1_ring_allreduce_f32_4MiB_vs_oracle(proto):
+    """C1: ring AllReduce, 1 channel, f32, 4 MiB per rank, per protocol."""
+    _oracle_full("ring_ar_8_ch1", "allreduce", (4 << 20) // 4, "float32", proto)
+
+
+def test_c5_ring_allgather_f32_64MiB_vs_oracle():
+    _oracle_full("ring_ag_8", "allgather", (64 << 20) // 4 // 8, "float32")
+
+
+def test_c2_twostep_alltoall_f32_64MiB_vs_oracle():
+    _oracle_full("twostep_a2a_2x4", "alltoall", (64 << 20) // 4 // 8, "float32")
