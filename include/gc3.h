@@ -130,6 +130,8 @@ typedef struct {
   char name[64];      /* IR name */
   int unit_warps;     /* warps interpreting one (thread block, lane) */
   int group;          /* tiles per op-major group inside a lane */
+  int mode;           /* 0: static lanes, 1: work queue, 2: dataflow (ready (op, tile) items) */
+  int mail_messages;  /* dataflow: messages carried through the launch's mailbox */
 } gc3PlanInfo;
 /* collective: 0 allreduce, 1 allgather, 2 reducescatter, 3 alltoall; count as in the NCCL call. */
 ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDataType_t datatype, gc3PlanInfo* info);

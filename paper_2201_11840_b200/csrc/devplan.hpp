@@ -74,6 +74,21 @@ struct DevTb {
   int32_t recv_slot;  // rank slot of the receive peer when it runs in the same launch, else -1
 };
 
+// Dataflow execution (interp_df_kernel): one node per op of every thread block of the launch; a work
+// item is (node, tile) and becomes ready when all of the node's predecessors in the happens-before
+// graph (the previous op of its thread block, its declared deps, the sender of its message) are
+// done for that tile. Messages that are neither direct nor pulled travel through a per-launch
+// mailbox (one span per message, written by the sender, read by the receiver).
+struct DfNode {     // 24 bytes
+  int32_t op;       // index into LaunchArgs::ops
+  int32_t tbi;      // launch thread block (LaunchArgs::tbs)
+  int32_t succ;     // first successor in LaunchArgs::df_succ
+  int16_t nsucc;
+  int16_t indeg;    // predecessors (distinct)
+  int32_t in_mail;  // >= 0: the incoming message is read from mail + in_mail chunks
+  int32_t out_mail; // >= 0: the outgoing message is written to mail + out_mail chunks
+};
+
 // One side of one connection for one lane.  The FIFOs and `head` live in the receiver's memory,
 // `tail` in the sender's memory (NVLink buffers on the receiving GPU). Every
 // protocol has its own slots (NCCL keeps per-protocol buffers for the same reason): a line protocol
@@ -125,6 +140,16 @@ struct LaunchArgs {
   int32_t* wq_next;     // work-queue claim counter (zeroed before the launch)
   const int32_t* wq_order;  // claim position -> item (tile * ntbs + thread block); null: identity
   uint64_t* prog;       // work-queue progress: [thread block][tile] = (epoch << 32) | steps done
+  // dataflow mode (interp_df_kernel)
+  const DfNode* df_nodes;
+  const int32_t* df_succ;    // successor node ids
+  const int32_t* df_roots;   // nodes without predecessors
+  int32_t* df_cnt;           // [tile][node] predecessors done (self-resetting: zero between launches)
+  int32_t* df_q;             // ready queue of items + 1 (self-resetting)
+  int32_t* df_ctr;           // {pop, push} counters (zeroed before the launch)
+  char* mail;                // mailbox of the launch's non-direct, non-pulled messages
+  int32_t df_n;              // nodes
+  int32_t df_nroots;
   char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source, result (the
                                      // caller's recvbuff shifted so that an owned ReduceScatter chunk
                                      // keeps its input offset; see result_writes), source (the caller's

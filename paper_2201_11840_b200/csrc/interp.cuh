@@ -1265,6 +1265,146 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(cons
   interp_wq<R>(w, s_bufs, tma, pol_last, t, n, uw, uib, bar_id);
 }
 
+// ------------------------------------------------------------------ dataflow execution
+// Programs whose ranks all run in this launch (Simple protocol) can execute as a dataflow graph:
+// a work item is (node, tile), a node being one op of one thread block, and it is claimed only when
+// every predecessor of the node in the happens-before graph (the previous op of its thread block,
+// its declared deps -- PAPER.md:424, 431-433 -- and the sender of its message) has finished that
+// tile. Units never block on a dependency: whatever is ready is what runs, so chains of dependent
+// hops (ring / hierarchical AllReduce, ReduceScatter, AllGather) pipeline across tiles without idle
+// units, and a producer's output is consumed while it is still in L2.
+// Tiles are position-disjoint instances of the program (every op maps byte x of a chunk to byte x
+// of a chunk), so the per-tile graphs are independent and any linear extension of each is a valid
+// execution. Messages are direct, pulled (as in the static interpreter) or mailed: written by the
+// sender into a per-message mailbox span and read from there by the receiver.
+// Ready queue: the first df_nroots x ntiles positions are the root items (tile-major, implicit);
+// later positions are filled by the unit that completes an item's last predecessor. A unit that
+// claims position p waits until p is filled: every position is eventually filled (the graph is a
+// DAG and claimed items never wait), so this cannot deadlock. Counters and queue slots are reset
+// by their consumer, so the tables are zero at every launch without a memset.
+__device__ __forceinline__ int32_t ld_relaxed32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed32(int32_t* p, int32_t v) {
+  asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+template <class R>
+__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(const LaunchArgs a) {
+  __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
+#pragma unroll
+  for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
+    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  __syncthreads();
+  const int uw = a.unit_warps;
+  const int n = uw * 32;
+  const int uib = threadIdx.x / n;
+  const int t = threadIdx.x - uib * n;
+  const int bar_id = 1 + uib;
+  extern __shared__ __align__(128) char s_stage[];
+  __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
+  __shared__ uint32_t s_seq[kThreads / 32];
+  __shared__ int64_t s_item[kThreads / 32];
+  Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0,
+          (a.l2hint & 2) ? l2_evict_first_policy() : 0};
+  const uint64_t pol_last = l2_evict_last_policy();
+  if (t == 0) s_seq[uib] = 0;
+  if (t == 0 && a.tma_stages > 0) {
+    for (int s = 0; s < a.tma_stages; ++s) mbar_init(&s_bar[uib][s]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unit_sync(uw, bar_id, n);
+  const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
+  const int64_t chunk_bytes = chunk_elems * R::kEsize;
+  const int64_t nn = a.df_n;
+  const int64_t total = nn * ntiles;
+  const int64_t nroot_items = static_cast<int64_t>(a.df_nroots) * ntiles;
+  for (;;) {
+    if (t == 0) {
+      const int64_t idx = atomicAdd(a.df_ctr, 1);
+      int64_t item = -1;
+      if (idx < nroot_items) {
+        item = (idx / a.df_nroots) * nn + a.df_roots[idx % a.df_nroots];
+      } else if (idx < total) {
+        int32_t* slot = a.df_q + (idx - nroot_items);
+        int32_t v = ld_relaxed32(slot);
+        if (v == 0) {
+          Ctx c{a.abort_flag, a.err_info, a.timeout_ns, 0, -1, 0, idx};
+          const uint64_t start = globaltimer();
+          for (int it = 0; (v = ld_relaxed32(slot)) == 0; ++it) {
+            if ((it & 255) == 255) {
+              if (*reinterpret_cast<volatile int*>(a.abort_flag)) break;
+              if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
+                raise_timeout(c, 5);
+                break;
+              }
+            }
+          }
+        }
+        if (v != 0) {
+          fence_acq_rel(false);  // the producers' data (released before the push) is visible
+          item = v - 1;
+          st_relaxed32(slot, 0);
+        }
+      }
+      s_item[uib] = item;
+    }
+    unit_sync(uw, bar_id, n);
+    const int64_t item = s_item[uib];
+    if (item < 0) return;
+    const int64_t tile = item / nn;
+    const int u = static_cast<int>(item - tile * nn);
+    const DfNode nd = a.df_nodes[u];
+    const DevOp op = a.ops[nd.op];
+    const DevTb tb = a.tbs[nd.tbi];
+    char* const* const mine = s_bufs + kBufs * tb.rank_slot;
+    char* const* const peer = s_bufs + kBufs * (tb.peer_slot >= 0 ? tb.peer_slot : 0);
+    char* const* const rpeer = s_bufs + kBufs * (tb.recv_slot >= 0 ? tb.recv_slot : 0);
+    const int64_t t0 = tile * tile_elems;
+    const int64_t tbytes = min(tile_elems, chunk_elems - t0) * R::kEsize;
+    const int64_t t0_bytes = t0 * R::kEsize;
+    tma.pol = op.hot ? pol_last : 0;
+    const bool in_d = (op.direct & kInDirect) != 0, in_p = (op.direct & kInPull) != 0;
+    const bool out_d = (op.direct & kOutDirect) != 0;
+    char* src = mine[op.src_buf] + op.src_off * chunk_bytes + t0_bytes;
+    char* dst = mine[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes;
+    const char* srcr = mine[op.src_rbuf] + op.src_off * chunk_bytes + t0_bytes;
+    const char* dstr = mine[op.dst_rbuf] + op.dst_off * chunk_bytes + t0_bytes;
+    const char* in = nd.in_mail >= 0 ? a.mail + nd.in_mail * chunk_bytes + t0_bytes
+                     : in_p          ? rpeer[op.in_buf] + op.in_off * chunk_bytes + t0_bytes
+                                     : nullptr;
+    char* out = nd.out_mail >= 0 ? a.mail + nd.out_mail * chunk_bytes + t0_bytes
+                : out_d          ? peer[op.dst_buf] + op.dst_off * chunk_bytes + t0_bytes
+                                 : nullptr;
+    transfer<R>(op, in_d, src, dst, srcr, dstr, in, chunk_bytes, out, chunk_bytes, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw, bar_id,
+                a.tma_min);
+    unit_sync(uw, bar_id, n);
+    if (a.discard && nd.in_mail >= 0 && ((reinterpret_cast<uintptr_t>(in) | static_cast<uintptr_t>(chunk_bytes)) & 127) == 0) {
+      // the mailbox span is dead once read: drop its (whole, 128-byte aligned) lines from L2 so
+      // they are never written back
+      for (int j = 0; j < op.count; ++j)
+        for (int64_t off = static_cast<int64_t>(t) * 128; off + 128 <= tbytes; off += static_cast<int64_t>(n) * 128)
+          asm volatile("discard.global.L2 [%0], 128;" ::"l"(in + j * chunk_bytes + off) : "memory");
+    }
+    if (t == 0 && nd.nsucc > 0) {
+      fence_acq_rel(false);  // release the unit's data (gathered by the barrier) before the counts
+      for (int k = 0; k < nd.nsucc; ++k) {
+        const int32_t sn = a.df_succ[nd.succ + k];
+        int32_t* cnt = a.df_cnt + tile * nn + sn;
+        const int32_t need = a.df_nodes[sn].indeg;
+        if (atomicAdd(cnt, 1) + 1 == need) {  // the last predecessor: the item is ready
+          *cnt = 0;
+          const int32_t pos = atomicAdd(a.df_ctr + 1, 1);
+          __threadfence();
+          st_relaxed32(a.df_q + pos, static_cast<int32_t>(tile * nn + sn) + 1);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace dev
 
 }  // namespace gc3

@@ -11,5 +11,6 @@ KernelFn interp_kernel_copy(int proto) {
                               : dev::interp<dev::RedNone, kProtoSimple>;
 }
 KernelFn interp_kernel_copy_wq() { return dev::interp_wq_kernel<dev::RedNone>; }
+KernelFn interp_kernel_copy_df() { return dev::interp_df_kernel<dev::RedNone>; }
 
 }  // namespace gc3

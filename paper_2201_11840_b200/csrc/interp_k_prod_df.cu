@@ -1,5 +1,5 @@
-// Interpreter instantiations for the prod reduction over every ncclDataType_t (see interp.cuh):
-// the static-lane interpreter per protocol (the dataflow kernel is in interp_k_prod_df.cu).
+// Dataflow-kernel instantiations for the prod reduction over every ncclDataType_t (see interp.cuh):
+// the dataflow kernel (interp_df_kernel, Simple protocol).
 #include "interp.cuh"
 
 namespace gc3 {
@@ -7,8 +7,8 @@ namespace gc3 {
 using KernelFn = void (*)(LaunchArgs);
 
 template <class R>
-static KernelFn pick(int proto) {
-  return proto == kProtoLL128 ? dev::interp<R, kProtoLL128> : proto == kProtoLL ? dev::interp<R, kProtoLL> : dev::interp<R, kProtoSimple>;
+static KernelFn pick_df() {
+  return dev::interp_df_kernel<R>;
 }
 
 #define GC3_BY_DTYPE(EXPR)                                   \
@@ -26,9 +26,9 @@ static KernelFn pick(int proto) {
     default: return nullptr;                                 \
   }
 
-KernelFn interp_kernel_prod(int dtype, int proto) {
+KernelFn interp_kernel_prod_df(int dtype) {
   constexpr int OP = dev::kProd;
-  GC3_BY_DTYPE(return pick<R>(proto))
+  GC3_BY_DTYPE(return pick_df<R>())
 }
 
 }  // namespace gc3

@@ -1,4 +1,5 @@
-// Interpreter instantiations for the sum reduction over every ncclDataType_t (see interp.cuh).
+// Interpreter instantiations for the sum reduction over every ncclDataType_t (see interp.cuh):
+// the static-lane interpreter per protocol (the dataflow kernel is in interp_k_sum_df.cu).
 #include "interp.cuh"
 
 namespace gc3 {
@@ -10,21 +11,24 @@ static KernelFn pick(int proto) {
   return proto == kProtoLL128 ? dev::interp<R, kProtoLL128> : proto == kProtoLL ? dev::interp<R, kProtoLL> : dev::interp<R, kProtoSimple>;
 }
 
-KernelFn interp_kernel_sum(int dtype, int ll) {
-  constexpr int OP = dev::kSum;
-  switch (dtype) {
-    case 0: return pick<dev::RedInt<int8_t, OP>>(ll);
-    case 1: return pick<dev::RedInt<uint8_t, OP>>(ll);
-    case 2: return pick<dev::RedInt<int32_t, OP>>(ll);
-    case 3: return pick<dev::RedInt<uint32_t, OP>>(ll);
-    case 4: return pick<dev::RedInt<int64_t, OP>>(ll);
-    case 5: return pick<dev::RedInt<uint64_t, OP>>(ll);
-    case 6: return pick<dev::RedHalf<false, OP>>(ll);
-    case 7: return pick<dev::RedFloat<float, OP>>(ll);
-    case 8: return pick<dev::RedFloat<double, OP>>(ll);
-    case 9: return pick<dev::RedHalf<true, OP>>(ll);
-    default: return nullptr;
+#define GC3_BY_DTYPE(EXPR)                                   \
+  switch (dtype) {                                           \
+    case 0: { using R = dev::RedInt<int8_t, OP>; EXPR; }     \
+    case 1: { using R = dev::RedInt<uint8_t, OP>; EXPR; }    \
+    case 2: { using R = dev::RedInt<int32_t, OP>; EXPR; }    \
+    case 3: { using R = dev::RedInt<uint32_t, OP>; EXPR; }   \
+    case 4: { using R = dev::RedInt<int64_t, OP>; EXPR; }    \
+    case 5: { using R = dev::RedInt<uint64_t, OP>; EXPR; }   \
+    case 6: { using R = dev::RedHalf<false, OP>; EXPR; }     \
+    case 7: { using R = dev::RedFloat<float, OP>; EXPR; }    \
+    case 8: { using R = dev::RedFloat<double, OP>; EXPR; }   \
+    case 9: { using R = dev::RedHalf<true, OP>; EXPR; }      \
+    default: return nullptr;                                 \
   }
+
+KernelFn interp_kernel_sum(int dtype, int proto) {
+  constexpr int OP = dev::kSum;
+  GC3_BY_DTYPE(return pick<R>(proto))
 }
 
 }  // namespace gc3

@@ -17,10 +17,27 @@ KernelFn interp_kernel_sum(int dtype, int proto);
 KernelFn interp_kernel_prod(int dtype, int proto);
 KernelFn interp_kernel_max(int dtype, int proto);
 KernelFn interp_kernel_min(int dtype, int proto);
+KernelFn interp_kernel_copy_df();
+KernelFn interp_kernel_sum_df(int dtype);
+KernelFn interp_kernel_prod_df(int dtype);
+KernelFn interp_kernel_max_df(int dtype);
+KernelFn interp_kernel_min_df(int dtype);
 
 constexpr int kMaxDynamicSmem = 220 << 10;  // TMA staging budget per block (runtime smem_kb <= 220)
 
 KernelFn interp_kernel_wq(int redop) { return redop == -1 ? interp_kernel_copy_wq() : nullptr; }
+
+// dataflow kernel (Simple protocol, every rank of the program in the launch)
+KernelFn interp_kernel_df(int dtype, int redop) {
+  switch (redop) {
+    case -1: return interp_kernel_copy_df();
+    case 0: return interp_kernel_sum_df(dtype);
+    case 1: return interp_kernel_prod_df(dtype);
+    case 2: return interp_kernel_max_df(dtype);
+    case 3: return interp_kernel_min_df(dtype);
+    default: return nullptr;
+  }
+}
 
 // dtype: ncclDataType_t; redop: ncclRedOp_t or -1 for copy-only programs; ll: kProtoSimple / kProtoLL / kProtoLL128.
 KernelFn interp_kernel(int dtype, int redop, int ll) {

@@ -47,6 +47,7 @@ namespace gc3 {
 using KernelFn = void (*)(LaunchArgs);
 KernelFn interp_kernel(int dtype, int redop, int proto);
 KernelFn interp_kernel_wq(int redop);  // work-queue kernel (copy-only programs), nullptr otherwise
+KernelFn interp_kernel_df(int dtype, int redop);  // dataflow kernel (Simple, every rank in the launch)
 cudaError_t interp_launch(KernelFn fn, const LaunchArgs& args, int grid, size_t smem, cudaStream_t stream);
 int interp_blocks_per_sm(KernelFn fn, size_t smem);
 constexpr int kStageBytesHost = 16 << 10;  // interp.cuh kStageBytes
@@ -121,6 +122,12 @@ struct Config {
   int wq_lag = 0;                    // claim deeper thread blocks' items this many tiles later (0: off)
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
+  int df = 1;                        // dataflow execution (interp_df_kernel) when every rank is in the
+                                     // launch: 1 = programs with receive-and-forward chains, 2 = every
+                                     // Simple program, 0 = off
+  int df_items = 4;                  // dataflow: ready items per unit targeted by the tile size
+  int64_t df_max_tile = 256 << 10;   // dataflow: largest tile
+  int64_t df_min_tile = 16 << 10;    // dataflow: smallest tile (unless the chunk is smaller)
 };
 
 Config config_from_env() {
@@ -152,6 +159,10 @@ Config config_from_env() {
   c.wq_items = static_cast<int>(env_int("GC3_WQ_ITEMS", c.wq_items));
   c.wq_lag = static_cast<int>(env_int("GC3_WQ_LAG", c.wq_lag));
   c.discard = static_cast<int>(env_int("GC3_DISCARD", c.discard));
+  c.df = static_cast<int>(env_int("GC3_DF", c.df));
+  c.df_items = static_cast<int>(env_int("GC3_DF_ITEMS", c.df_items));
+  c.df_max_tile = env_int("GC3_DF_MAX_TILE", c.df_max_tile);
+  c.df_min_tile = env_int("GC3_DF_MIN_TILE", c.df_min_tile);
   return c;
 }
 
@@ -316,6 +327,13 @@ struct DevicePlan {  // one registered IR on one device
   DevChan* d_chans = nullptr;
   uint64_t* d_sems = nullptr;
   bool sys_scope = false;
+  // dataflow graph (every rank of the program in this launch): nodes in launch op order
+  bool df_ok = false;
+  int df_n = 0, df_nroots = 0, df_mail_msgs = 0;
+  int64_t df_mail_chunks = 0;  // mailbox size in chunks
+  DfNode* d_df_nodes = nullptr;
+  int32_t* d_df_succ = nullptr;
+  int32_t* d_df_roots = nullptr;
 };
 
 struct DeviceState {
@@ -329,6 +347,11 @@ struct DeviceState {
   std::map<std::pair<KernelFn, size_t>, int> occupancy;  // (kernel, dynamic smem) -> blocks per SM
   uint64_t* d_trace = nullptr;  // event log of the last traced launch
   size_t trace_bytes = 0;
+  int32_t* d_df_cnt = nullptr;   // dataflow predecessor counters [tile][node] (self-resetting)
+  int32_t* d_df_q = nullptr;     // dataflow ready queue (self-resetting)
+  size_t df_items_cap = 0;       // entries of d_df_cnt / d_df_q
+  char* d_mail = nullptr;        // dataflow mailbox
+  size_t mail_bytes = 0;
   int32_t* d_wq_next = nullptr;  // work-queue claim counter
   uint64_t* d_prog = nullptr;    // work-queue progress table
   size_t prog_bytes = 0;
@@ -1222,6 +1245,62 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   }
   for (const DevOp& o : ops)
     if (o.ndeps > 400) return set_error(ncclInvalidArgument, "an op with %d deps exceeds the 400-dep limit", o.ndeps);
+  // dataflow graph: possible when every rank of the program runs in this launch and the
+  // happens-before graph is acyclic. Node = op (launch order); edges = previous op of the thread
+  // block, declared deps, message sender -> receiver; messages neither direct nor pulled get a
+  // mailbox span each.
+  std::vector<DfNode> df_nodes;
+  std::vector<int32_t> df_succ, df_roots;
+  plan.df_ok = false;
+  plan.df_mail_chunks = 0;
+  plan.df_mail_msgs = 0;
+  if (static_cast<int>(plan.ranks.size()) == p.ranks() && HbGraph(p).ok) {
+    std::vector<std::set<int>> succ(ops.size());
+    std::vector<int> indeg(ops.size(), 0);
+    auto node = [&](int r, int t, int s) { return tbs[launch_index[{r, t}]].op_begin + s; };
+    df_nodes.assign(ops.size(), DfNode{});
+    for (int r : plan.ranks)
+      for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+        const ThreadBlock& tb = p.gpus[r].tbs[t];
+        for (size_t s = 0; s < tb.ops.size(); ++s) {
+          const int v = node(r, static_cast<int>(t), static_cast<int>(s));
+          df_nodes[v].op = v;
+          df_nodes[v].tbi = launch_index[{r, static_cast<int>(t)}];
+          df_nodes[v].in_mail = df_nodes[v].out_mail = -1;
+          if (s > 0) succ[node(r, static_cast<int>(t), static_cast<int>(s) - 1)].insert(v);
+          for (const Dep& dp : tb.ops[s].deps) succ[node(r, tb_index(p, r, dp.tb), dp.step)].insert(v);
+          const auto& sd = senders[r][t][s];
+          if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0 && sd.rank >= 0) {
+            const int x = node(sd.rank, sd.tb, sd.step);
+            succ[x].insert(v);
+            if (!(eff[r][t][s] & (kInDirect | kInPull))) {  // a mailed message
+              df_nodes[v].in_mail = static_cast<int32_t>(plan.df_mail_chunks);
+              df_nodes[x].out_mail = static_cast<int32_t>(plan.df_mail_chunks);
+              plan.df_mail_chunks += tb.ops[s].count;
+              plan.df_mail_msgs++;
+            }
+          }
+        }
+      }
+    bool fits = true;
+    for (size_t u = 0; u < ops.size(); ++u) {
+      df_nodes[u].succ = static_cast<int32_t>(df_succ.size());
+      df_nodes[u].nsucc = static_cast<int16_t>(succ[u].size());
+      fits = fits && succ[u].size() < 32768;
+      for (int v : succ[u]) {
+        df_succ.push_back(v);
+        indeg[v]++;
+      }
+    }
+    for (size_t u = 0; u < ops.size(); ++u) {
+      df_nodes[u].indeg = static_cast<int16_t>(indeg[u]);
+      fits = fits && indeg[u] < 32768;
+      if (indeg[u] == 0) df_roots.push_back(static_cast<int32_t>(u));
+    }
+    plan.df_ok = fits && !df_roots.empty() && ops.size() < (1u << 20);
+    plan.df_n = static_cast<int>(ops.size());
+    plan.df_nroots = static_cast<int>(df_roots.size());
+  }
   DeviceGuard g(ds.device);
   auto upload = [&](auto*& dptr, const auto& vec) -> ncclResult_t {
     using T = typename std::decay_t<decltype(vec)>::value_type;
@@ -1234,6 +1313,11 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   NCCL_TRY(upload(plan.d_ops, ops));
   NCCL_TRY(upload(plan.d_deps, deps));
   NCCL_TRY(upload(plan.d_chans, chans));
+  if (plan.df_ok) {
+    NCCL_TRY(upload(plan.d_df_nodes, df_nodes));
+    NCCL_TRY(upload(plan.d_df_succ, df_succ));
+    NCCL_TRY(upload(plan.d_df_roots, df_roots));
+  }
   const size_t nsem = std::max(sem_next, 1);
   CUDA_TRY(cudaMalloc(&plan.d_sems, nsem * sizeof(uint64_t)));
   CUDA_TRY(cudaMemset(plan.d_sems, 0, nsem * sizeof(uint64_t)));
@@ -1511,6 +1595,7 @@ struct CallPlan {
   int64_t small_elems = 0, n_head = 0, n_big = 0;  // tapered tiles (see plan_call)
   int stage_bytes = 16 << 10;
   bool wq = false;  // work-queue mode (interp_wq)
+  bool df = false;  // dataflow mode (interp_df_kernel)
   int weight = 0;        // units per lane: sum of multipliers, or thread blocks when uniform
 };
 
@@ -1695,6 +1780,33 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
                                               : chunk_bytes * ntbs_local / (static_cast<int64_t>(std::max(1, c->cfg.wq_items)) * units);
     tb_bytes = std::min<int64_t>(std::max<int64_t>(tb_bytes, 32 << 10), 1 << 20);
     tb_bytes = align_up(static_cast<size_t>(tb_bytes), 16);
+    if (chunk_bytes <= tb_bytes) tb_bytes = chunk_bytes;
+    cp.tile_elems = std::max<int64_t>(tb_bytes / cp.kesize, 1);
+    cp.ntiles = (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems;
+    cp.small_elems = cp.tile_elems;
+    cp.n_head = 0;
+    cp.n_big = cp.ntiles;
+    cp.lanes = 1;
+    cp.weight = units;
+    cp.group = 1;
+    cp.grid = (units + units_per_block - 1) / units_per_block;
+  }
+  // dataflow mode: every co-resident unit runs ready (op, tile) items (interp_df_kernel)
+  cp.df = false;
+  const bool df_ok = ds.plans.size() > static_cast<size_t>(id) && ds.plans[id].df_ok;
+  KernelFn df_fn = df_ok ? interp_kernel_df(cp.redop < 0 ? 0 : dtype, cp.redop) : nullptr;
+  if (c->cfg.df && df_fn && !cp.ll && !sys_scope && c->cfg.lanes <= 0 && chunk_bytes > 0 && (ir.has_chain || c->cfg.df > 1) &&
+      interp_blocks_per_sm(df_fn, cp.smem) >= bps) {
+    cp.df = true;
+    cp.wq = false;
+    cp.fn = df_fn;
+    cp.uniform = true;
+    const int units = capacity;
+    const int64_t nn = ds.plans[id].df_n;
+    int64_t tb_bytes = c->cfg.tile_bytes > 0 ? c->cfg.tile_bytes
+                                              : chunk_bytes * nn / (static_cast<int64_t>(std::max(1, c->cfg.df_items)) * units);
+    tb_bytes = std::min<int64_t>(std::max<int64_t>(tb_bytes, c->cfg.df_min_tile), c->cfg.df_max_tile);
+    tb_bytes = std::max<int64_t>(tb_bytes / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
     if (chunk_bytes <= tb_bytes) tb_bytes = chunk_bytes;
     cp.tile_elems = std::max<int64_t>(tb_bytes / cp.kesize, 1);
     cp.ntiles = (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems;
@@ -1924,6 +2036,40 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][2] = c->scratch;
     a.bufs[slot][kSource] = source ? source : in;
     a.bufs[slot][kResult] = result ? result : in;
+  }
+  if (cp.df) {  // ready-queue counters reset; self-resetting tables sized for this tile count; mailbox
+    DeviceGuard gw(dev);
+    const size_t items = static_cast<size_t>(plan.df_n) * static_cast<size_t>(cp.ntiles);
+    if (items > ds->df_items_cap) {
+      if (ds->d_df_cnt) CUDA_TRY(cudaFree(ds->d_df_cnt));
+      if (ds->d_df_q) CUDA_TRY(cudaFree(ds->d_df_q));
+      ds->d_df_cnt = ds->d_df_q = nullptr;
+      ds->df_items_cap = 0;
+      CUDA_TRY(cudaMalloc(&ds->d_df_cnt, items * sizeof(int32_t)));
+      CUDA_TRY(cudaMalloc(&ds->d_df_q, items * sizeof(int32_t)));
+      CUDA_TRY(cudaMemset(ds->d_df_cnt, 0, items * sizeof(int32_t)));
+      CUDA_TRY(cudaMemset(ds->d_df_q, 0, items * sizeof(int32_t)));
+      ds->df_items_cap = items;
+    }
+    const size_t mail_need = std::max<size_t>(static_cast<size_t>(plan.df_mail_chunks) * static_cast<size_t>(chunk_bytes), 256);
+    if (mail_need > ds->mail_bytes) {
+      if (ds->d_mail) CUDA_TRY(cudaFree(ds->d_mail));
+      ds->d_mail = nullptr;
+      ds->mail_bytes = 0;
+      CUDA_TRY(cudaMalloc(&ds->d_mail, mail_need));
+      ds->mail_bytes = mail_need;
+    }
+    if (!ds->d_wq_next) CUDA_TRY(cudaMalloc(&ds->d_wq_next, 256));
+    CUDA_TRY(cudaMemsetAsync(ds->d_wq_next, 0, 2 * sizeof(int32_t), stream));
+    a.df_nodes = plan.d_df_nodes;
+    a.df_succ = plan.d_df_succ;
+    a.df_roots = plan.d_df_roots;
+    a.df_cnt = ds->d_df_cnt;
+    a.df_q = ds->d_df_q;
+    a.df_ctr = ds->d_wq_next;
+    a.mail = ds->d_mail;
+    a.df_n = plan.df_n;
+    a.df_nroots = plan.df_nroots;
   }
   if (cp.wq) {  // claim counter reset + progress table (epoch-tagged, never reset)
     DeviceGuard gw(dev);
@@ -2260,12 +2406,18 @@ static void release_comm(Comm* c) {
         cudaFree(p.d_deps);
         cudaFree(p.d_chans);
         cudaFree(p.d_sems);
+        if (p.d_df_nodes) cudaFree(p.d_df_nodes);
+        if (p.d_df_succ) cudaFree(p.d_df_succ);
+        if (p.d_df_roots) cudaFree(p.d_df_roots);
         for (auto& [k, d] : p.wq_order) cudaFree(d);
       }
       cudaFree(ds.d_abort);
       if (ds.d_trace) cudaFree(ds.d_trace);
       if (ds.d_wq_next) cudaFree(ds.d_wq_next);
       if (ds.d_prog) cudaFree(ds.d_prog);
+      if (ds.d_df_cnt) cudaFree(ds.d_df_cnt);
+      if (ds.d_df_q) cudaFree(ds.d_df_q);
+      if (ds.d_mail) cudaFree(ds.d_mail);
       if (ds.last_done) cudaEventDestroy(ds.last_done);
       cudaFreeHost(ds.h_err);
     }
@@ -2430,6 +2582,10 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "wq_items") c.wq_items = static_cast<int>(value);
   else if (k == "wq_lag") c.wq_lag = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
+  else if (k == "df") c.df = static_cast<int>(value);
+  else if (k == "df_items") c.df_items = static_cast<int>(value);
+  else if (k == "df_max_tile") c.df_max_tile = value;
+  else if (k == "df_min_tile") c.df_min_tile = value;
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
@@ -2468,8 +2624,21 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
       ++nlocal;
     }
   CallPlan cp;
-  NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1, ntbs, false, cp));
+  {  // the device plan decides the execution mode: build it now when every rank lives in this process
+     // and has registered the IR (never blocks on other processes)
+    bool ready = true;
+    for (int r = 0; r < comm->nranks; ++r) {
+      Comm* lc = comm->clique->local[r];
+      ready = ready && lc && lc->irs.size() > static_cast<size_t>(info->ir_id);
+    }
+    if (ready) NCCL_TRY(build_plan(comm->clique, *ds, info->ir_id));
+  }
+  const bool built = ds->plans.size() > static_cast<size_t>(info->ir_id) && ds->plans[info->ir_id].built;
+  NCCL_TRY(plan_call(comm, *ds, info->ir_id, collective, count, datatype, collective == kAllReduce || collective == kReduceScatter ? 0 : -1,
+                     built ? ds->plans[info->ir_id].weight : ntbs, built && ds->plans[info->ir_id].sys_scope, cp));
   info->protocol = cp.proto;
+  info->mode = cp.df ? 2 : cp.wq ? 1 : 0;
+  info->mail_messages = cp.df ? ds->plans[info->ir_id].df_mail_msgs : 0;
   info->lanes = cp.lanes;
   info->unit_warps = cp.unit_warps;
   info->group = cp.group;

@@ -37,6 +37,7 @@ class PlanInfo(ctypes.Structure):
         ("chunk_elems", ctypes.c_int64), ("tile_elems", ctypes.c_int64), ("ntiles", ctypes.c_int64),
         ("slot_bytes", ctypes.c_int64), ("wire_bytes", ctypes.c_int64), ("hbm_bytes", ctypes.c_int64),
         ("name", ctypes.c_char * 64), ("unit_warps", ctypes.c_int), ("group", ctypes.c_int),
+        ("mode", ctypes.c_int), ("mail_messages", ctypes.c_int),
     ]
 
     def as_dict(self):

@@ -394,3 +394,54 @@ def test_small_messages_switch_to_ll():
             c.destroy()
     _check("ring_ar_8_ch8_inst4", 32 * 1024, ll_max_bytes=256 << 10)
     _check("ring_ar_8_ch8_inst4", 32 * 65536, ll_max_bytes=256 << 10)
+
+
+@pytest.mark.parametrize("name,count,dtype", [
+    ("ring_ar_8_ch1", 8 * 4096, "float32"), ("ring_ar_8_ch8_inst4", 32 * 4096, "float32"), ("hier_ar_2x4_par1", 8 * 6000, "bfloat16"),
+    ("hier_ar_2x4_par2", 16 * 512, "float32"), ("allpairs_ar_8", 8 * 777, "float32"), ("ring_ar_8_inst4_auto", 32 * 1000, "int32"),
+    ("ring_ag_8", 4096, "float32"), ("ring_rs_8", 4096, "bfloat16"), ("twostep_a2a_2x4", 4096, "float32"),
+    ("ring_ar_8_ch8_inst1.unfused", 8 * 1024, "float32"), ("hier_ar_2x4_par1.unfused", 8 * 2048, "float16"),
+])
+@pytest.mark.parametrize("df,tile", [(2, 0), (2, 1024), (2, 128), (0, 0)])
+def test_dataflow_mode(name, count, dtype, df, tile):
+    """Dataflow execution (interp_df_kernel: ready (op, tile) items, mailed messages for rrs) vs
+    static lanes: bit-exact vs the oracle for every family, tile size and dtype."""
+    _check(name, count, dtype, df=df, tile_bytes=tile, df_min_tile=128)
+
+
+def test_dataflow_mode_is_selected_and_mails_rrs_messages():
+    comms, irj = _setup("hier_ar_2x4_par1")
+    try:
+        plan = comms[0].query_plan("allreduce", 8 * 65536, "float32")
+        assert plan["mode"] == 2
+        assert plan["mail_messages"] == 8  # one rrs -> rrc message per rank
+    finally:
+        for c in comms:
+            c.destroy()
+    comms, irj = _setup("hier_ar_2x4_par1", df=0)
+    try:
+        assert comms[0].query_plan("allreduce", 8 * 65536, "float32")["mode"] == 0
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+@pytest.mark.parametrize("name,count", [("ring_ar_8_ch1", 8 * 1000 + 3), ("ring_rs_8", 777), ("ring_ag_8", 1001)])
+def test_dataflow_ragged_and_repeated(name, count):
+    from gpu_util import make_input, oracle_collective, run_collective, to_np_bits
+    comms, irj = _setup(name, df=2)
+    try:
+        coll = irj["collective"]
+        R = len(comms)
+        for it, n in enumerate([count, 8 * 64, count * 3, 8]):
+            from gpu_util import input_len
+            inputs = [make_input(input_len(coll, n, R), "float32", 17 * it + r) for r in range(R)]
+            expected = oracle_collective(irj, coll, [x.clone() for x in inputs], n, "float32")
+            outs = run_collective(comms, coll, inputs, n, "float32")
+            torch.cuda.synchronize()
+            assert comms[0].async_error()[0] == 0
+            for r in range(R):
+                assert np.array_equal(to_np_bits(outs[r], "float32"), expected[r]), (it, r)
+    finally:
+        for c in comms:
+            c.destroy()
