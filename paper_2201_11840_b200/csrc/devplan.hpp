@@ -79,14 +79,23 @@ struct DevTb {
 // graph (the previous op of its thread block, its declared deps, the sender of its message) are
 // done for that tile. Messages that are neither direct nor pulled travel through a per-launch
 // mailbox (one span per message, written by the sender, read by the receiver).
-struct DfNode {     // 24 bytes
-  int32_t op;       // index into LaunchArgs::ops
-  int32_t tbi;      // launch thread block (LaunchArgs::tbs)
-  int32_t succ;     // first successor in LaunchArgs::df_succ
+struct alignas(64) DfNode {  // 64 bytes: everything an item needs in one line
+  DevOp op;          // the op (launch order; DevOp::direct carries the in-launch transports)
+  int32_t succ;      // first successor in LaunchArgs::df_succ
   int16_t nsucc;
-  int16_t indeg;    // predecessors (distinct)
-  int32_t in_mail;  // >= 0: the incoming message is read from mail + in_mail chunks
-  int32_t out_mail; // >= 0: the outgoing message is written to mail + out_mail chunks
+  int16_t indeg;     // predecessors (distinct)
+  int32_t in_mail;   // >= 0: the incoming message is read from mail + in_mail chunks
+  int32_t out_mail;  // >= 0: the outgoing message is written to mail + out_mail chunks
+  int8_t rank_slot;  // the thread block's rank slot (LaunchArgs::bufs), its send and receive peers'
+  int8_t peer_slot;
+  int8_t recv_slot;
+  int8_t pad_;
+  int32_t tbi;       // launch thread block
+  int32_t pad2_[2];
+};
+struct DfSucc {  // successor node and its predecessor count
+  int32_t node;
+  int32_t indeg;
 };
 
 // One side of one connection for one lane.  The FIFOs and `head` live in the receiver's memory,
@@ -142,7 +151,7 @@ struct LaunchArgs {
   uint64_t* prog;       // work-queue progress: [thread block][tile] = (epoch << 32) | steps done
   // dataflow mode (interp_df_kernel)
   const DfNode* df_nodes;
-  const int32_t* df_succ;    // successor node ids
+  const DfSucc* df_succ;     // successors
   const int32_t* df_roots;   // nodes without predecessors
   int32_t* df_cnt;           // [tile][node] predecessors done (self-resetting: zero between launches)
   int32_t* df_q;             // ready queue of items + 1 (self-resetting)

@@ -1290,6 +1290,9 @@ __device__ __forceinline__ int32_t ld_relaxed32(const int32_t* p) {
 __device__ __forceinline__ void st_relaxed32(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release32(int32_t* p, int32_t v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <class R>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(const LaunchArgs a) {
@@ -1321,9 +1324,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
   const int64_t nn = a.df_n;
   const int64_t total = nn * ntiles;
   const int64_t nroot_items = static_cast<int64_t>(a.df_nroots) * ntiles;
+  uint64_t* const trace = a.trace;
+  // thread 0 claims its next queue position while the current item runs (a claim never blocks
+  // progress: every claimed position is filled once its item is ready, and ready items never wait)
+  int64_t next_idx = t == 0 ? static_cast<int64_t>(atomicAdd(a.df_ctr, 1)) : 0;
   for (;;) {
     if (t == 0) {
-      const int64_t idx = atomicAdd(a.df_ctr, 1);
+      const int64_t idx = next_idx;
+      const uint64_t t_claim = trace ? globaltimer() : 0;
       int64_t item = -1;
       if (idx < nroot_items) {
         item = (idx / a.df_nroots) * nn + a.df_roots[idx % a.df_nroots];
@@ -1344,10 +1352,15 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
           }
         }
         if (v != 0) {
-          fence_acq_rel(false);  // the producers' data (released before the push) is visible
+          fence_acq_rel(false);  // acquire: the producers' data (released before the push) is visible
           item = v - 1;
           st_relaxed32(slot, 0);
         }
+      }
+      if (item >= 0) next_idx = atomicAdd(a.df_ctr, 1);
+      if (trace && item >= 0) {
+        trace[item * 4 + 0] = t_claim;
+        trace[item * 4 + 1] = globaltimer();
       }
       s_item[uib] = item;
     }
@@ -1356,12 +1369,11 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
     if (item < 0) return;
     const int64_t tile = item / nn;
     const int u = static_cast<int>(item - tile * nn);
-    const DfNode nd = a.df_nodes[u];
-    const DevOp op = a.ops[nd.op];
-    const DevTb tb = a.tbs[nd.tbi];
-    char* const* const mine = s_bufs + kBufs * tb.rank_slot;
-    char* const* const peer = s_bufs + kBufs * (tb.peer_slot >= 0 ? tb.peer_slot : 0);
-    char* const* const rpeer = s_bufs + kBufs * (tb.recv_slot >= 0 ? tb.recv_slot : 0);
+    const DfNode nd = a.df_nodes[u];  // one 64-byte line: op, transports, peers, successors
+    const DevOp& op = nd.op;
+    char* const* const mine = s_bufs + kBufs * nd.rank_slot;
+    char* const* const peer = s_bufs + kBufs * (nd.peer_slot >= 0 ? nd.peer_slot : 0);
+    char* const* const rpeer = s_bufs + kBufs * (nd.recv_slot >= 0 ? nd.recv_slot : 0);
     const int64_t t0 = tile * tile_elems;
     const int64_t tbytes = min(tile_elems, chunk_elems - t0) * R::kEsize;
     const int64_t t0_bytes = t0 * R::kEsize;
@@ -1381,6 +1393,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
     transfer<R>(op, in_d, src, dst, srcr, dstr, in, chunk_bytes, out, chunk_bytes, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw, bar_id,
                 a.tma_min);
     unit_sync(uw, bar_id, n);
+    if (trace && t == 0) trace[item * 4 + 2] = globaltimer();
     if (a.discard && nd.in_mail >= 0 && ((reinterpret_cast<uintptr_t>(in) | static_cast<uintptr_t>(chunk_bytes)) & 127) == 0) {
       // the mailbox span is dead once read: drop its (whole, 128-byte aligned) lines from L2 so
       // they are never written back
@@ -1388,20 +1401,20 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
         for (int64_t off = static_cast<int64_t>(t) * 128; off + 128 <= tbytes; off += static_cast<int64_t>(n) * 128)
           asm volatile("discard.global.L2 [%0], 128;" ::"l"(in + j * chunk_bytes + off) : "memory");
     }
-    if (t == 0 && nd.nsucc > 0) {
-      fence_acq_rel(false);  // release the unit's data (gathered by the barrier) before the counts
-      for (int k = 0; k < nd.nsucc; ++k) {
-        const int32_t sn = a.df_succ[nd.succ + k];
-        int32_t* cnt = a.df_cnt + tile * nn + sn;
-        const int32_t need = a.df_nodes[sn].indeg;
-        if (atomicAdd(cnt, 1) + 1 == need) {  // the last predecessor: the item is ready
-          *cnt = 0;
-          const int32_t pos = atomicAdd(a.df_ctr + 1, 1);
-          __threadfence();
-          st_relaxed32(a.df_q + pos, static_cast<int32_t>(tile * nn + sn) + 1);
-        }
+    // publish, one successor per thread: release the unit's data (gathered by the barrier above),
+    // count the predecessor in; the last one pushes the ready item
+    for (int k = t; k < nd.nsucc; k += n) {
+      const DfSucc sc = a.df_succ[nd.succ + k];
+      int32_t* cnt = a.df_cnt + tile * nn + sc.node;
+      fence_acq_rel(false);
+      if (atomicAdd(cnt, 1) + 1 == sc.indeg) {
+        __threadfence();  // acquire the other predecessors' releases (read through the counter)
+        *cnt = 0;         // ready: reset for the next launch
+        const int32_t pos = atomicAdd(a.df_ctr + 1, 1);
+        st_release32(a.df_q + pos, static_cast<int32_t>(tile * nn + sc.node) + 1);
       }
     }
+    if (trace && t == 0) trace[item * 4 + 3] = globaltimer();
   }
 }
 

@@ -329,10 +329,10 @@ struct DevicePlan {  // one registered IR on one device
   bool sys_scope = false;
   // dataflow graph (every rank of the program in this launch): nodes in launch op order
   bool df_ok = false;
-  int df_n = 0, df_nroots = 0, df_mail_msgs = 0;
+  int df_n = 0, df_nroots = 0, df_mail_msgs = 0, df_depth = 1;
   int64_t df_mail_chunks = 0;  // mailbox size in chunks
   DfNode* d_df_nodes = nullptr;
-  int32_t* d_df_succ = nullptr;
+  DfSucc* d_df_succ = nullptr;
   int32_t* d_df_roots = nullptr;
 };
 
@@ -1250,7 +1250,8 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   // block, declared deps, message sender -> receiver; messages neither direct nor pulled get a
   // mailbox span each.
   std::vector<DfNode> df_nodes;
-  std::vector<int32_t> df_succ, df_roots;
+  std::vector<DfSucc> df_succ;
+  std::vector<int32_t> df_roots;
   plan.df_ok = false;
   plan.df_mail_chunks = 0;
   plan.df_mail_msgs = 0;
@@ -1259,14 +1260,20 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
     std::vector<int> indeg(ops.size(), 0);
     auto node = [&](int r, int t, int s) { return tbs[launch_index[{r, t}]].op_begin + s; };
     df_nodes.assign(ops.size(), DfNode{});
+    for (size_t v = 0; v < ops.size(); ++v) {
+      df_nodes[v].op = ops[v];
+      df_nodes[v].in_mail = df_nodes[v].out_mail = -1;
+    }
     for (int r : plan.ranks)
       for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
         const ThreadBlock& tb = p.gpus[r].tbs[t];
         for (size_t s = 0; s < tb.ops.size(); ++s) {
           const int v = node(r, static_cast<int>(t), static_cast<int>(s));
-          df_nodes[v].op = v;
+          const DevTb& dtb = tbs[launch_index[{r, static_cast<int>(t)}]];
           df_nodes[v].tbi = launch_index[{r, static_cast<int>(t)}];
-          df_nodes[v].in_mail = df_nodes[v].out_mail = -1;
+          df_nodes[v].rank_slot = static_cast<int8_t>(dtb.rank_slot);
+          df_nodes[v].peer_slot = static_cast<int8_t>(dtb.peer_slot);
+          df_nodes[v].recv_slot = static_cast<int8_t>(dtb.recv_slot);
           if (s > 0) succ[node(r, static_cast<int>(t), static_cast<int>(s) - 1)].insert(v);
           for (const Dep& dp : tb.ops[s].deps) succ[node(r, tb_index(p, r, dp.tb), dp.step)].insert(v);
           const auto& sd = senders[r][t][s];
@@ -1284,20 +1291,29 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       }
     bool fits = true;
     for (size_t u = 0; u < ops.size(); ++u) {
-      df_nodes[u].succ = static_cast<int32_t>(df_succ.size());
       df_nodes[u].nsucc = static_cast<int16_t>(succ[u].size());
       fits = fits && succ[u].size() < 32768;
-      for (int v : succ[u]) {
-        df_succ.push_back(v);
-        indeg[v]++;
-      }
+      for (int v : succ[u]) indeg[v]++;
+    }
+    for (size_t u = 0; u < ops.size(); ++u) {
+      df_nodes[u].succ = static_cast<int32_t>(df_succ.size());
+      for (int v : succ[u]) df_succ.push_back(DfSucc{v, indeg[v]});
     }
     for (size_t u = 0; u < ops.size(); ++u) {
       df_nodes[u].indeg = static_cast<int16_t>(indeg[u]);
       fits = fits && indeg[u] < 32768;
       if (indeg[u] == 0) df_roots.push_back(static_cast<int32_t>(u));
     }
-    plan.df_ok = fits && !df_roots.empty() && ops.size() < (1u << 20);
+    // average width of the graph (nodes / longest path): the ready items of one tile at a time
+    std::vector<int> level(ops.size(), 1);
+    std::vector<int> order(df_roots.begin(), df_roots.end()), deg(indeg);
+    for (size_t i = 0; i < order.size(); ++i)
+      for (int v : succ[order[i]]) {
+        level[v] = std::max(level[v], level[order[i]] + 1);
+        if (--deg[v] == 0) order.push_back(v);
+      }
+    plan.df_depth = order.empty() ? 1 : *std::max_element(level.begin(), level.end());
+    plan.df_ok = fits && !df_roots.empty() && order.size() == ops.size() && ops.size() < (1u << 20);
     plan.df_n = static_cast<int>(ops.size());
     plan.df_nroots = static_cast<int>(df_roots.size());
   }
@@ -1802,9 +1818,11 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     cp.fn = df_fn;
     cp.uniform = true;
     const int units = capacity;
-    const int64_t nn = ds.plans[id].df_n;
+    // enough tiles that the graph's average width (nodes / depth) x tiles gives every unit
+    // df_items ready items at a time
+    const int64_t width = std::max<int64_t>(1, ds.plans[id].df_n / std::max(1, ds.plans[id].df_depth));
     int64_t tb_bytes = c->cfg.tile_bytes > 0 ? c->cfg.tile_bytes
-                                              : chunk_bytes * nn / (static_cast<int64_t>(std::max(1, c->cfg.df_items)) * units);
+                                              : chunk_bytes * width / (static_cast<int64_t>(std::max(1, c->cfg.df_items)) * units);
     tb_bytes = std::min<int64_t>(std::max<int64_t>(tb_bytes, c->cfg.df_min_tile), c->cfg.df_max_tile);
     tb_bytes = std::max<int64_t>(tb_bytes / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
     if (chunk_bytes <= tb_bytes) tb_bytes = chunk_bytes;
@@ -1919,8 +1937,13 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     int max_nops = 0;
     for (int r : plan.ranks)
       for (const auto& tb : c0->irs[id]->prog.gpus[r].tbs) max_nops = std::max(max_nops, static_cast<int>(tb.ops.size()));
-    const int ops_per_block = static_cast<int>(std::min<int64_t>((cp.ntiles + cp.lanes - 1) / cp.lanes * max_nops, 1 << 20));
-    const size_t need = static_cast<size_t>(cp.weight) * cp.lanes * ops_per_block * 4 * sizeof(uint64_t);
+    int ops_per_block = static_cast<int>(std::min<int64_t>((cp.ntiles + cp.lanes - 1) / cp.lanes * max_nops, 1 << 20));
+    int rows = cp.weight * cp.lanes;
+    if (cp.df) {  // dataflow: one row per (node, tile) item: claim, ready, moved, published
+      rows = static_cast<int>(plan.df_n * cp.ntiles);
+      ops_per_block = 1;
+    }
+    const size_t need = static_cast<size_t>(rows) * ops_per_block * 4 * sizeof(uint64_t);
     DeviceGuard gt(dev);
     if (need > ds->trace_bytes) {
       if (ds->d_trace) cudaFree(ds->d_trace);
@@ -1932,7 +1955,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     CUDA_TRY(cudaMemsetAsync(ds->d_trace, 0, need, p0.stream));
     a.trace = ds->d_trace;
     a.trace_ops = ops_per_block;
-    ds->trace_grid = cp.weight * cp.lanes;
+    ds->trace_grid = rows;
     ds->trace_ops = ops_per_block;
     ds->trace_lanes = cp.lanes;
   }
