@@ -547,6 +547,149 @@ done:
   return rc;
 }
 
+/* ---- race detection ("happens-before race detection over (rank, buffer,
+ * index) slots", "vector clocks over block steps, comm edges, and semaphore edges") ------------
+ * One dry deterministic run: every thread block carries a vector clock (ops completed per thread
+ * block); a message carries its sender's clock (comm edge, k-th send -> k-th receive), a dep joins
+ * the clock the depended-on op published (semaphore edge).  Every local access of a chunk slot is
+ * checked against the slot's last write and the reads since: two accesses conflict when at least
+ * one writes and neither clock has seen the other.  In-place programs alias output onto input
+ * (core.hpp:167-170). */
+typedef struct {
+  int tb, clk, step; /* accessor, its own clock after the op (1-based op count), its step */
+} acc_t;
+typedef struct {
+  acc_t w;      /* last write (tb < 0: none) */
+  acc_t* rd;    /* reads since the last write */
+  int nrd, cap;
+} slot_t;
+
+static void race_add(gc3o_race* out, int max, int* n, const gc3o_program* p, const ctx_t* c, int rank, int buf, int idx,
+                     acc_t a, acc_t b, int kind) {
+  if (*n < max && out) {
+    gc3o_race* r = &out[*n];
+    r->rank = rank, r->buf = buf, r->index = idx, r->kind = kind;
+    r->tb_a = a.tb - c->tb_base[rank], r->step_a = a.step;
+    r->tb_b = b.tb - c->tb_base[rank], r->step_b = b.step;
+  }
+  (*n)++;
+  (void)p;
+}
+
+int gc3o_races(const gc3o_program* p, gc3o_race* out, int max, char* err, size_t errlen) {
+  ctx_t c;
+  if (err && errlen) err[0] = 0;
+  if (ctx_init(&c, p, NULL, 1, 7 /* f32: dry run */, 0, 0, err, errlen)) { ctx_free(&c); return -1; }
+  const int nt = p->ntbs;
+  int nops = 0;
+  for (int t = 0; t < nt; t++) nops += p->tbs[t].nops;
+  int* vc = calloc((size_t)nt * nt, sizeof(int));                  /* current clock per tb */
+  int* snap = calloc((size_t)(nops + 1) * nt, sizeof(int));        /* clock after every op */
+  int* pc = calloc(nt, sizeof(int));
+  /* per connection: FIFO of sender clocks (unbounded, k-th send -> k-th receive) */
+  int** fifo = calloc(c.nconn + 1, sizeof(int*));
+  int* fhead = calloc(c.nconn + 1, sizeof(int));
+  int* ftail = calloc(c.nconn + 1, sizeof(int));
+  int* fcap = calloc(c.nconn + 1, sizeof(int));
+  /* slots: per rank, buffers 0..2 x nchunks */
+  const int nslot_rank = p->nchunks[0] + p->nchunks[1] + p->nchunks[2];
+  slot_t* slots = calloc((size_t)p->nranks * nslot_rank + 1, sizeof(slot_t));
+  for (int i = 0; i < p->nranks * nslot_rank; i++) slots[i].w.tb = -1;
+  int nraces = 0, rc = 0;
+  for (;;) {
+    int progress = 0, all_done = 1;
+    for (int t = 0; t < nt; t++) {
+      const gc3o_tb* tb = &p->tbs[t];
+      if (pc[t] >= tb->nops) continue;
+      all_done = 0;
+      const gc3o_op* op = &p->ops[tb->first_op + pc[t]];
+      int ok = 1;
+      for (int d = 0; d < op->ndeps && ok; d++) {
+        const int dt = c.tb_base[tb->rank] + op->dep_tb[d];
+        if (pc[dt] <= op->dep_step[d]) ok = 0;
+      }
+      if (ok && receives(op->opcode) && fhead[c.conn_in[t]] == ftail[c.conn_in[t]]) ok = 0;
+      if (!ok) continue;
+      int* me = vc + (size_t)t * nt;
+      for (int d = 0; d < op->ndeps; d++) { /* semaphore edge */
+        const int dt = c.tb_base[tb->rank] + op->dep_tb[d];
+        const int* s = snap + (size_t)(p->tbs[dt].first_op + op->dep_step[d]) * nt;
+        for (int k = 0; k < nt; k++) if (s[k] > me[k]) me[k] = s[k];
+      }
+      if (receives(op->opcode)) { /* comm edge */
+        const int ci = c.conn_in[t];
+        const int* s = fifo[ci] + (size_t)fhead[ci]++ * nt;
+        for (int k = 0; k < nt; k++) if (s[k] > me[k]) me[k] = s[k];
+      }
+      me[t] = pc[t] + 1;
+      /* local accesses (lowering.hpp:96-119): reads first, then writes */
+      int rb[2] = {-1, -1}, ro[2] = {0, 0}, wb = -1, wo = 0, nr = 0;
+      switch (op->opcode) {
+        case GC3O_SEND: case GC3O_RRS: rb[nr] = op->src_buf, ro[nr++] = op->src_off; break;
+        case GC3O_RECV: wb = op->dst_buf, wo = op->dst_off; break;
+        case GC3O_COPY: case GC3O_RRC: rb[nr] = op->src_buf, ro[nr++] = op->src_off; wb = op->dst_buf, wo = op->dst_off; break;
+        case GC3O_REDUCE:
+          rb[nr] = op->src_buf, ro[nr++] = op->src_off;
+          rb[nr] = op->dst_buf, ro[nr++] = op->dst_off;
+          wb = op->dst_buf, wo = op->dst_off;
+          break;
+        case GC3O_RCS: wb = op->src_buf, wo = op->src_off; break;
+        case GC3O_RRCS: rb[nr] = op->src_buf, ro[nr++] = op->src_off; wb = op->src_buf, wo = op->src_off; break;
+        default: break;
+      }
+      const acc_t cur = {t, me[t], pc[t]};
+      for (int i = 0; i <= nr; i++) {
+        const int is_write = i == nr;
+        const int b = is_write ? wb : rb[i];
+        const int off = is_write ? wo : ro[i];
+        if (b < 0) continue;
+        const int sb = (p->inplace && b == GC3O_OUTPUT) ? GC3O_INPUT : b;
+        const int base = sb == 0 ? 0 : sb == 1 ? p->nchunks[0] : p->nchunks[0] + p->nchunks[1];
+        for (int j = 0; j < op->count; j++) {
+          slot_t* s = &slots[(size_t)tb->rank * nslot_rank + base + off + j];
+          if (s->w.tb >= 0 && s->w.tb != t && me[s->w.tb] < s->w.clk)
+            race_add(out, max, &nraces, p, &c, tb->rank, sb, off + j, s->w, cur, is_write ? 0 : 1);
+          if (is_write) {
+            for (int k = 0; k < s->nrd; k++)
+              if (s->rd[k].tb != t && me[s->rd[k].tb] < s->rd[k].clk)
+                race_add(out, max, &nraces, p, &c, tb->rank, sb, off + j, s->rd[k], cur, 2);
+            s->w = cur;
+            s->nrd = 0;
+          } else {
+            if (s->nrd == s->cap) {
+              s->cap = s->cap ? 2 * s->cap : 4;
+              s->rd = realloc(s->rd, sizeof(acc_t) * s->cap);
+            }
+            s->rd[s->nrd++] = cur;
+          }
+        }
+      }
+      if (sends(op->opcode)) {
+        const int co = c.conn_out[t];
+        if (ftail[co] == fcap[co]) {
+          fcap[co] = fcap[co] ? 2 * fcap[co] : 8;
+          fifo[co] = realloc(fifo[co], sizeof(int) * (size_t)fcap[co] * nt);
+        }
+        memcpy(fifo[co] + (size_t)ftail[co]++ * nt, me, sizeof(int) * nt);
+      }
+      memcpy(snap + (size_t)(tb->first_op + pc[t]) * nt, me, sizeof(int) * nt);
+      pc[t]++;
+      progress = 1;
+    }
+    if (all_done) break;
+    if (!progress) {
+      set_err(err, errlen, "deadlock: the program cannot complete, races undetermined");
+      rc = -1;
+      break;
+    }
+  }
+  for (int i = 0; i < p->nranks * nslot_rank; i++) free(slots[i].rd);
+  for (int i = 0; i < c.nconn; i++) free(fifo[i]);
+  free(slots); free(fifo); free(fhead); free(ftail); free(fcap); free(vc); free(snap); free(pc);
+  ctx_free(&c);
+  return rc < 0 ? rc : nraces;
+}
+
 int gc3o_run(const gc3o_program* p, void* const* bufs, size_t chunk_elems, int dtype, int redop,
              int mode, uint64_t seed, int slots, size_t tile_elems, char* err, size_t errlen) {
   ctx_t c;

@@ -82,6 +82,18 @@ int gc3o_reduce(void* a, const void* b, size_t n, int dtype, int redop);
 
 size_t gc3o_dtype_size(int dtype);
 
+/* One conflicting pair of accesses to chunk slot (rank, buf, index): accesses (tb_a, step_a) and
+ * (tb_b, step_b) of that rank, unordered by happens-before.  kind: 0 write/write, 1 write then
+ * read, 2 read then write. */
+typedef struct {
+  int32_t rank, buf, index, kind, tb_a, step_a, tb_b, step_b;
+} gc3o_race;
+
+/* Vector-clock race detection over block steps, message edges (k-th send
+ * -> k-th receive) and dep (semaphore) edges.  Fills up to `max` pairs into `out`; returns the
+ * number of conflicting pairs found, or -1 (err set) for a malformed or deadlocking program. */
+int gc3o_races(const gc3o_program* p, gc3o_race* out, int max, char* err, size_t errlen);
+
 #ifdef __cplusplus
 }
 #endif

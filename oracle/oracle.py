@@ -43,6 +43,12 @@ class Program(ctypes.Structure):
                 ("ops", ctypes.POINTER(Op)), ("nchunks", ctypes.c_int32 * 3), ("inplace", ctypes.c_int32)]
 
 
+class Race(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int32) for k in ("rank", "buf", "index", "kind", "tb_a", "step_a", "tb_b", "step_b")]
+
+
+RACE_KINDS = ("write/write", "write/read", "read/write")
+
 _lib = None
 
 
@@ -60,6 +66,9 @@ def lib():
         _lib.gc3o_run.restype = ctypes.c_int
         _lib.gc3o_reduce.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int, ctypes.c_int]
         _lib.gc3o_reduce.restype = ctypes.c_int
+        _lib.gc3o_races.argtypes = [ctypes.POINTER(Program), ctypes.POINTER(Race), ctypes.c_int, ctypes.c_char_p,
+                                    ctypes.c_size_t]
+        _lib.gc3o_races.restype = ctypes.c_int
     return _lib
 
 
@@ -112,6 +121,22 @@ class FlatIR:
         rc = lib().gc3o_run(ctypes.byref(self.prog), arr, chunk_elems, dt, op, MODES[mode], seed, slots, tile_elems,
                             err, 512)
         return rc, err.value.decode()
+
+    def races(self, max_pairs=64):
+        """Vector-clock race detection (gc3o_races): a list of dicts naming each conflicting pair of
+        accesses to one (rank, buffer, chunk) slot, unordered by happens-before. Raises ValueError
+        for a malformed or deadlocking program."""
+        out = (Race * max_pairs)()
+        err = ctypes.create_string_buffer(512)
+        n = lib().gc3o_races(ctypes.byref(self.prog), out, max_pairs, err, 512)
+        if n < 0:
+            raise ValueError(err.value.decode())
+        names = {v: k for k, v in BUFS.items()}
+        res = []
+        for r in out[:min(n, max_pairs)]:
+            res.append({"rank": r.rank, "buf": names[r.buf], "index": r.index, "kind": RACE_KINDS[r.kind],
+                        "a": (r.tb_a, r.step_a), "b": (r.tb_b, r.step_b)})
+        return res if n <= max_pairs else res + [{"truncated": n}]
 
 
 def reduce_arrays(a, b, dtype, redop="sum"):
