@@ -200,6 +200,11 @@ ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);
 /* The built-in program the runtime uses for `collective` ("allreduce", "allgather", "reducescatter",
  * "alltoall") on nranks ranks when no registered IR matches a call (see gc3RegisterIR). */
 ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir);
+/* Comm-time program generation (compiler in the loop): algo "ring" (allreduce on
+ * `channels` rings, chunk k on channel k % channels; allgather / reducescatter on one), "allpairs"
+ * (allreduce) or "direct" (alltoall), replicated into `instances` instances -- the reference
+ * compiler's parallelize(k) (program.hpp:366-419). ncclInvalidArgument for other combinations. */
+ncclResult_t gc3IrGenerate(const char* algo, const char* collective, int nranks, int channels, int instances, gc3Ir_t* ir);
 /* Timed model (SPEC.md:464-481 run_timed, as an alpha-beta model over the happens-before graph,
  * calibrated on a B200 in loopback): predicted microseconds of one launch of the program with chunks
  * of chunk_bytes, protocol (0 simple, 1 ll) and `lanes` lanes per thread block. */

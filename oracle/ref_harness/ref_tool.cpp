@@ -386,11 +386,107 @@ char* ref_symbolic(const char* text) {
 	return dup_string(out.dump());
 }
 
+// Parametric generators for the runtime's built-in program families (tests/test_builtin_irs.py):
+//   gen_ring_ar_R_C_K   ring AllReduce, chunk r on channel r % C, parallelize(K)
+//   gen_allpairs_ar_R   all-pairs AllReduce
+//   gen_hier_ar_N_G_P   hierarchical AllReduce N nodes x G GPUs, parallelize(P)
+//   gen_ring_ag_R_K / gen_ring_rs_R_K   ring AllGather / ReduceScatter, parallelize(K)
+gen_fn param_generator(const std::string& name) {
+	std::vector<int> v;
+	std::string kind;
+	{
+		std::string s = name.substr(4);
+		size_t i = 0;
+		while(i < s.size() && !std::isdigit(static_cast<unsigned char>(s[i]))) kind += s[i++];
+		while(i < s.size()) {
+			size_t j = i;
+			while(j < s.size() && std::isdigit(static_cast<unsigned char>(s[j]))) ++j;
+			v.push_back(std::stoi(s.substr(i, j - i)));
+			i = j + 1;
+		}
+	}
+	if(kind == "ring_ar_" && v.size() == 3) {
+		const int R = v[0], C = v[1], K = v[2];
+		return [R, C, K, name](bool fused, protocol proto) {
+			program_builder b(allreduce_spec(R, R), name);
+			b.parallelize(K, [&] {
+				for(int r = 0; r < R; ++r) {
+					auto x = b.chunk((r + 1) % R, buffer::input, r);
+					for(int s = 1; s < R; ++s) x = b.chunk((s + r + 1) % R, buffer::input, r).reduce(x, ch_dir(r % C));
+				}
+				for(int r = 0; r < R; ++r) {
+					auto x = b.chunk(r, buffer::input, r);
+					for(int s = 1; s < R; ++s) x = x.copy((s + r) % R, buffer::input, r, ch_dir(r % C));
+				}
+			});
+			return compile(b, make_topo(1, R), fused, proto);
+		};
+	}
+	if(kind == "allpairs_ar_" && v.size() == 1) {
+		const int R = v[0];
+		return [R, name](bool fused, protocol proto) {
+			program_builder b(allreduce_spec(R, R), name);
+			for(int r = 0; r < R; ++r)
+				for(int q = 0; q < R; ++q)
+					if(q != r) b.chunk(r, buffer::input, r).reduce(b.chunk(q, buffer::input, r));
+			for(int r = 0; r < R; ++r)
+				for(int q = 0; q < R; ++q)
+					if(q != r) b.chunk(r, buffer::input, r).copy(q, buffer::input, r);
+			return compile(b, make_topo(1, R), fused, proto);
+		};
+	}
+	if(kind == "hier_ar_" && v.size() == 3) {
+		const int N = v[0], G = v[1], par = v[2];
+		return [N, G, par, name](bool fused, protocol proto) {
+			const int a = 0, bch = par, c = 2 * par;
+			program_builder b(allreduce_spec(N * G, N * G), name);
+			for(int n = 0; n < N; ++n) b.parallelize(par, [&] { RS(b, iota_ranks(G, n * G), 0, N, a); });
+			for(int gg = 0; gg < G; ++gg) {
+				std::vector<int> cross;
+				for(int n = 0; n < N; ++n) cross.push_back(n * G + gg);
+				RS(b, cross, gg * N, 1, bch);
+				AG(b, cross, gg * N, 1, bch);
+			}
+			for(int n = 0; n < N; ++n) b.parallelize(par, [&] { AG(b, iota_ranks(G, n * G), 0, N, c); });
+			return compile(b, make_topo(N, G), fused, proto);
+		};
+	}
+	if((kind == "ring_ag_" || kind == "ring_rs_") && v.size() == 2) {
+		const int R = v[0], K = v[1];
+		const bool ag = kind == "ring_ag_";
+		return [R, K, ag, name](bool fused, protocol proto) {
+			program_builder b(ag ? allgather_spec(R, 1) : reducescatter_spec(R, 1), name);
+			b.parallelize(K, [&] {
+				for(int r = 0; r < R; ++r) {
+					if(ag) {
+						auto x = b.chunk(r, buffer::input, 0).copy(r, buffer::output, r);
+						for(int s = 1; s < R; ++s) x = x.copy((r + s) % R, buffer::output, r);
+					} else {
+						auto x = b.chunk((r + 1) % R, buffer::input, r);
+						for(int s = 2; s <= R; ++s) x = b.chunk((r + s) % R, buffer::input, r).reduce(x);
+					}
+				}
+			});
+			return compile(b, make_topo(1, R), fused, proto);
+		};
+	}
+	return nullptr;
+}
+
 /// Compiles one named fixture with the reference compiler. proto: 0 simple, 1 ll, 2 ll128.
 char* ref_compile(const char* name, int fused, int proto) {
 	const auto gens = generators();
-	const auto it = gens.find(name);
-	if(it == gens.end()) return nullptr;
+	auto it = gens.find(name);
+	gen_fn param;
+	if(it == gens.end() && std::string(name).rfind("gen_", 0) == 0) param = param_generator(name);
+	if(it == gens.end() && !param) return nullptr;
+	if(param) {
+		try {
+			return dup_string(param(fused != 0, static_cast<protocol>(proto)));
+		} catch(const std::exception& e) {
+			return dup_string(std::string("ERROR: ") + e.what());
+		}
+	}
 	try {
 		return dup_string(it->second(fused != 0, static_cast<protocol>(proto)));
 	} catch(const std::exception& e) {

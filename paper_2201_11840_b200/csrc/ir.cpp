@@ -502,7 +502,7 @@ Program replicate_instances(const Program& p, int k) {
   return q;
 }
 
-bool builtin_program(const std::string& collective, int R, Program& out) {
+bool builtin_program(const std::string& collective, int R, Program& out, int channels) {
   if (R < 2) return false;
   auto mod = [R](int x) { return ((x % R) + R) % R; };
   Program p;
@@ -537,6 +537,35 @@ bool builtin_program(const std::string& collective, int R, Program& out) {
         g.tbs.push_back(tb);
         ++id;
       }
+    } else if (collective == "allreduce") {
+      // ring, one thread block per channel: chunk k travels on channel k % C. Chunk k is sent raw by
+      // rank k+1 and reduced along the ring (RS step s = (r - k - 1) mod R at rank r; the rank
+      // before the owner forwards the sum without storing it: rrs), completed by its owner k
+      // (rrcs) and forwarded around (AG step a = (r - k) mod R). A thread block runs its chunks'
+      // ops in global ring-step order (RS steps 0..R-1, then AG steps R..2R-2): the order the
+      // reference scheduler gives these programs.
+      const int C = std::max(1, std::min(channels, R));
+      for (int ch = 0; ch < C; ++ch) {
+        ThreadBlock tb;
+        tb.id = ch;
+        tb.send_peer = mod(r + 1);
+        tb.recv_peer = mod(r - 1);
+        tb.channel = ch;
+        std::vector<std::pair<int, Op>> steps;
+        for (int k = ch; k < R; k += C) {
+          const int s = mod(r - k - 1);
+          const Opcode rs = s == 0 ? Opcode::send : (s == R - 2 && R >= 3) ? Opcode::rrs : Opcode::rrcs;
+          steps.push_back({s, op(0, rs, Buf::input, k, Buf::input, k)});
+          const int ag = mod(r - k);
+          if (ag >= 1) steps.push_back({R - 1 + ag, op(0, ag == R - 1 ? Opcode::recv : Opcode::rcs, Buf::input, k, Buf::input, k)});
+        }
+        std::sort(steps.begin(), steps.end(), [](const auto& x, const auto& y) { return x.first < y.first; });
+        for (auto& [gs, o] : steps) {
+          o.step = static_cast<int>(tb.ops.size());
+          tb.ops.push_back(o);
+        }
+        g.tbs.push_back(tb);
+      }
     } else {  // ring: send to r+1, receive from r-1
       ThreadBlock tb;
       tb.id = 0;
@@ -545,20 +574,7 @@ bool builtin_program(const std::string& collective, int R, Program& out) {
       tb.channel = 0;
       int s = 0;
       auto same = [&](Opcode o, Buf b, int c) { tb.ops.push_back(op(s++, o, b, mod(c), b, mod(c))); };
-      if (collective == "allreduce") {
-        // chunk c: sent raw by rank c+1, reduced along the ring (the rank before its owner forwards the
-        // sum without storing it: rrs), completed by rank c, then forwarded around to every rank
-        same(Opcode::send, Buf::input, r - 1);
-        if (R == 2) {
-          same(Opcode::rrcs, Buf::input, r);
-        } else {
-          for (int k = 1; k <= R - 3; ++k) same(Opcode::rrcs, Buf::input, r - 1 - k);
-          same(Opcode::rrs, Buf::input, r + 1);
-          same(Opcode::rrcs, Buf::input, r);
-          for (int k = 0; k <= R - 3; ++k) same(Opcode::rcs, Buf::input, r - 1 - k);
-        }
-        same(Opcode::recv, Buf::input, r + 1);
-      } else if (collective == "allgather") {
+      if (collective == "allgather") {
         tb.ops.push_back(op(s++, Opcode::copy, Buf::input, 0, Buf::output, r));
         same(Opcode::send, Buf::output, r);
         for (int k = 1; k <= R - 2; ++k) same(Opcode::rcs, Buf::output, r - k);
@@ -584,6 +600,83 @@ bool builtin_program(const std::string& collective, int R, Program& out) {
     p.nchunks[0] = p.nchunks[1] = R;
   }
   p.name = "builtin_" + collective + "_" + std::to_string(R);
+  out = std::move(p);
+  return true;
+}
+
+// All-pairs AllReduce (two communication steps instead of Ring's 2R-2). Rank r
+// owns chunk r; one thread block per peer q (send and receive peer q, channel 0) runs: send chunk q
+// (r's contribution to q's chunk), rrc chunk r (q's contribution, reduced in), send chunk r (the
+// final value, back to q), recv chunk q (q's final value). The reductions into chunk r are chained
+// across the thread blocks with deps (one writer at a time) and every final send waits for the
+// last one. Equivalent to the reference compiler's all-pairs program (same final state, race free:
+// tests/test_builtin_irs.py), not its exact thread-block layout: that one fuses the last
+// reduction with the first final send (rrcs) and orders blocks by its scheduler's heuristics.
+static bool allpairs_allreduce(int R, Program& out) {
+  if (R < 2) return false;
+  Program p;
+  p.collective = "allreduce";
+  p.proto = Proto::simple;
+  p.inplace = true;
+  p.nchunks[0] = p.nchunks[1] = R;
+  for (int r = 0; r < R; ++r) {
+    Gpu g;
+    g.rank = r;
+    std::vector<int> peers;
+    for (int q = 0; q < R; ++q)
+      if (q != r) peers.push_back(q);
+    const int last = static_cast<int>(peers.size()) - 1;
+    for (int i = 0; i <= last; ++i) {
+      const int q = peers[i];
+      ThreadBlock tb;
+      tb.id = i;
+      tb.send_peer = tb.recv_peer = q;
+      tb.channel = 0;
+      auto mk = [&](Opcode o, int chunk) {
+        Op x;
+        x.step = static_cast<int>(tb.ops.size());
+        x.op = o;
+        x.src_buf = x.dst_buf = Buf::input;
+        x.src_off = x.dst_off = chunk;
+        x.count = 1;
+        return x;
+      };
+      tb.ops.push_back(mk(Opcode::send, q));
+      Op red = mk(Opcode::rrc, r);
+      if (i > 0) red.deps.push_back({i - 1, 1});
+      red.has_dep = true;  // the next reduction (or the final sends) wait on it
+      tb.ops.push_back(red);
+      Op fin = mk(Opcode::send, r);
+      if (i != last) fin.deps.push_back({last, 1});
+      tb.ops.push_back(fin);
+      tb.ops.push_back(mk(Opcode::recv, q));
+      g.tbs.push_back(tb);
+    }
+    p.gpus.push_back(std::move(g));
+  }
+  p.name = "builtin_allpairs_allreduce_" + std::to_string(R);
+  out = std::move(p);
+  return true;
+}
+
+bool generate_program(const std::string& algo, const std::string& collective, int R, int channels, int instances, Program& out) {
+  if (R < 2 || channels < 1 || instances < 1 || instances > 64) return false;
+  Program p;
+  if (algo == "ring") {
+    if (collective == "alltoall" || (channels > 1 && collective != "allreduce")) return false;
+    if (!builtin_program(collective, R, p, channels)) return false;
+  } else if (algo == "direct") {
+    if (collective != "alltoall" || channels != 1) return false;
+    if (!builtin_program(collective, R, p)) return false;
+  } else if (algo == "allpairs") {
+    if (collective != "allreduce" || channels != 1) return false;
+    if (!allpairs_allreduce(R, p)) return false;
+  } else {
+    return false;
+  }
+  if (instances > 1) p = replicate_instances(p, instances);
+  p.name = "builtin_" + algo + "_" + collective + "_" + std::to_string(R) + "_ch" + std::to_string(channels) + "_inst" +
+           std::to_string(instances);
   out = std::move(p);
   return true;
 }

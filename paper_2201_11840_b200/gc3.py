@@ -93,6 +93,7 @@ def lib():
         "gc3IrSourceReads": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrResultWrites": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrBuiltin": [cp, i, ctypes.POINTER(vp)],
+        "gc3IrGenerate": [cp, cp, i, i, i, ctypes.POINTER(vp)],
         "gc3IrPredict": [vp, ctypes.c_int64, i, i, ctypes.POINTER(ctypes.c_double)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
@@ -150,6 +151,14 @@ class IR:
         """The runtime's built-in program for `collective` on nranks ranks."""
         h = ctypes.c_void_p()
         check(lib().gc3IrBuiltin(collective.encode(), nranks, ctypes.byref(h)))
+        return cls._wrap(h)
+
+    @classmethod
+    def generate(cls, algo, collective, nranks, channels=1, instances=1):
+        """A program generated at communicator time: algo "ring" / "allpairs" / "direct" with
+        `channels` rings and `instances` instances (gc3IrGenerate)."""
+        h = ctypes.c_void_p()
+        check(lib().gc3IrGenerate(algo.encode(), collective.encode(), nranks, channels, instances, ctypes.byref(h)))
         return cls._wrap(h)
 
     @classmethod

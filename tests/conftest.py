@@ -72,6 +72,16 @@ def reflib():
             import json
             return json.loads(self._take(L.ref_check_slots(text.encode(), slots)))
 
+        def compile(self, name, fused=True, proto=0):
+            import json
+            p = L.ref_compile(name.encode(), int(fused), proto)
+            if not p:
+                raise KeyError(name)
+            s = self._take(p)
+            if s.startswith("ERROR"):
+                raise RuntimeError(s)
+            return json.loads(s)
+
         def symbolic(self, text):
             import json
             return json.loads(self._take(L.ref_symbolic(text.encode())))
