@@ -23,10 +23,10 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CXX_SRCS = ["json.cpp", "ir.cpp", "msccl_xml.cpp", "runtime.cpp"]
+CXX_SRCS = ["json.cpp", "ir.cpp", "msccl_xml.cpp", "timed.cpp", "runtime.cpp"]
 CU_SRCS = ["interp_launch.cu", "interp_k_copy.cu", "interp_k_sum.cu", "interp_k_prod.cu", "interp_k_max.cu", "interp_k_min.cu",
            "interp_k_sum_df.cu", "interp_k_prod_df.cu", "interp_k_max_df.cu", "interp_k_min_df.cu"]
-HEADERS = ["json.hpp", "ir.hpp", "msccl_xml.hpp", "devplan.hpp", "interp.cuh"]
+HEADERS = ["json.hpp", "ir.hpp", "msccl_xml.hpp", "timed.hpp", "devplan.hpp", "interp.cuh"]
 
 ORACLE_DIR = os.path.join(REPO, "oracle")
 ORACLE_LIB = os.path.join(ORACLE_DIR, "liboracle.so")
