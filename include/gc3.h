@@ -132,6 +132,9 @@ typedef struct {
   int group;          /* tiles per op-major group inside a lane */
   int mode;           /* 0: static lanes, 1: work queue, 2: dataflow (ready (op, tile) items) */
   int mail_messages;  /* dataflow: messages carried through the launch's mailbox */
+  int remote_messages; /* direct / pulled receives whose sender runs in another launch (registered user buffers) */
+  int sys_scope;      /* 1: some thread block has a connection to another GPU (.sys fences there) */
+  int tma_stages;     /* bulk-copy stages per unit (0: register path only) */
 } gc3PlanInfo;
 /* collective: 0 allreduce, 1 allgather, 2 reducescatter, 3 alltoall; count as in the NCCL call. */
 ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDataType_t datatype, gc3PlanInfo* info);
@@ -209,6 +212,41 @@ ncclResult_t gc3IrGenerate(const char* algo, const char* collective, int nranks,
  * calibrated on a B200 in loopback): predicted microseconds of one launch of the program with chunks
  * of chunk_bytes, protocol (0 simple, 1 ll) and `lanes` lanes per thread block. */
 ncclResult_t gc3IrPredict(gc3Ir_t ir, int64_t chunk_bytes, int protocol, int lanes, double* us);
+/* Timed simulator (SPEC.md:464-481 run_timed / sweep): discrete-event alpha-beta model with chunk
+ * tiling; a message on an ordered GPU pair costs alpha + bytes / bandwidth of its link class (0 same
+ * GPU, 1 same node, 2 other node), concurrent messages on one pair share its bandwidth (processor
+ * sharing); local reductions cost bytes / gamma. gc3SimDefaults fills the B200 calibration. */
+typedef struct {
+  int nranks_gpu;          /* entries of rank_gpu (0: rank r on GPU r) */
+  const int* rank_gpu;     /* GPU of each rank (e.g. all 0: loopback on one GPU) */
+  int gpus_per_node;
+  double alpha_us[3];      /* per message, per link class */
+  double gbps[3];          /* bandwidth of one ordered GPU pair, per link class */
+  double gamma_gbps;       /* local reduction rate */
+  double copy_gbps;        /* local copy rate */
+  int protocol;            /* 0 simple, 1 ll, 2 ll128 (alpha x 1 / 0.25 / 0.5, beta x 1 / 2 / 1.07) */
+  int slots;               /* FIFO slots per connection (0: the protocol's, 2 / 8 / 4) */
+  int64_t chunk_bytes;
+  int64_t tile_bytes;      /* 0: one tile per chunk */
+  double launch_us;        /* added to the makespan */
+  double hbm_gbps;         /* 0: off (SPEC); else local reads/writes and same-GPU messages share one
+                              processor-shared device-memory resource per GPU of this rate */
+  int lanes;               /* units per thread block, lane l taking tiles l, l + lanes, ... (0 or 1: one) */
+  int group;               /* tiles per op-major group inside a lane (0 or 1: tile-major, Fig. 4) */
+} gc3SimConfig;
+typedef struct {
+  int completed;           /* 0: deadlock (see `deadlock`) */
+  double makespan_us;
+  double util[3];          /* mean busy fraction of the ordered GPU pairs used, per link class */
+  int64_t messages;
+  int64_t tiles;
+  char deadlock[256];
+} gc3SimReport;
+ncclResult_t gc3SimDefaults(gc3SimConfig* cfg);
+ncclResult_t gc3IrSimulate(gc3Ir_t ir, const gc3SimConfig* cfg, gc3SimReport* report);
+/* one run per size (bytes of a rank's input buffer); *csv = "size_bytes,makespan_us,util_intra,util_inter"
+ * rows (free with gc3Free) */
+ncclResult_t gc3IrSweep(gc3Ir_t ir, const gc3SimConfig* cfg, const int64_t* sizes, int nsizes, int64_t tile_bytes, char** csv);
 ncclResult_t gc3IrFree(gc3Ir_t ir);
 void gc3Free(void* p);
 

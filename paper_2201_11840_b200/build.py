@@ -27,6 +27,7 @@ CXX_SRCS = ["json.cpp", "ir.cpp", "msccl_xml.cpp", "timed.cpp", "runtime.cpp"]
 CU_SRCS = ["interp_launch.cu", "interp_k_copy.cu", "interp_k_sum.cu", "interp_k_prod.cu", "interp_k_max.cu", "interp_k_min.cu",
            "interp_k_sum_df.cu", "interp_k_prod_df.cu", "interp_k_max_df.cu", "interp_k_min_df.cu"]
 HEADERS = ["json.hpp", "ir.hpp", "msccl_xml.hpp", "timed.hpp", "devplan.hpp", "interp.cuh"]
+CU_HEADERS = ["devplan.hpp", "interp.cuh"]
 
 ORACLE_DIR = os.path.join(REPO, "oracle")
 ORACLE_LIB = os.path.join(ORACLE_DIR, "liboracle.so")
@@ -78,10 +79,11 @@ def build(force=False, verbose=False):
         if force or _newer(obj, [src] + hdrs):
             jobs.append(["g++", "-std=c++17", "-O2", "-g", "-fPIC", "-fvisibility=hidden", "-Wall", "-Wextra",
                          "-Wno-unused-parameter", "-I" + os.path.join(CUDA, "include"), *NVCC_DEFS, "-c", src, "-o", obj])
+    cu_hdrs = [os.path.join(CSRC, h) for h in CU_HEADERS]  # what the kernels include
     for s in CU_SRCS:
         src, obj = os.path.join(CSRC, s), os.path.join(BUILD, s + ".o")
         objs.append(obj)
-        if force or _newer(obj, [src] + hdrs):
+        if force or _newer(obj, [src] + cu_hdrs):
             jobs.append([NVCC, *ARCH, "-std=c++17", "-O3", "-lineinfo", "-Xptxas", "-v", "-Xcompiler", "-fPIC",
                          "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr", *NVCC_DEFS, "-c", src, "-o", obj])
     logs = []

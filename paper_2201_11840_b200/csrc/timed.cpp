@@ -17,7 +17,8 @@ struct SimTb {
   int rank = 0;
   const ThreadBlock* tb = nullptr;
   int conn_in = -1, conn_out = -1;
-  int64_t pos = 0;    // (tile, step) positions completed, tile-major
+  int lane = 0;
+  int64_t pos = 0;    // (tile of the lane, step) positions completed, tile-major
   int64_t total = 0;  // tiles x ops
   bool running = false;
 };
@@ -38,16 +39,28 @@ struct SimLink {
   double busy_us = 0.0;
 };
 
-enum Phase { kLocal, kAlpha, kXfer };
+enum Phase { kLocal, kLocalFlow, kAlpha, kXfer };
 
 struct Running {
   int tb;
   Phase phase;
   double end_us;     // kLocal / kAlpha: phase end
-  double remaining;  // kXfer: bytes left
+  double remaining;  // kLocalFlow / kXfer: bytes left on resource `res`
   double bytes;      // message bytes
-  int link;
+  int link;          // transfer resource (-1: the op sends nothing)
+  int res;           // resource of the current flow
+  double local;      // local bytes (device-memory resource on)
+  int hbm;           // device-memory resource of the op's GPU (-1: off)
 };
+
+int local_passes(Opcode o) {
+  switch (o) {
+    case Opcode::send: case Opcode::recv: case Opcode::rcs: case Opcode::rrs: return 1;
+    case Opcode::copy: case Opcode::rrc: case Opcode::rrcs: return 2;
+    case Opcode::reduce: return 3;
+    default: return 0;
+  }
+}
 
 }  // namespace
 
@@ -81,6 +94,18 @@ SimReport simulate(const Program& p, const SimParams& sp) {
     links.push_back(l);
     return link_id[key] = static_cast<int>(links.size()) - 1;
   };
+  std::map<int, int> hbm_id;  // GPU -> device-memory resource
+  auto hbm_of = [&](int g) {
+    if (sp.hbm_gbps <= 0) return -1;
+    auto f = hbm_id.find(g);
+    if (f != hbm_id.end()) return f->second;
+    SimLink l;
+    l.cls = 3;
+    l.gbps = sp.hbm_gbps;
+    l.alpha_us = sp.alpha_us[0] * sp.alpha_mult[pr];  // same-GPU messages routed here keep their alpha
+    links.push_back(l);
+    return hbm_id[g] = static_cast<int>(links.size()) - 1;
+  };
   auto conn_of = [&](int src, int dst, int ch) {
     const auto key = std::make_tuple(src, dst, ch);
     auto f = conn_id.find(key);
@@ -90,16 +115,21 @@ SimReport simulate(const Program& p, const SimParams& sp) {
     conns.push_back(c);
     return conn_id[key] = static_cast<int>(conns.size()) - 1;
   };
+  const int L = std::max(1, sp.lanes);
   for (int r = 0; r < R; ++r)
     for (const ThreadBlock& tb : p.gpus[r].tbs) {
-      SimTb s;
-      s.rank = r;
-      s.tb = &tb;
-      if (tb.send_peer >= 0 && tb.send_peer < R) s.conn_out = conn_of(r, tb.send_peer, tb.channel);
-      if (tb.recv_peer >= 0 && tb.recv_peer < R) s.conn_in = conn_of(tb.recv_peer, r, tb.channel);
-      s.total = ntiles * static_cast<int64_t>(tb.ops.size());
       first[r].push_back(static_cast<int>(tbs.size()));
-      tbs.push_back(s);
+      for (int l = 0; l < L; ++l) {  // sim tb index = first + lane
+        SimTb s;
+        s.rank = r;
+        s.tb = &tb;
+        s.lane = l;
+        if (tb.send_peer >= 0 && tb.send_peer < R) s.conn_out = conn_of(r, tb.send_peer, tb.channel * L + l);
+        if (tb.recv_peer >= 0 && tb.recv_peer < R) s.conn_in = conn_of(tb.recv_peer, r, tb.channel * L + l);
+        const int64_t lane_tiles = ntiles > l ? (ntiles - 1 - l) / L + 1 : 0;
+        s.total = lane_tiles * static_cast<int64_t>(tb.ops.size());
+        tbs.push_back(s);
+      }
     }
   auto tb_by_id = [&](int r, int id) {
     const auto& v = p.gpus[r].tbs;
@@ -107,18 +137,40 @@ SimReport simulate(const Program& p, const SimParams& sp) {
       if (v[t].id == id) return first[r][t];
     return -1;
   };
+  // a lane's order: groups of G tiles, op-major inside a group (G = 1: the paper's tile-major loop)
+  const int64_t G = std::max<int64_t>(1, sp.group);
+  auto lane_tiles = [&](const SimTb& s) { return s.total / static_cast<int64_t>(std::max<size_t>(1, s.tb->ops.size())); };
+  auto decode = [&](const SimTb& s, int64_t pos, int64_t& lt, int& step) {  // pos -> (tile of the lane, step)
+    const int64_t nops = static_cast<int64_t>(s.tb->ops.size());
+    const int64_t g0 = pos / (G * nops) * G;
+    const int64_t gs = std::min<int64_t>(G, lane_tiles(s) - g0);
+    const int64_t in = pos - g0 * nops;
+    step = static_cast<int>(in / gs);
+    lt = g0 + in % gs;
+  };
+  auto encode = [&](const SimTb& s, int64_t lt, int step) {  // (tile of the lane, step) -> pos
+    const int64_t nops = static_cast<int64_t>(s.tb->ops.size());
+    const int64_t g0 = lt / G * G;
+    const int64_t gs = std::min<int64_t>(G, lane_tiles(s) - g0);
+    return g0 * nops + step * gs + (lt - g0);
+  };
   const int slots = std::max(1, sp.slots[pr]);
   std::vector<Running> run;
   double now = 0.0;
   auto ready = [&](const SimTb& s) {
     const int nops = static_cast<int>(s.tb->ops.size());
-    const int64_t i = s.pos / nops;
-    const Op& op = s.tb->ops[s.pos % nops];
+    int64_t i;
+    int step;
+    decode(s, s.pos, i, step);
+    (void)nops;
+    const Op& op = s.tb->ops[step];
     for (const Dep& d : op.deps) {
-      const int dt = tb_by_id(s.rank, d.tb);
-      if (dt < 0) continue;
+      const int dt0 = tb_by_id(s.rank, d.tb);
+      if (dt0 < 0) continue;
+      const int dt = dt0 + s.lane;
       const int64_t dn = static_cast<int64_t>(tbs[dt].tb->ops.size());
-      if (tbs[dt].pos < i * dn + d.step + 1) return false;
+      (void)dn;
+      if (tbs[dt].pos < encode(tbs[dt], i, d.step) + 1) return false;
     }
     if (op_receives(op.op) && s.conn_in >= 0 && conns[s.conn_in].delivered <= conns[s.conn_in].received) return false;
     if (op_sends(op.op) && s.conn_out >= 0 && conns[s.conn_out].sent - conns[s.conn_out].consumed >= slots) return false;
@@ -135,20 +187,40 @@ SimReport simulate(const Program& p, const SimParams& sp) {
   auto start = [&](int ti) {
     SimTb& s = tbs[ti];
     const int nops = static_cast<int>(s.tb->ops.size());
-    const int64_t i = s.pos / nops;
-    const Op& op = s.tb->ops[s.pos % nops];
+    int64_t lt;
+    int step;
+    decode(s, s.pos, lt, step);
+    (void)nops;
+    const int64_t i = s.lane + lt * L;  // the tile
+    const Op& op = s.tb->ops[step];
     const double bytes = tile_len(i);
     if (op_receives(op.op) && s.conn_in >= 0) conns[s.conn_in].received++;
     if (op_sends(op.op) && s.conn_out >= 0) conns[s.conn_out].sent++;
     s.running = true;
-    Running x{ti, kLocal, now + local_us(op, bytes), 0.0, bytes * op.count, -1};
-    if (op_sends(op.op) && s.conn_out >= 0) x.link = conns[s.conn_out].link;
+    const int hbm = hbm_of(gpu[s.rank]);
+    Running x{ti, kLocal, hbm >= 0 ? now : now + local_us(op, bytes), 0.0, bytes * op.count, -1, -1,
+              bytes * op.count * local_passes(op.op), hbm};
+    if (op_sends(op.op) && s.conn_out >= 0) {
+      x.link = conns[s.conn_out].link;
+      if (hbm >= 0 && links[x.link].cls == 0) {  // same GPU: the message's bytes are the ops' local passes
+        x.link = hbm;                            // (direct writes, pulled reads); it pays its alpha
+        x.bytes = 0;
+      }
+    }
+    if (hbm >= 0 && x.local > 0) {
+      x.phase = kLocalFlow;
+      x.remaining = x.local;
+      x.res = hbm;
+      links[hbm].flows.push_back(ti);
+    }
     run.push_back(x);
   };
   auto finish = [&](int ti) {
     SimTb& s = tbs[ti];
-    const int nops = static_cast<int>(s.tb->ops.size());
-    const Op& op = s.tb->ops[s.pos % nops];
+    int64_t lt;
+    int step;
+    decode(s, s.pos, lt, step);
+    const Op& op = s.tb->ops[step];
     if (op_receives(op.op) && s.conn_in >= 0) conns[s.conn_in].consumed++;
     if (op_sends(op.op) && s.conn_out >= 0) {
       conns[s.conn_out].delivered++;
@@ -171,8 +243,10 @@ SimReport simulate(const Program& p, const SimParams& sp) {
       std::ostringstream os;
       for (const SimTb& s : tbs)
         if (s.pos < s.total) {
-          const int nops = static_cast<int>(s.tb->ops.size());
-          os << " r" << s.rank << ".tb" << s.tb->id << "@t" << s.pos / nops << ".s" << s.pos % nops;
+          int64_t lt;
+          int step;
+          decode(s, s.pos, lt, step);
+          os << " r" << s.rank << ".tb" << s.tb->id << "@t" << s.lane + lt * L << ".s" << step;
         }
       rep.deadlock = "deadlock: blocked" + os.str();
       rep.makespan_us = now;
@@ -192,6 +266,7 @@ SimReport simulate(const Program& p, const SimParams& sp) {
             if (x.link >= 0 && x.bytes > 0) {
               x.phase = kXfer;
               x.remaining = x.bytes;
+              x.res = x.link;
               links[x.link].flows.push_back(x.tb);
             } else {
               finish(x.tb);
@@ -207,33 +282,39 @@ SimReport simulate(const Program& p, const SimParams& sp) {
     if (finished_now || run.empty()) continue;
     // next event: a phase end or a transfer completion (processor sharing on each ordered pair)
     double dt = kInf;
+    auto rate = [&](int res) { return links[res].gbps * 1e3 / static_cast<double>(links[res].flows.size()); };
     for (const Running& x : run) {
-      if (x.phase != kXfer) dt = std::min(dt, x.end_us - now);
-      else dt = std::min(dt, x.remaining / (links[x.link].gbps * 1e3 / static_cast<double>(links[x.link].flows.size())));
+      if (x.phase == kLocal || x.phase == kAlpha) dt = std::min(dt, x.end_us - now);
+      else dt = std::min(dt, x.remaining / rate(x.res));
     }
     if (!(dt < kInf)) dt = 0.0;
     dt = std::max(dt, 0.0);
     for (SimLink& l : links)
       if (!l.flows.empty()) l.busy_us += dt;
     for (Running& x : run)
-      if (x.phase == kXfer) x.remaining -= dt * links[x.link].gbps * 1e3 / static_cast<double>(links[x.link].flows.size());
+      if (x.phase == kXfer || x.phase == kLocalFlow) x.remaining -= dt * rate(x.res);
     now += dt;
     for (size_t k = 0; k < run.size(); ++k) {
       Running& x = run[k];
-      if (x.phase == kXfer && x.remaining <= 1e-9 * std::max(1.0, x.bytes)) {
-        auto& f = links[x.link].flows;
-        f.erase(std::find(f.begin(), f.end(), x.tb));
-        finish(x.tb);
-        run.erase(run.begin() + static_cast<long>(k));
-        --k;
+      const bool flow = x.phase == kXfer || x.phase == kLocalFlow;
+      if (!flow || x.remaining > 1e-9 * std::max(1.0, x.phase == kXfer ? x.bytes : x.local)) continue;
+      auto& f = links[x.res].flows;
+      f.erase(std::find(f.begin(), f.end(), x.tb));
+      if (x.phase == kLocalFlow) {  // local work done: the message (if any) follows
+        x.phase = kLocal;
+        x.end_us = now;
+        continue;
       }
+      finish(x.tb);
+      run.erase(run.begin() + static_cast<long>(k));
+      --k;
     }
   }
   rep.completed = true;
   rep.makespan_us = now + (ntiles > 0 ? sp.launch_us : 0.0);
   int used[3] = {0, 0, 0};
   for (const SimLink& l : links) {
-    if (l.busy_us <= 0.0) continue;
+    if (l.busy_us <= 0.0 || l.cls > 2) continue;
     used[l.cls]++;
     rep.util[l.cls] += now > 0 ? l.busy_us / now : 0.0;
   }

@@ -38,6 +38,16 @@ struct SimParams {
   int64_t chunk_bytes = 1 << 20;
   int64_t tile_bytes = 0;                      // 0: one tile per chunk
   double launch_us = 0.0;                      // added to the makespan
+  // Optional device-memory resource (0: off, SPEC semantics). On: every op's local reads and writes
+  // (send 1, recv 1, copy 2, reduce 3, rrc 2, rcs 1, rrcs 2, rrs 1 passes of its bytes: the
+  // runtime's algorithmic bytes) are flows on one processor-shared resource per GPU of this rate;
+  // same-GPU messages then pay only their alpha -- the loopback calibration, where all ranks share
+  // one GPU's HBM.
+  double hbm_gbps = 0.0;
+  // Lanes (the runtime's parallelism): every thread block runs as `lanes` independent
+  // units, lane l taking tiles l, l + lanes, ...; each connection has its FIFO slots per lane.
+  int lanes = 1;
+  int group = 1;  // tiles per op-major group inside a lane (the runtime's tile groups; 1: tile-major)
 };
 
 struct SimReport {

@@ -30,6 +30,19 @@ class NcclError(RuntimeError):
         self.code = code
 
 
+class SimConfig(ctypes.Structure):
+    _fields_ = [("nranks_gpu", ctypes.c_int), ("rank_gpu", ctypes.POINTER(ctypes.c_int)), ("gpus_per_node", ctypes.c_int),
+                ("alpha_us", ctypes.c_double * 3), ("gbps", ctypes.c_double * 3), ("gamma_gbps", ctypes.c_double),
+                ("copy_gbps", ctypes.c_double), ("protocol", ctypes.c_int), ("slots", ctypes.c_int),
+                ("chunk_bytes", ctypes.c_int64), ("tile_bytes", ctypes.c_int64), ("launch_us", ctypes.c_double),
+                ("hbm_gbps", ctypes.c_double), ("lanes", ctypes.c_int), ("group", ctypes.c_int)]
+
+
+class SimReport(ctypes.Structure):
+    _fields_ = [("completed", ctypes.c_int), ("makespan_us", ctypes.c_double), ("util", ctypes.c_double * 3),
+                ("messages", ctypes.c_int64), ("tiles", ctypes.c_int64), ("deadlock", ctypes.c_char * 256)]
+
+
 class PlanInfo(ctypes.Structure):
     _fields_ = [
         ("ir_id", ctypes.c_int), ("protocol", ctypes.c_int), ("lanes", ctypes.c_int), ("grid", ctypes.c_int),
@@ -37,7 +50,8 @@ class PlanInfo(ctypes.Structure):
         ("chunk_elems", ctypes.c_int64), ("tile_elems", ctypes.c_int64), ("ntiles", ctypes.c_int64),
         ("slot_bytes", ctypes.c_int64), ("wire_bytes", ctypes.c_int64), ("hbm_bytes", ctypes.c_int64),
         ("name", ctypes.c_char * 64), ("unit_warps", ctypes.c_int), ("group", ctypes.c_int),
-        ("mode", ctypes.c_int), ("mail_messages", ctypes.c_int),
+        ("mode", ctypes.c_int), ("mail_messages", ctypes.c_int), ("remote_messages", ctypes.c_int),
+        ("sys_scope", ctypes.c_int), ("tma_stages", ctypes.c_int),
     ]
 
     def as_dict(self):
@@ -95,6 +109,9 @@ def lib():
         "gc3IrBuiltin": [cp, i, ctypes.POINTER(vp)],
         "gc3IrGenerate": [cp, cp, i, i, i, ctypes.POINTER(vp)],
         "gc3IrPredict": [vp, ctypes.c_int64, i, i, ctypes.POINTER(ctypes.c_double)],
+        "gc3SimDefaults": [ctypes.POINTER(SimConfig)],
+        "gc3IrSimulate": [vp, ctypes.POINTER(SimConfig), ctypes.POINTER(SimReport)],
+        "gc3IrSweep": [vp, ctypes.POINTER(SimConfig), ctypes.POINTER(ctypes.c_int64), i, ctypes.c_int64, ctypes.POINTER(vp)],
         "gc3IrValidate": [vp, i, i, i, i, ctypes.POINTER(vp)],
         "gc3IrCheckSlots": [vp, i, ctypes.POINTER(vp)],
         "gc3IrReplicate": [vp, i, ctypes.POINTER(vp)],
@@ -234,6 +251,43 @@ class IR:
         check(lib().gc3IrPredict(self._h, chunk_bytes, {"simple": 0, "ll": 1}.get(protocol, protocol), lanes,
                                  ctypes.byref(out)))
         return out.value
+
+    @staticmethod
+    def _sim_config(rank_gpu=None, protocol="simple", **kw):
+        cfg = SimConfig()
+        check(lib().gc3SimDefaults(ctypes.byref(cfg)))
+        keep = None
+        if rank_gpu is not None:
+            keep = (ctypes.c_int * len(rank_gpu))(*rank_gpu)
+            cfg.nranks_gpu, cfg.rank_gpu = len(rank_gpu), keep
+        cfg.protocol = {"simple": 0, "ll": 1, "ll128": 2}.get(protocol, protocol)
+        for k, v in kw.items():
+            if k in ("alpha_us", "gbps"):
+                for j, x in enumerate(v):
+                    getattr(cfg, k)[j] = x
+            else:
+                setattr(cfg, k, v)
+        return cfg, keep
+
+    def simulate(self, chunk_bytes, tile_bytes=0, **kw):
+        """Timed simulation (gc3IrSimulate): dict with completed, makespan_us, util (per link class),
+        messages, tiles, deadlock. kw: rank_gpu, protocol, alpha_us, gbps, gamma_gbps, copy_gbps,
+        slots, gpus_per_node, launch_us."""
+        cfg, keep = self._sim_config(chunk_bytes=chunk_bytes, tile_bytes=tile_bytes, **kw)
+        rep = SimReport()
+        check(lib().gc3IrSimulate(self._h, ctypes.byref(cfg), ctypes.byref(rep)))
+        del keep
+        return {"completed": bool(rep.completed), "makespan_us": rep.makespan_us, "util": list(rep.util),
+                "messages": rep.messages, "tiles": rep.tiles, "deadlock": rep.deadlock.decode()}
+
+    def sweep(self, sizes, tile_bytes=0, **kw):
+        """CSV rows size_bytes,makespan_us,util_intra,util_inter, one timed run per size (gc3IrSweep)."""
+        cfg, keep = self._sim_config(**kw)
+        arr = (ctypes.c_int64 * max(1, len(sizes)))(*sizes)
+        out = ctypes.c_void_p()
+        check(lib().gc3IrSweep(self._h, ctypes.byref(cfg), arr, len(sizes), tile_bytes, ctypes.byref(out)))
+        del keep
+        return _take(out.value)
 
     def lane_multipliers(self):
         import json
