@@ -42,6 +42,10 @@ CONFIGS = {
                  desc="Ring AllGather GC3-IR, 8 ranks"),
     "c5rs": dict(ir="ring_rs_8", coll="reducescatter", dtype="float32", bytes=64 << 20, proto=None,
                  desc="Ring ReduceScatter GC3-IR, 8 ranks"),
+    "c1ap": dict(ir="allpairs_ar_8", coll="allreduce", dtype="float32", bytes=4 << 20, proto=None,
+                 desc="All-pairs AllReduce GC3-IR, 8 ranks, fp32 4 MB buffer (small-message alternative to C1)"),
+    "c4auto": dict(ir="ring_ar_8_inst4_auto", coll="allreduce", dtype="float32", bytes=64 << 20, proto="simple",
+                   desc="Ring AllReduce instances=4, automatic channels"),
     # C5 at 2 and 4 ranks (sweep / quick only; the 8-rank bench line stays the default contract)
     "c5ag4": dict(ir="ring_ag_4", coll="allgather", dtype="float32", bytes=64 << 20, proto=None, desc="Ring AllGather, 4 ranks"),
     "c5ag2": dict(ir="ring_ag_2", coll="allgather", dtype="float32", bytes=64 << 20, proto=None, desc="Ring AllGather, 2 ranks"),

@@ -72,6 +72,9 @@ struct DevTb {
   int32_t mult;       // lane multiplier: this thread block runs lanes x mult lanes (work balance)
   int32_t unit_base;  // sum of the multipliers of the launch's earlier thread blocks
   int32_t recv_slot;  // rank slot of the receive peer when it runs in the same launch, else -1
+                      // (slots past the launch's own ranks hold other launches' ranks whose
+                      // registered buffers this launch addresses: remote direct / pulled messages)
+  int32_t sys;        // 1: a connection of this thread block reaches another GPU (.sys scope)
 };
 
 // Dataflow execution (interp_df_kernel): one node per op of every thread block of the launch; a work
@@ -128,7 +131,10 @@ struct LaunchArgs {
   int64_t small_elems;  // tapered tiles: n_head small tiles, n_big big ones, then small ones to the end
   int64_t n_head;
   int64_t n_big;
-  uint64_t epoch;       // launch counter of this device (semaphore tag)
+  uint64_t epoch;       // launch counter of this device (semaphore tag); used when epoch_ptr is null
+  uint64_t* epoch_ptr;  // device-side launch counter: read by every block at start, advanced by the last
+                        // block to read it (so CUDA-graph replays of a captured launch get fresh epochs)
+  int32_t* epoch_ctr;   // blocks of the current launch that have read *epoch_ptr (reset by the last one)
   uint64_t timeout_ns;  // spin-wait watchdog; 0 disables
   int32_t* abort_flag;  // device word: any block that times out raises it
   uint64_t* err_info;   // host-mapped: {code, rank, tb, step, tile, what, 0, 0}
@@ -140,6 +146,7 @@ struct LaunchArgs {
   int32_t stage_bytes;  // bytes per stage
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
+  int32_t tma_sys_ops;  // mask applied to tma_ops on thread blocks with a cross-GPU connection (DevTb::sys)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
   int64_t tma_min;      // bytes below which an op takes the register path
   int32_t l2hint;       // bit 0: evict_last stores of hot data (DevOp::hot), bit 1: evict_first bulk loads
@@ -159,6 +166,7 @@ struct LaunchArgs {
   char* mail;                // mailbox of the launch's non-direct, non-pulled messages
   int32_t df_n;              // nodes
   int32_t df_nroots;
+  int32_t df_policy;         // bit 0: continuations (a unit runs the successor it made ready next)
   char* bufs[kMaxLocalRanks][kBufs];  // per local rank: input, output, scratch, source, result (the
                                      // caller's recvbuff shifted so that an owned ReduceScatter chunk
                                      // keeps its input offset; see result_writes), source (the caller's

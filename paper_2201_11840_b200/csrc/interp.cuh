@@ -563,6 +563,22 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
   if (t == 0) *m.seq = base + static_cast<uint32_t>(total);
 }
 
+// ------------------------------------------------------------------ launch epoch
+// The semaphore / progress tag of this launch. Read from device memory (not a kernel argument) so
+// a launch captured in a CUDA graph gets a new epoch at every replay: every block reads the counter
+// once, and the last block to do so advances it for the next launch (launches of a device are
+// serialised, so the next one starts after every block of this one has read it).
+__device__ __forceinline__ uint64_t launch_epoch(uint64_t* epoch_ptr, int32_t* epoch_ctr, uint64_t fallback) {
+  if (!epoch_ptr) return fallback;
+  uint64_t e;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(e) : "l"(epoch_ptr) : "memory");
+  if (atomicAdd(epoch_ctr, 1) == static_cast<int>(gridDim.x) - 1) {
+    *epoch_ctr = 0;
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(epoch_ptr), "l"(e + 1) : "memory");
+  }
+  return e;
+}
+
 // ------------------------------------------------------------------ watchdog
 // Everything here is passed by value: taking the address of a kernel parameter would force the
 // whole LaunchArgs into local memory.
@@ -1043,9 +1059,11 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   // every rank's buffers of this launch, staged in shared memory once: ops index them by rank slot
   // and buffer id (a dynamically indexed kernel parameter would be copied to local memory)
   __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
+  __shared__ uint64_t s_epoch;
 #pragma unroll
   for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
     if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  if (threadIdx.x == kThreads - 1) s_epoch = launch_epoch(a.epoch_ptr, a.epoch_ctr, a.epoch);
   __syncthreads();
   const int uw = a.unit_warps;
   const int n = uw * 32;                         // threads per unit
@@ -1083,12 +1101,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   const DevTb tb = a.tbs[tbi];
   const int lanes = a.uniform ? L0 : L0 * tb.mult;
   const int lane = a.uniform ? unit - tbi * L0 : unit - tb.unit_base * L0;
-  const bool sys = a.sys_scope != 0;
+  // scope per thread block: .sys fences and flags only where a connection reaches another GPU
+  const bool sys = a.sys_scope != 0 && tb.sys != 0;
+  const int tma_ops = sys ? (a.tma_ops & a.tma_sys_ops) : a.tma_ops;
   const bool has_in = tb.chan_in >= 0, has_out = tb.chan_out >= 0;
   const int64_t chunk_elems = a.chunk_elems, tile_elems = a.tile_elems, ntiles = a.ntiles;
   const int64_t chunk_bytes = chunk_elems * R::kEsize;
   const uint64_t slots = static_cast<uint64_t>(a.slots);
-  const uint64_t epoch = a.epoch;
+  const uint64_t epoch = s_epoch;
   char* const* const mine = s_bufs + kBufs * tb.rank_slot;                            // this rank's buffers
   char* const* const peer = s_bufs + kBufs * (tb.peer_slot >= 0 ? tb.peer_slot : 0);  // send peer's (direct)
   char* const* const rpeer = s_bufs + kBufs * (tb.recv_slot >= 0 ? tb.recv_slot : 0); // receive peer's (pull)
@@ -1195,7 +1215,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
                       in_p ? in : nullptr, ll_out ? reinterpret_cast<uint4*>(out) : nullptr, out_d ? out : nullptr,
                       static_cast<uint32_t>(rcvd + 1), static_cast<uint32_t>(sent + 1), sys, c, t, n);
       } else {
-        transfer<R>(op, in_d, src, dst, srcr, dstr, in, in_stride, out, out_stride, tbytes, chunk_bytes, a.tma_ops, tma, t, n, uw,
+        transfer<R>(op, in_d, src, dst, srcr, dstr, in, in_stride, out, out_stride, tbytes, chunk_bytes, tma_ops, tma, t, n, uw,
                     bar_id, a.tma_min);
       }
       if (t == 0) stamp(q, 2);
@@ -1239,9 +1259,11 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
 template <class R>
 __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(const LaunchArgs a) {
   __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
+  __shared__ uint64_t s_epoch;
 #pragma unroll
   for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
     if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  if (threadIdx.x == kThreads - 1) s_epoch = launch_epoch(a.epoch_ptr, a.epoch_ctr, a.epoch);
   __syncthreads();
   const int uw = a.unit_warps;
   const int n = uw * 32;
@@ -1261,7 +1283,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(cons
   }
   unit_sync(uw, bar_id, n);
   const WqArgs w{a.tbs, a.ops, a.deps, a.wq_next, a.wq_order, a.prog, a.abort_flag, a.err_info, a.timeout_ns,
-                 a.chunk_elems, a.tile_elems, a.ntiles, a.epoch, a.ntbs, a.tma_ops, a.tma_min};
+                 a.chunk_elems, a.tile_elems, a.ntiles, s_epoch, a.ntbs, a.tma_ops, a.tma_min};
   interp_wq<R>(w, s_bufs, tma, pol_last, t, n, uw, uib, bar_id);
 }
 
@@ -1277,11 +1299,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(cons
 // of a chunk), so the per-tile graphs are independent and any linear extension of each is a valid
 // execution. Messages are direct, pulled (as in the static interpreter) or mailed: written by the
 // sender into a per-message mailbox span and read from there by the receiver.
-// Ready queue: the first df_nroots x ntiles positions are the root items (tile-major, implicit);
-// later positions are filled by the unit that completes an item's last predecessor. A unit that
-// claims position p waits until p is filled: every position is eventually filled (the graph is a
-// DAG and claimed items never wait), so this cannot deadlock. Counters and queue slots are reset
-// by their consumer, so the tables are zero at every launch without a memset.
+// Scheduling: a unit that completes an item's last predecessor runs that item next itself (its
+// continuation: the data it just produced is still in L2); further items it makes ready go to a
+// ready queue. A unit without a continuation takes the next root item (nodes without predecessors,
+// tile-major), else claims the next queue position (atomicAdd: positions are filled in push order)
+// and waits until a unit fills it or every item has run. Only ready items are ever pushed and a
+// running item never waits, so some claimed position is always filled while items remain: no
+// deadlock. Predecessor counters and queue slots are reset by their consumer, so the tables are
+// zero at every launch without a memset (only the four counters are).
 __device__ __forceinline__ int32_t ld_relaxed32(const int32_t* p) {
   int32_t v;
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -1325,44 +1350,55 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
   const int64_t total = nn * ntiles;
   const int64_t nroot_items = static_cast<int64_t>(a.df_nroots) * ntiles;
   uint64_t* const trace = a.trace;
-  // thread 0 claims its next queue position while the current item runs (a claim never blocks
-  // progress: every claimed position is filled once its item is ready, and ready items never wait)
-  int64_t next_idx = t == 0 ? static_cast<int64_t>(atomicAdd(a.df_ctr, 1)) : 0;
+  // counters (zeroed before the launch), one 128-byte line each: root items claimed, queue pushes,
+  // queue pops, items finished
+  int32_t* const roots_ctr = a.df_ctr;
+  int32_t* const push_ctr = a.df_ctr + 32;
+  int32_t* const pop_ctr = a.df_ctr + 64;
+  int32_t* const done_ctr = a.df_ctr + 96;
+  __shared__ int64_t s_cont[kThreads / 32];
+  int64_t cont = -1;  // (thread 0) the ready successor this unit runs next
   for (;;) {
     if (t == 0) {
-      const int64_t idx = next_idx;
       const uint64_t t_claim = trace ? globaltimer() : 0;
-      int64_t item = -1;
-      if (idx < nroot_items) {
-        item = (idx / a.df_nroots) * nn + a.df_roots[idx % a.df_nroots];
-      } else if (idx < total) {
-        int32_t* slot = a.df_q + (idx - nroot_items);
-        int32_t v = ld_relaxed32(slot);
-        if (v == 0) {
-          Ctx c{a.abort_flag, a.err_info, a.timeout_ns, 0, -1, 0, idx};
-          const uint64_t start = globaltimer();
-          for (int it = 0; (v = ld_relaxed32(slot)) == 0; ++it) {
-            if ((it & 255) == 255) {
-              if (*reinterpret_cast<volatile int*>(a.abort_flag)) break;
-              if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
-                raise_timeout(c, 5);
-                break;
-              }
+      int64_t item = cont;
+      cont = -1;
+      // work, in this order: a continuation (depth first: the producer's data is still in L2), the
+      // next root item (tile-major), the next position of the ready queue (waited on until a unit
+      // fills it; positions are taken with atomicAdd, never retried)
+      if (item < 0 && ld_relaxed32(roots_ctr) < nroot_items) {
+        const int64_t idx = atomicAdd(roots_ctr, 1);
+        if (idx < nroot_items) item = (idx / a.df_nroots) * nn + a.df_roots[idx % a.df_nroots];
+      }
+      if (item < 0) {
+        const int32_t q = atomicAdd(pop_ctr, 1);
+        int32_t* slot = a.df_q + q;
+        Ctx c{a.abort_flag, a.err_info, a.timeout_ns, 0, -1, 0, q};
+        const uint64_t start = globaltimer();
+        for (int it = 0;; ++it) {
+          const int32_t v = ld_relaxed32(slot);
+          if (v != 0) {
+            fence_acq_rel(false);  // acquire: the producers' data (released before the push) is visible
+            st_relaxed32(slot, 0);
+            item = v - 1;
+            break;
+          }
+          if ((it & 15) == 15) {
+            if (ld_relaxed32(done_ctr) >= total) break;  // every item has run: this position stays empty
+            if (*reinterpret_cast<volatile int*>(a.abort_flag)) break;
+            if (c.timeout_ns && globaltimer() - start > c.timeout_ns) {
+              raise_timeout(c, 5);
+              break;
             }
           }
         }
-        if (v != 0) {
-          fence_acq_rel(false);  // acquire: the producers' data (released before the push) is visible
-          item = v - 1;
-          st_relaxed32(slot, 0);
-        }
       }
-      if (item >= 0) next_idx = atomicAdd(a.df_ctr, 1);
       if (trace && item >= 0) {
         trace[item * 4 + 0] = t_claim;
         trace[item * 4 + 1] = globaltimer();
       }
       s_item[uib] = item;
+      s_cont[uib] = -1;
     }
     unit_sync(uw, bar_id, n);
     const int64_t item = s_item[uib];
@@ -1402,7 +1438,8 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
           asm volatile("discard.global.L2 [%0], 128;" ::"l"(in + j * chunk_bytes + off) : "memory");
     }
     // publish, one successor per thread: release the unit's data (gathered by the barrier above),
-    // count the predecessor in; the last one pushes the ready item
+    // count the predecessor in; the last one makes the item ready: the first such becomes this
+    // unit's continuation, the others go to the ready queue
     for (int k = t; k < nd.nsucc; k += n) {
       const DfSucc sc = a.df_succ[nd.succ + k];
       int32_t* cnt = a.df_cnt + tile * nn + sc.node;
@@ -1410,9 +1447,19 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
       if (atomicAdd(cnt, 1) + 1 == sc.indeg) {
         __threadfence();  // acquire the other predecessors' releases (read through the counter)
         *cnt = 0;         // ready: reset for the next launch
-        const int32_t pos = atomicAdd(a.df_ctr + 1, 1);
-        st_release32(a.df_q + pos, static_cast<int32_t>(tile * nn + sc.node) + 1);
+        const int64_t ready = tile * nn + sc.node;
+        if (!(a.df_policy & 1) ||
+            atomicCAS(reinterpret_cast<unsigned long long*>(&s_cont[uib]), static_cast<unsigned long long>(-1LL),
+                      static_cast<unsigned long long>(ready)) != static_cast<unsigned long long>(-1LL)) {
+          const int32_t pos = atomicAdd(push_ctr, 1);
+          st_release32(a.df_q + pos, static_cast<int32_t>(ready) + 1);
+        }
       }
+    }
+    unit_sync(uw, bar_id, n);
+    if (t == 0) {
+      cont = s_cont[uib];
+      atomicAdd(done_ctr, 1);
     }
     if (trace && t == 0) trace[item * 4 + 3] = globaltimer();
   }

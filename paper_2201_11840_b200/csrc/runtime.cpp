@@ -15,6 +15,8 @@
 #include <fcntl.h>
 #include <sys/stat.h>
 #include <sys/types.h>
+#include <dlfcn.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -41,6 +43,7 @@
 #include "devplan.hpp"
 #include "ir.hpp"
 #include "msccl_xml.hpp"
+#include "timed.hpp"
 
 namespace gc3 {
 
@@ -53,6 +56,7 @@ int interp_blocks_per_sm(KernelFn fn, size_t smem);
 constexpr int kStageBytesHost = 16 << 10;  // interp.cuh kStageBytes
 constexpr int kMaxStagesHost = 8;          // interp.cuh kMaxStages
 constexpr int kSmemBudget = 192 << 10;
+constexpr size_t kDfQueueSlack = 4096;     // dataflow queue positions beyond the items (>= co-resident units)
 
 namespace {
 
@@ -123,11 +127,16 @@ struct Config {
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
   int df = 1;                        // dataflow execution (interp_df_kernel) when every rank is in the
-                                     // launch: 1 = programs with receive-and-forward chains, 2 = every
-                                     // Simple program, 0 = off
+                                     // launch: 1 = reducing programs with receive-and-forward chains and
+                                     // >= 2 items per unit, 2 = every Simple program, 0 = off
   int df_items = 4;                  // dataflow: ready items per unit targeted by the tile size
   int64_t df_max_tile = 256 << 10;   // dataflow: largest tile
-  int64_t df_min_tile = 16 << 10;    // dataflow: smallest tile (unless the chunk is smaller)
+  int64_t df_min_tile = 128 << 10;   // dataflow: smallest tile (unless the chunk is smaller; measured
+                                     // best on C3 / C4 / C5-RS: 64-128 KiB, per-item costs ~3 us)
+  int df_policy = 1;                 // dataflow scheduling: bit 0 continuations (depth first)
+  int remote = 1;                    // direct / pulled messages to ranks of other launches through
+                                     // registered user buffers (exchange_buffers); 0: FIFO only
+  int tma_remote = 0;                // bulk copies on thread blocks with a cross-GPU connection
 };
 
 Config config_from_env() {
@@ -163,6 +172,9 @@ Config config_from_env() {
   c.df_items = static_cast<int>(env_int("GC3_DF_ITEMS", c.df_items));
   c.df_max_tile = env_int("GC3_DF_MAX_TILE", c.df_max_tile);
   c.df_min_tile = env_int("GC3_DF_MIN_TILE", c.df_min_tile);
+  c.remote = static_cast<int>(env_int("GC3_REMOTE", c.remote));
+  c.df_policy = static_cast<int>(env_int("GC3_DF_POLICY", c.df_policy));
+  c.tma_remote = static_cast<int>(env_int("GC3_TMA_REMOTE", c.tma_remote));
   return c;
 }
 
@@ -326,7 +338,9 @@ struct DevicePlan {  // one registered IR on one device
   DevDep* d_deps = nullptr;
   DevChan* d_chans = nullptr;
   uint64_t* d_sems = nullptr;
-  bool sys_scope = false;
+  bool sys_scope = false;     // some thread block has a connection to another GPU (DevTb::sys)
+  std::vector<int> remote_ranks;  // ranks of other launches with buffer slots (remote transports)
+  int remote_msgs = 0;            // direct / pulled receives of this launch whose sender is remote
   // dataflow graph (every rank of the program in this launch): nodes in launch op order
   bool df_ok = false;
   int df_n = 0, df_nroots = 0, df_mail_msgs = 0, df_depth = 1;
@@ -339,6 +353,8 @@ struct DevicePlan {  // one registered IR on one device
 struct DeviceState {
   int device = -1;
   uint64_t epoch = 0;
+  uint64_t* d_epoch = nullptr;     // device-side launch counter (LaunchArgs::epoch_ptr)
+  int32_t* d_epoch_ctr = nullptr;  // blocks that have read it in the current launch
   int32_t* d_abort = nullptr;
   uint64_t* h_err = nullptr;  // host-mapped err_info[8]
   uint64_t* d_err = nullptr;
@@ -372,6 +388,9 @@ struct Clique {
   std::vector<int> rank_pid;
   std::map<int, DeviceState> devs;
   int refs = 0;
+  std::vector<std::string> rank_uuid;  // GPU of every rank (UUID; read from the bootstrap records on demand)
+  char* calls = nullptr;               // shared-memory call-descriptor table (remote transports)
+  size_t calls_bytes = 0;
 };
 
 }  // namespace
@@ -396,6 +415,16 @@ struct gc3Comm {
   std::string last_error;
   bool destroyed = false;
   std::vector<void*> opened_ipc;  // peer arenas opened via IPC (to close)
+  // user-buffer registration (remote direct / pulled messages): allocations this rank exported
+  // (driver buffer id -> registration), peers' registrations opened here ((rank, id) -> base)
+  struct Reg {
+    uint64_t buffer_id;
+    uintptr_t base;
+    size_t size;
+  };
+  std::vector<Reg> regs;
+  std::map<std::pair<int, int>, char*> peer_regs;
+  uint64_t xcall_seq = 0;  // calls whose buffers were exchanged with other launches
 };
 
 namespace gc3 {
@@ -447,6 +476,13 @@ ncclResult_t device_state(Clique* cl, int dev, DeviceState*& out) {
   DeviceGuard g(dev);
   CUDA_TRY(cudaMalloc(&ds.d_abort, sizeof(int32_t)));
   CUDA_TRY(cudaMemset(ds.d_abort, 0, sizeof(int32_t)));
+  {
+    CUDA_TRY(cudaMalloc(&ds.d_epoch, 256));
+    const uint64_t one = 1;
+    CUDA_TRY(cudaMemset(ds.d_epoch, 0, 256));
+    CUDA_TRY(cudaMemcpy(ds.d_epoch, &one, sizeof(one), cudaMemcpyHostToDevice));
+    ds.d_epoch_ctr = reinterpret_cast<int32_t*>(reinterpret_cast<char*>(ds.d_epoch) + 128);
+  }
   CUDA_TRY(cudaHostAlloc(&ds.h_err, 8 * sizeof(uint64_t), cudaHostAllocMapped));
   std::memset(ds.h_err, 0, 8 * sizeof(uint64_t));
   CUDA_TRY(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ds.d_err), ds.h_err, 0));
@@ -525,6 +561,167 @@ ncclResult_t peer_arena(Comm* c, int id, int r, char*& out) {
   }
   out = v[r];
   return ncclSuccess;
+}
+
+// ------------------------------------------------------------------------------- GPU identity
+std::string device_bus_id(int dev) {
+  char buf[64] = {0};
+  if (cudaDeviceGetPCIBusId(buf, sizeof(buf), dev) != cudaSuccess) return "dev" + std::to_string(dev);
+  return buf;
+}
+
+// PCI bus id of rank r's GPU (device ordinals differ across processes with CUDA_VISIBLE_DEVICES)
+ncclResult_t rank_gpu(Comm* c, int r, std::string& out) {
+  Clique* cl = c->clique;
+  if (cl->rank_uuid.size() != static_cast<size_t>(cl->nranks)) cl->rank_uuid.assign(cl->nranks, "");
+  if (cl->rank_uuid[r].empty()) {
+    if (cl->local[r]) {
+      cl->rank_uuid[r] = device_bus_id(cl->local[r]->device);
+    } else {
+      std::string rec;
+      if (!read_record(shm_dir(cl->key), "rank" + std::to_string(r), rec, c->cfg.timeout_ms + 60000))
+        return set_error(ncclSystemError, "timed out waiting for rank %d's bootstrap record", r);
+      std::istringstream in(rec);
+      long pid = 0;
+      int dev = -1;
+      std::string bus;
+      in >> pid >> dev >> bus;
+      cl->rank_uuid[r] = bus.empty() ? "pid" + std::to_string(pid) + "dev" + std::to_string(dev) : bus;
+    }
+  }
+  out = cl->rank_uuid[r];
+  return ncclSuccess;
+}
+
+// ------------------------------------------------------------------------------- user buffers
+// Direct and pulled messages between ranks of different launches (other processes or GPUs) address
+// the peer's user buffers. As with NCCL user-buffer registration, every allocation a collective
+// touches is exported once (cudaIpcGetMemHandle of the allocation's base, keyed by the driver's
+// process-wide unique buffer id, so a freed and re-allocated range is never taken for the old one)
+// and opened once by each peer process that addresses it; per call, the ranks exchange
+// (registration, offset) descriptors through a shared-memory table (exchange_buffers).
+using CuPointerGetAttributeFn = int (*)(void*, int, unsigned long long);
+CuPointerGetAttributeFn cu_pointer_get_attribute() {
+  static CuPointerGetAttributeFn fn = [] {
+    void* h = dlopen("libcuda.so.1", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcuda.so.1", RTLD_NOW);
+    return h ? reinterpret_cast<CuPointerGetAttributeFn>(dlsym(h, "cuPointerGetAttribute")) : nullptr;
+  }();
+  return fn;
+}
+
+// Registration id and offset of device pointer p (exports its allocation on first use).
+ncclResult_t export_buffer(Comm* c, const void* p, int32_t& id, int64_t& off) {
+  id = -1;
+  off = 0;
+  if (!p) return ncclSuccess;
+  CuPointerGetAttributeFn fn = cu_pointer_get_attribute();
+  if (!fn) return set_error(ncclSystemError, "cuPointerGetAttribute unavailable (libcuda.so.1)");
+  const auto ptr = static_cast<unsigned long long>(reinterpret_cast<uintptr_t>(p));
+  unsigned long long bid = 0, base = 0;
+  size_t size = 0;
+  if (fn(&bid, 7 /* CU_POINTER_ATTRIBUTE_BUFFER_ID */, ptr) || fn(&base, 11 /* RANGE_START_ADDR */, ptr) ||
+      fn(&size, 12 /* RANGE_SIZE */, ptr))
+    return set_error(ncclInvalidArgument, "buffer %p is not device memory the driver knows", p);
+  for (size_t i = 0; i < c->regs.size(); ++i)
+    if (c->regs[i].buffer_id == bid) {
+      id = static_cast<int32_t>(i);
+      off = static_cast<int64_t>(ptr - c->regs[i].base);
+      return ncclSuccess;
+    }
+  cudaIpcMemHandle_t h{};
+  {
+    DeviceGuard g(c->device);
+    CUDA_TRY(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(static_cast<uintptr_t>(base))));
+  }
+  id = static_cast<int32_t>(c->regs.size());
+  std::string rec(reinterpret_cast<const char*>(&h), sizeof(h));
+  rec.append(reinterpret_cast<const char*>(&base), sizeof(base));
+  rec.append(reinterpret_cast<const char*>(&size), sizeof(size));
+  if (!post_record(shm_dir(c->clique->key), "buf" + std::to_string(c->rank) + "." + std::to_string(id), rec))
+    return set_error(ncclSystemError, "cannot post the buffer registration record");
+  c->regs.push_back({bid, static_cast<uintptr_t>(base), size});
+  off = static_cast<int64_t>(ptr - base);
+  return ncclSuccess;
+}
+
+// Base address, in this process, of rank r's registration `id` (opened on first use).
+ncclResult_t peer_buffer(Comm* c, int r, int32_t id, char*& out) {
+  out = nullptr;
+  if (id < 0) return ncclSuccess;
+  Clique* cl = c->clique;
+  if (cl->local[r]) {  // same process: the exporter's own pointer (unified addressing)
+    if (static_cast<size_t>(id) >= cl->local[r]->regs.size()) return set_error(ncclInternalError, "unknown registration");
+    out = reinterpret_cast<char*>(cl->local[r]->regs[id].base);
+    return ncclSuccess;
+  }
+  auto f = c->peer_regs.find({r, id});
+  if (f != c->peer_regs.end()) {
+    out = f->second;
+    return ncclSuccess;
+  }
+  std::string rec;
+  if (!read_record(shm_dir(cl->key), "buf" + std::to_string(r) + "." + std::to_string(id), rec, c->cfg.timeout_ms + 60000) ||
+      rec.size() < sizeof(cudaIpcMemHandle_t))
+    return set_error(ncclSystemError, "rank %d's buffer registration %d is missing", r, id);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, rec.data(), sizeof(h));
+  void* p = nullptr;
+  DeviceGuard g(c->device);
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+  c->opened_ipc.push_back(p);
+  out = static_cast<char*>(p);
+  c->peer_regs[{r, id}] = out;
+  return ncclSuccess;
+}
+
+// Call-descriptor table: one ring of kCallRing records per rank in a shared-memory file of the
+// clique. Record (rank, seq % kCallRing) holds the registration and offset of each of the rank's
+// launch buffers for its seq-th exchanged call; `done` is the last seq for which the rank has read
+// every peer record it needs (a writer never laps a reader: it waits for done >= seq - kCallRing).
+constexpr int kCallRing = 64;
+struct CallRec {
+  std::atomic<uint64_t> seq;
+  int32_t reg[kBufs];
+  int32_t pad;
+  int64_t off[kBufs];
+};
+struct CallRank {
+  std::atomic<uint64_t> done;
+  char pad[56];
+  CallRec rec[kCallRing];
+};
+
+ncclResult_t call_table(Comm* c, CallRank*& out) {
+  Clique* cl = c->clique;
+  if (!cl->calls) {
+    const std::string dir = shm_dir(cl->key);
+    mkdir(dir.c_str(), 0700);
+    const std::string path = dir + "/calls";
+    const size_t bytes = sizeof(CallRank) * static_cast<size_t>(cl->nranks);
+    const int fd = open(path.c_str(), O_RDWR | O_CREAT, 0600);
+    if (fd < 0) return set_error(ncclSystemError, "cannot open %s", path.c_str());
+    if (ftruncate(fd, static_cast<off_t>(bytes)) != 0) {
+      close(fd);
+      return set_error(ncclSystemError, "cannot size %s", path.c_str());
+    }
+    void* m = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    close(fd);
+    if (m == MAP_FAILED) return set_error(ncclSystemError, "cannot map %s", path.c_str());
+    cl->calls = static_cast<char*>(m);
+    cl->calls_bytes = bytes;
+  }
+  out = reinterpret_cast<CallRank*>(cl->calls);
+  return ncclSuccess;
+}
+
+bool spin_until(const std::function<bool()>& ok, int64_t timeout_ms) {
+  const auto deadline = std::chrono::steady_clock::now() + std::chrono::milliseconds(timeout_ms);
+  for (int i = 0; !ok(); ++i) {
+    if (i > 64) std::this_thread::yield();
+    if ((i & 1023) == 1023 && std::chrono::steady_clock::now() > deadline) return false;
+  }
+  return true;
 }
 
 // Message transports, decided statically from the happens-before relation of the program:
@@ -1008,20 +1205,49 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       if (plan.ranks[i] == rank) return static_cast<int>(i);
     return -1;
   };
-  // the transports this launch applies (both ends in it); with per-connection lanes (lane_mask) exactly
-  // the ones the lane multipliers assumed
+  // GPU of every rank: scope per thread block (.sys only where a connection reaches another GPU)
+  std::vector<std::string> gpu_of(p.ranks());
+  for (int r = 0; r < p.ranks(); ++r) NCCL_TRY(rank_gpu(c0, r, gpu_of[r]));
+  const std::string& my_gpu = gpu_of[plan.ranks[0]];
+  // remote transports: direct and pulled messages to and from ranks of other launches address their
+  // registered user buffers (exchanged per call, exchange_buffers); those ranks get buffer slots
+  // after the launch's own. Every rank of the program decides the same way (same program, config
+  // and placement), so both ends of a connection agree on its transport.
+  plan.remote_ranks.clear();
+  bool remote_ok = c0->cfg.remote && static_cast<int>(plan.ranks.size()) < p.ranks() && !direct.empty();
+  if (remote_ok) {
+    for (int r = 0; r < p.ranks(); ++r)
+      if (slot_of(r) < 0) plan.remote_ranks.push_back(r);
+    if (plan.ranks.size() + plan.remote_ranks.size() > static_cast<size_t>(kMaxLocalRanks)) {
+      remote_ok = false;
+      plan.remote_ranks.clear();
+    }
+  }
+  auto vslot_of = [&](int rank) {
+    const int s0 = slot_of(rank);
+    if (s0 >= 0) return s0;
+    for (size_t i = 0; i < plan.remote_ranks.size(); ++i)
+      if (plan.remote_ranks[i] == rank) return static_cast<int>(plan.ranks.size() + i);
+    return -1;
+  };
+  // the transports this launch applies (both ends in it, or reachable through registered buffers);
+  // with per-connection lanes (lane_mask) exactly the ones the lane multipliers assumed
   std::vector<std::vector<std::vector<uint8_t>>> eff(p.ranks());
+  plan.remote_msgs = 0;
   for (int r = 0; r < p.ranks(); ++r) {
     eff[r].resize(p.gpus[r].tbs.size());
     for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
       const ThreadBlock& tb = p.gpus[r].tbs[t];
       eff[r][t].assign(tb.ops.size(), 0);
-      if (direct.empty() || slot_of(r) < 0) continue;
+      if (direct.empty() || vslot_of(r) < 0) continue;
       for (size_t s = 0; s < tb.ops.size(); ++s) {
         uint8_t f = direct[r][t][s];
         if (ir0.lane_mask) f &= ir0.lane_mask;
-        if ((f & (kInDirect | kInPull)) && tb.recv_peer >= 0 && slot_of(tb.recv_peer) >= 0) eff[r][t][s] |= f & (kInDirect | kInPull);
-        if ((f & (kOutDirect | kOutPull)) && tb.send_peer >= 0 && slot_of(tb.send_peer) >= 0)
+        if ((f & (kInDirect | kInPull)) && tb.recv_peer >= 0 && vslot_of(tb.recv_peer) >= 0) {
+          eff[r][t][s] |= f & (kInDirect | kInPull);
+          if (slot_of(r) >= 0 && slot_of(tb.recv_peer) < 0) plan.remote_msgs++;
+        }
+        if ((f & (kOutDirect | kOutPull)) && tb.send_peer >= 0 && vslot_of(tb.send_peer) >= 0)
           eff[r][t][s] |= f & (kOutDirect | kOutPull);
       }
     }
@@ -1111,8 +1337,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       d.unit_base = weight;
       weight += mult[r][t];
       d.chan_in = d.chan_out = -1;
-      d.peer_slot = tb.send_peer >= 0 ? slot_of(tb.send_peer) : -1;
-      d.recv_slot = tb.recv_peer >= 0 ? slot_of(tb.recv_peer) : -1;
+      d.peer_slot = tb.send_peer >= 0 ? vslot_of(tb.send_peer) : -1;
+      d.recv_slot = tb.recv_peer >= 0 ? vslot_of(tb.recv_peer) : -1;
+      d.sys = ((tb.send_peer >= 0 && gpu_of[tb.send_peer] != my_gpu) || (tb.recv_peer >= 0 && gpu_of[tb.recv_peer] != my_gpu)) ? 1 : 0;
+      if (d.sys) plan.sys_scope = true;
       const bool in_local = d.recv_slot >= 0;
       for (size_t s = 0; s < tb.ops.size(); ++s) {
         const Op& op = tb.ops[s];
@@ -1198,7 +1426,6 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         if (st < 0) return set_error(ncclInvalidArgument, "connection %d->%d ch %d has no sender", s, r, tb.channel);
         char* sender_arena = nullptr;
         NCCL_TRY(peer_arena(c, id, s, sender_arena));
-        if (!cl->local[s] || cl->local[s]->device != c->device) plan.sys_scope = true;
         const int k = ir.lay.in_index[t];
         const ArenaLayout slay = make_layout(p, s, L, ir.slots, ir.slot_bytes, mult);
         const int m = slay.out_index[st];
@@ -1222,7 +1449,6 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
         if (rt < 0) return set_error(ncclInvalidArgument, "connection %d->%d ch %d has no receiver", r, dst, tb.channel);
         char* recv_arena = nullptr;
         NCCL_TRY(peer_arena(c, id, dst, recv_arena));
-        if (!cl->local[dst] || cl->local[dst]->device != c->device) plan.sys_scope = true;
         const ArenaLayout rlay = make_layout(p, dst, L, ir.slots, ir.slot_bytes, mult);
         const int k = rlay.in_index[rt];
         const int m = ir.lay.out_index[t];
@@ -1689,7 +1915,8 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.stage_bytes = c->cfg.stage_kb > 0 ? static_cast<int>(c->cfg.stage_kb) << 10
                    : wide             ? 24 << 10
                                       : std::max(4 << 10, std::min(kStageBytesHost, budget / (units_per_block * 3) / 1024 * 1024));
-  if (c->cfg.tma && !sys_scope) cp.tma_stages = std::min(kMaxStagesHost, budget / (units_per_block * cp.stage_bytes));
+  // (thread blocks with a cross-GPU connection use them only with config tma_remote: LaunchArgs::tma_sys_ops)
+  if (c->cfg.tma) cp.tma_stages = std::min(kMaxStagesHost, budget / (units_per_block * cp.stage_bytes));
   cp.smem = static_cast<size_t>(units_per_block) * cp.tma_stages * cp.stage_bytes;
   int bps = occupancy(cp.smem);
   if (bps * ds.num_sms * units_per_block < weight && cp.smem) {  // staging would break co-residency
@@ -1811,21 +2038,33 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.df = false;
   const bool df_ok = ds.plans.size() > static_cast<size_t>(id) && ds.plans[id].df_ok;
   KernelFn df_fn = df_ok ? interp_kernel_df(cp.redop < 0 ? 0 : dtype, cp.redop) : nullptr;
-  if (c->cfg.df && df_fn && !cp.ll && !sys_scope && c->cfg.lanes <= 0 && chunk_bytes > 0 && (ir.has_chain || c->cfg.df > 1) &&
-      interp_blocks_per_sm(df_fn, cp.smem) >= bps) {
+  // df 1 (default): reducing programs with receive-and-forward chains (measured on B200: C3 1.61 ->
+  // 1.39 ms, C4 0.377 -> 0.335 ms, C5-RS 0.230 -> 0.228 ms; the copy-only ring AllGather runs faster
+  // on static lanes) when the launch has at least two items per unit (small messages are latency
+  // bound: static lanes); df 2: every Simple program
+  const int df_units = capacity;
+  int64_t df_tile = 0;
+  bool use_df = c->cfg.df && df_fn && !cp.ll && !sys_scope && c->cfg.lanes <= 0 && chunk_bytes > 0 &&
+                interp_blocks_per_sm(df_fn, cp.smem) >= bps;
+  if (use_df) {
+    // enough tiles that the graph's average width (nodes / depth) x tiles gives every unit
+    // df_items ready items at a time, within [df_min_tile, df_max_tile]
+    const int64_t width = std::max<int64_t>(1, ds.plans[id].df_n / std::max(1, ds.plans[id].df_depth));
+    df_tile = c->cfg.tile_bytes > 0 ? c->cfg.tile_bytes
+                                    : chunk_bytes * width / (static_cast<int64_t>(std::max(1, c->cfg.df_items)) * df_units);
+    df_tile = std::min<int64_t>(std::max<int64_t>(df_tile, c->cfg.df_min_tile), c->cfg.df_max_tile);
+    df_tile = std::max<int64_t>(df_tile / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
+    if (chunk_bytes <= df_tile) df_tile = chunk_bytes;
+    const int64_t items = static_cast<int64_t>(ds.plans[id].df_n) * ((chunk_bytes + df_tile - 1) / df_tile);
+    if (c->cfg.df == 1) use_df = ir.has_chain && ir.has_reduce && items >= 2LL * df_units;
+  }
+  if (use_df) {
     cp.df = true;
     cp.wq = false;
     cp.fn = df_fn;
     cp.uniform = true;
-    const int units = capacity;
-    // enough tiles that the graph's average width (nodes / depth) x tiles gives every unit
-    // df_items ready items at a time
-    const int64_t width = std::max<int64_t>(1, ds.plans[id].df_n / std::max(1, ds.plans[id].df_depth));
-    int64_t tb_bytes = c->cfg.tile_bytes > 0 ? c->cfg.tile_bytes
-                                              : chunk_bytes * width / (static_cast<int64_t>(std::max(1, c->cfg.df_items)) * units);
-    tb_bytes = std::min<int64_t>(std::max<int64_t>(tb_bytes, c->cfg.df_min_tile), c->cfg.df_max_tile);
-    tb_bytes = std::max<int64_t>(tb_bytes / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
-    if (chunk_bytes <= tb_bytes) tb_bytes = chunk_bytes;
+    const int units = df_units;
+    const int64_t tb_bytes = df_tile;
     cp.tile_elems = std::max<int64_t>(tb_bytes / cp.kesize, 1);
     cp.ntiles = (cp.chunk_elems + cp.tile_elems - 1) / cp.tile_elems;
     cp.small_elems = cp.tile_elems;
@@ -1857,6 +2096,60 @@ ncclResult_t ensure_buffer(Comm* c, char*& buf, size_t& have, size_t need) {
 }
 
 // Launches one group's collectives that live on one device.
+// Per-call exchange of the launch buffers with the ranks of other launches (remote direct and
+// pulled messages, see export_buffer): every local rank posts (registration, offset) of its five
+// launch buffers as its next call record, then each remote rank's record of the same call is read
+// and its buffers are opened into the launch's remote slots. anchor[slot] (non-null): the result
+// buffer is recvbuff `anchor` shifted (ReduceScatter result_writes).
+ncclResult_t exchange_buffers(Clique* cl, const DevicePlan& plan, LaunchArgs& a, const std::vector<char*>& anchor) {
+  Comm* c0 = cl->local[plan.ranks[0]];
+  CallRank* tab = nullptr;
+  NCCL_TRY(call_table(c0, tab));
+  const int64_t tmo = c0->cfg.timeout_ms + 60000;
+  uint64_t seq = 0;
+  for (size_t slot = 0; slot < plan.ranks.size(); ++slot) {
+    Comm* c = cl->local[plan.ranks[slot]];
+    const uint64_t sq = ++c->xcall_seq;
+    if (slot > 0 && sq != seq) return set_error(ncclInternalError, "ranks of one launch disagree on the call sequence");
+    seq = sq;
+    if (sq > static_cast<uint64_t>(kCallRing)) {  // never overwrite a record a peer has not read yet
+      const uint64_t need = sq - kCallRing;
+      const bool ok = spin_until([&] {
+        for (int r = 0; r < cl->nranks; ++r)
+          if (r != c->rank && tab[r].done.load(std::memory_order_acquire) < need) return false;
+        return true;
+      }, tmo);
+      if (!ok) return set_error(ncclSystemError, "timed out waiting for peers to read call %llu's buffers", static_cast<unsigned long long>(need));
+    }
+    CallRec& rec = tab[c->rank].rec[sq % kCallRing];
+    for (int b = 0; b < kBufs; ++b) {
+      const char* p = a.bufs[slot][b];
+      const char* anc = (b == kResult && anchor[slot]) ? anchor[slot] : p;
+      int32_t reg = -1;
+      int64_t off = 0;
+      NCCL_TRY(export_buffer(c, anc, reg, off));
+      rec.reg[b] = reg;
+      rec.off[b] = off + (p - anc);
+    }
+    rec.seq.store(sq, std::memory_order_release);
+  }
+  for (size_t i = 0; i < plan.remote_ranks.size(); ++i) {
+    const int r = plan.remote_ranks[i];
+    CallRec& rec = tab[r].rec[seq % kCallRing];
+    if (!spin_until([&] { return rec.seq.load(std::memory_order_acquire) == seq; }, tmo))
+      return set_error(ncclSystemError, "timed out waiting for rank %d's buffers of call %llu (collectives issued in different orders?)", r,
+                       static_cast<unsigned long long>(seq));
+    const size_t vs = plan.ranks.size() + i;
+    for (int b = 0; b < kBufs; ++b) {
+      char* base = nullptr;
+      NCCL_TRY(peer_buffer(c0, r, rec.reg[b], base));
+      a.bufs[vs][b] = base ? base + rec.off[b] : nullptr;
+    }
+  }
+  for (int r : plan.ranks) tab[r].done.store(seq, std::memory_order_release);
+  return ncclSuccess;
+}
+
 ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   DeviceState* ds = nullptr;
   NCCL_TRY(device_state(cl, dev, ds));
@@ -1898,6 +2191,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     size_t spitch, width, rows;
   };
   std::vector<PostCopy> post;
+  std::vector<char*> anchor(plan.ranks.size(), nullptr);
 
   LaunchArgs a{};
   a.tbs = plan.d_tbs;
@@ -1915,6 +2209,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.tma_stages = cp.tma_stages;
   a.stage_bytes = cp.stage_bytes;
   a.tma_ops = c0->cfg.tma;
+  a.tma_sys_ops = c0->cfg.tma_remote ? 0xff : 0;
   a.tma_min = c0->cfg.tma_min;
   a.l2hint = c0->cfg.l2hint;
   a.discard = c0->cfg.discard;
@@ -1930,6 +2225,8 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.n_head = cp.n_head;
   a.n_big = cp.n_big;
   a.epoch = ++ds->epoch;
+  a.epoch_ptr = ds->d_epoch;
+  a.epoch_ctr = ds->d_epoch_ctr;
   a.timeout_ns = static_cast<uint64_t>(c0->cfg.timeout_ms) * 1000000ull;
   a.abort_flag = ds->d_abort;
   a.err_info = ds->d_err;
@@ -2059,7 +2356,11 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.bufs[slot][2] = c->scratch;
     a.bufs[slot][kSource] = source ? source : in;
     a.bufs[slot][kResult] = result ? result : in;
+    // the result base may lie outside recvbuff's allocation (shifted by the owned block's offset):
+    // peers get it as recvbuff's registration plus that shift
+    anchor[slot] = result ? recv : nullptr;
   }
+  if (!plan.remote_ranks.empty()) NCCL_TRY(exchange_buffers(cl, plan, a, anchor));
   if (cp.df) {  // ready-queue counters reset; self-resetting tables sized for this tile count; mailbox
     DeviceGuard gw(dev);
     const size_t items = static_cast<size_t>(plan.df_n) * static_cast<size_t>(cp.ntiles);
@@ -2069,9 +2370,10 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
       ds->d_df_cnt = ds->d_df_q = nullptr;
       ds->df_items_cap = 0;
       CUDA_TRY(cudaMalloc(&ds->d_df_cnt, items * sizeof(int32_t)));
-      CUDA_TRY(cudaMalloc(&ds->d_df_q, items * sizeof(int32_t)));
+      // queue positions: every pushed item plus one idle claim per unit at the end
+      CUDA_TRY(cudaMalloc(&ds->d_df_q, (items + kDfQueueSlack) * sizeof(int32_t)));
       CUDA_TRY(cudaMemset(ds->d_df_cnt, 0, items * sizeof(int32_t)));
-      CUDA_TRY(cudaMemset(ds->d_df_q, 0, items * sizeof(int32_t)));
+      CUDA_TRY(cudaMemset(ds->d_df_q, 0, (items + kDfQueueSlack) * sizeof(int32_t)));
       ds->df_items_cap = items;
     }
     const size_t mail_need = std::max<size_t>(static_cast<size_t>(plan.df_mail_chunks) * static_cast<size_t>(chunk_bytes), 256);
@@ -2082,8 +2384,8 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
       CUDA_TRY(cudaMalloc(&ds->d_mail, mail_need));
       ds->mail_bytes = mail_need;
     }
-    if (!ds->d_wq_next) CUDA_TRY(cudaMalloc(&ds->d_wq_next, 256));
-    CUDA_TRY(cudaMemsetAsync(ds->d_wq_next, 0, 2 * sizeof(int32_t), stream));
+    if (!ds->d_wq_next) CUDA_TRY(cudaMalloc(&ds->d_wq_next, 1024));
+    CUDA_TRY(cudaMemsetAsync(ds->d_wq_next, 0, 512, stream));  // four counters, one 128-byte line each
     a.df_nodes = plan.d_df_nodes;
     a.df_succ = plan.d_df_succ;
     a.df_roots = plan.d_df_roots;
@@ -2093,11 +2395,12 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.mail = ds->d_mail;
     a.df_n = plan.df_n;
     a.df_nroots = plan.df_nroots;
+    a.df_policy = c0->cfg.df_policy;
   }
   if (cp.wq) {  // claim counter reset + progress table (epoch-tagged, never reset)
     DeviceGuard gw(dev);
     const size_t need = static_cast<size_t>(plan.ntbs) * cp.ntiles * sizeof(uint64_t);
-    if (!ds->d_wq_next) CUDA_TRY(cudaMalloc(&ds->d_wq_next, 256));
+    if (!ds->d_wq_next) CUDA_TRY(cudaMalloc(&ds->d_wq_next, 1024));
     if (need > ds->prog_bytes) {
       if (ds->d_prog) CUDA_TRY(cudaFree(ds->d_prog));
       ds->d_prog = nullptr;
@@ -2363,7 +2666,7 @@ ncclResult_t ncclCommInitRank(ncclComm_t* comm, int nranks, ncclUniqueId id, int
   NCCL_TRY(make_comm(cl, rank, dev, &c));
   // publish (pid, device) and learn the peers'
   const std::string dir = shm_dir(key);
-  if (!post_record(dir, "rank" + std::to_string(rank), std::to_string(getpid()) + " " + std::to_string(dev)))
+  if (!post_record(dir, "rank" + std::to_string(rank), std::to_string(getpid()) + " " + std::to_string(dev) + " " + device_bus_id(dev)))
     return set_error(ncclSystemError, "cannot write bootstrap record in %s", dir.c_str());
   *comm = c;
   return ncclSuccess;
@@ -2418,6 +2721,12 @@ static void release_comm(Comm* c) {
   const std::string dir = shm_dir(cl->key);
   unlink((dir + "/rank" + std::to_string(c->rank)).c_str());
   for (size_t i = 0; i < c->irs.size(); ++i) unlink((dir + "/ir" + std::to_string(i) + ".rank" + std::to_string(c->rank)).c_str());
+  for (size_t i = 0; i < c->regs.size(); ++i) unlink((dir + "/buf" + std::to_string(c->rank) + "." + std::to_string(i)).c_str());
+  if (cl->refs == 1 && cl->calls) {  // the process's last rank of the clique: drop the call table
+    munmap(cl->calls, cl->calls_bytes);
+    cl->calls = nullptr;
+    unlink((dir + "/calls").c_str());
+  }
   rmdir(dir.c_str());  // succeeds for the last rank only
   c->destroyed = true;
   if (--cl->refs == 0) {
@@ -2435,6 +2744,7 @@ static void release_comm(Comm* c) {
         for (auto& [k, d] : p.wq_order) cudaFree(d);
       }
       cudaFree(ds.d_abort);
+      if (ds.d_epoch) cudaFree(ds.d_epoch);
       if (ds.d_trace) cudaFree(ds.d_trace);
       if (ds.d_wq_next) cudaFree(ds.d_wq_next);
       if (ds.d_prog) cudaFree(ds.d_prog);
@@ -2606,6 +2916,9 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "wq_lag") c.wq_lag = static_cast<int>(value);
   else if (k == "discard") c.discard = static_cast<int>(value);
   else if (k == "df") c.df = static_cast<int>(value);
+  else if (k == "remote") c.remote = static_cast<int>(value);
+  else if (k == "df_policy") c.df_policy = static_cast<int>(value);
+  else if (k == "tma_remote") c.tma_remote = static_cast<int>(value);
   else if (k == "df_items") c.df_items = static_cast<int>(value);
   else if (k == "df_max_tile") c.df_max_tile = value;
   else if (k == "df_min_tile") c.df_min_tile = value;
@@ -2662,6 +2975,9 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
   info->protocol = cp.proto;
   info->mode = cp.df ? 2 : cp.wq ? 1 : 0;
   info->mail_messages = cp.df ? ds->plans[info->ir_id].df_mail_msgs : 0;
+  info->remote_messages = built ? ds->plans[info->ir_id].remote_msgs : 0;
+  info->sys_scope = built && ds->plans[info->ir_id].sys_scope ? 1 : 0;
+  info->tma_stages = cp.tma_stages;
   info->lanes = cp.lanes;
   info->unit_warps = cp.unit_warps;
   info->group = cp.group;
@@ -2891,6 +3207,70 @@ ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir) {
   if (!collective || !ir) return ncclInvalidArgument;
   auto h = std::make_unique<gc3Ir>();
   if (!builtin_program(collective, nranks, h->p)) return ncclInvalidArgument;
+  *ir = h.release();
+  return ncclSuccess;
+}
+ncclResult_t gc3SimDefaults(gc3SimConfig* cfg) {
+  if (!cfg) return ncclInvalidArgument;
+  std::memset(cfg, 0, sizeof(*cfg));
+  const SimParams d;
+  cfg->gpus_per_node = d.gpus_per_node;
+  for (int k = 0; k < 3; ++k) {
+    cfg->alpha_us[k] = d.alpha_us[k];
+    cfg->gbps[k] = d.gbps[k];
+  }
+  cfg->gamma_gbps = d.gamma_gbps;
+  cfg->copy_gbps = d.copy_gbps;
+  cfg->chunk_bytes = d.chunk_bytes;
+  cfg->launch_us = d.launch_us;
+  return ncclSuccess;
+}
+static SimParams sim_params(const gc3SimConfig* cfg) {
+  SimParams sp;
+  if (cfg->nranks_gpu > 0 && cfg->rank_gpu) sp.rank_gpu.assign(cfg->rank_gpu, cfg->rank_gpu + cfg->nranks_gpu);
+  sp.gpus_per_node = cfg->gpus_per_node > 0 ? cfg->gpus_per_node : 8;
+  for (int k = 0; k < 3; ++k) {
+    sp.alpha_us[k] = cfg->alpha_us[k];
+    sp.gbps[k] = cfg->gbps[k];
+  }
+  sp.gamma_gbps = cfg->gamma_gbps;
+  sp.copy_gbps = cfg->copy_gbps;
+  sp.proto = cfg->protocol;
+  if (cfg->slots > 0)
+    for (int& s : sp.slots) s = cfg->slots;
+  sp.chunk_bytes = cfg->chunk_bytes;
+  sp.tile_bytes = cfg->tile_bytes;
+  sp.launch_us = cfg->launch_us;
+  sp.hbm_gbps = cfg->hbm_gbps;
+  sp.lanes = std::max(1, cfg->lanes);
+  sp.group = std::max(1, cfg->group);
+  return sp;
+}
+ncclResult_t gc3IrSimulate(gc3Ir_t ir, const gc3SimConfig* cfg, gc3SimReport* report) {
+  if (!ir || !cfg || !report) return ncclInvalidArgument;
+  if (cfg->gamma_gbps <= 0 || cfg->copy_gbps <= 0 || cfg->chunk_bytes < 0) return ncclInvalidArgument;
+  const SimReport r = simulate(ir->p, sim_params(cfg));
+  std::memset(report, 0, sizeof(*report));
+  report->completed = r.completed ? 1 : 0;
+  report->makespan_us = r.makespan_us;
+  for (int k = 0; k < 3; ++k) report->util[k] = r.util[k];
+  report->messages = r.messages;
+  report->tiles = r.tiles;
+  std::snprintf(report->deadlock, sizeof(report->deadlock), "%s", r.deadlock.c_str());
+  return ncclSuccess;
+}
+ncclResult_t gc3IrSweep(gc3Ir_t ir, const gc3SimConfig* cfg, const int64_t* sizes, int nsizes, int64_t tile_bytes, char** csv) {
+  if (!ir || !cfg || !csv || nsizes < 0 || (nsizes > 0 && !sizes)) return ncclInvalidArgument;
+  if (cfg->gamma_gbps <= 0 || cfg->copy_gbps <= 0) return ncclInvalidArgument;
+  const std::string s = sweep_csv(ir->p, sim_params(cfg), std::vector<int64_t>(sizes, sizes + nsizes), tile_bytes);
+  *csv = static_cast<char*>(std::malloc(s.size() + 1));
+  std::memcpy(*csv, s.c_str(), s.size() + 1);
+  return ncclSuccess;
+}
+ncclResult_t gc3IrGenerate(const char* algo, const char* collective, int nranks, int channels, int instances, gc3Ir_t* ir) {
+  if (!algo || !collective || !ir) return ncclInvalidArgument;
+  auto h = std::make_unique<gc3Ir>();
+  if (!generate_program(algo, collective, nranks, channels, instances, h->p)) return ncclInvalidArgument;
   *ir = h.release();
   return ncclSuccess;
 }

@@ -1,7 +1,9 @@
 """The multi-process path on one B200: two processes host four ranks each (ncclCommInitRank inside
-a group, /dev/shm bootstrap, CUDA IPC arenas), so every message between the processes goes through
-the receiver-resident FIFOs with .sys-scope flags — the code the N-GPU runs use — and the results
-must be bit-exact vs the oracle."""
+a group, /dev/shm bootstrap, CUDA IPC arenas). Messages between the processes travel the way the
+N-GPU runs move them: direct writes into and pulled reads from the peer process's registered user
+buffers (per-call buffer exchange, remote=1, the default) or the receiver-resident FIFOs (remote=0,
+and every LL message); bulk copies stay on because both processes drive the same GPU. Results must
+be bit-exact vs the oracle, and the plan must show the transports it claims."""
 import json
 import os
 import socket
@@ -23,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(proc, nproc, port, name, coll, count, dtype, proto, q):
+def _worker(proc, nproc, port, name, coll, count, dtype, proto, q, remote=1):
     import torch.distributed as dist
     from paper_2201_11840_b200 import gc3
     from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
@@ -39,6 +41,8 @@ def _worker(proc, nproc, port, name, coll, count, dtype, proto, q):
         with gc3.group():
             comms = [gc3.init_rank(R, uid[0], proc * per + k) for k in range(per)]
         for c in comms:
+            c.set_config("remote", remote)
+            c.set_config("tma_min", 4096)  # these small calls take the bulk-copy paths too
             i = c.register_ir(ir_path(name))
             if proto:
                 c.set_protocol(i, proto)
@@ -61,11 +65,12 @@ def _worker(proc, nproc, port, name, coll, count, dtype, proto, q):
                     bad = np.nonzero(got != exp)[0]
                     why.append(f"it {it} rank {r}: {bad.size} mismatches, first {bad[:6].tolist()}")
             dist.barrier()
+        info = comms[0].query_plan(coll, count, dtype)
         for c in comms:
             c.destroy()
-        q.put((proc, ok, "; ".join(why)))
+        q.put((proc, ok, "; ".join(why), info))
     except Exception as e:  # reported to the parent
-        q.put((proc, False, repr(e)))
+        q.put((proc, False, repr(e), None))
     finally:
         dist.destroy_process_group()
 
@@ -76,20 +81,31 @@ def _worker(proc, nproc, port, name, coll, count, dtype, proto, q):
     ("ring_rs_8", "reducescatter", 20000, "int32", None),
     ("hier_ar_2x4_par1", "allreduce", 8 * 30000, "bfloat16", None),
     ("ring_ag_8", "allgather", 25000, "float32", None),
-    # LL lines across processes (.sys-scope line flags), and a ragged count (padded chunks)
+    # LL lines across processes, and a ragged count (padded chunks)
     ("ring_ar_8_ch1", "allreduce", 8 * 5000, "float32", "ll"),
     ("twostep_a2a_2x4", "alltoall", 7000, "float16", "ll"),
     ("ring_ar_8_ch1", "allreduce", 8 * 40000 + 13, "float32", None)])
-def test_two_processes_share_a_gpu(name, coll, count, dtype, proto):
+@pytest.mark.parametrize("remote", [1, 0])
+def test_two_processes_share_a_gpu(name, coll, count, dtype, proto, remote):
+    results = _run(name, coll, count, dtype, proto, remote)
+    for proc, ok, err, info in results:
+        assert ok, (proc, err)
+        assert info["local_ranks"] == 4 and info["sys_scope"] == 0, info  # one GPU: .gpu scope everywhere
+        if proto is None:
+            assert info["tma_stages"] > 0, info  # bulk copies across the process boundary too
+            # direct / pulled messages across the process boundary exactly when remote transports are on
+            assert (info["remote_messages"] > 0) == bool(remote), info
+
+
+def _run(name, coll, count, dtype, proto, remote):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, proto, q)) for p in range(2)]
+    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, proto, q, remote)) for p in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=240) for _ in procs]
     for p in procs:
         p.join(timeout=60)
-    for proc, ok, err in results:
-        assert ok, (proc, err)
+    return results

@@ -99,3 +99,54 @@ def test_watchdog_error_is_sticky():
     finally:
         for c in comms:
             c.abort()
+
+
+@pytest.mark.parametrize("name,coll,count,dtype,cfg", [
+    ("ring_ar_8_ch8_inst4", "allreduce", 8 * 4 * 8192, "float32", {}),               # static lanes, op-major groups
+    ("ring_ar_8_ch8_inst4", "allreduce", 8 * 4 * 8192, "float32", {"df": 2}),        # dataflow
+    ("hier_ar_2x4_par1", "allreduce", 8 * 65536, "bfloat16", {}),
+    ("twostep_a2a_2x4", "alltoall", 65536, "float32", {}),                          # work queue
+    ("ring_ar_8_ch1", "allreduce", 8 * 4096, "float32", {"proto": "ll"}),
+    ("ring_rs_8", "reducescatter", 40000, "int32", {"proto": "ll128"})])
+def test_cuda_graph_replays_are_fresh_launches(name, coll, count, dtype, cfg):
+    """Collectives captured in a CUDA graph and replayed: every replay must behave like a new launch
+    (semaphore / progress epochs come from a device-side counter, not a baked-in argument), bit-exact
+    against the oracle for new input contents at every replay."""
+    from paper_2201_11840_b200 import gc3
+    from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
+    irj = json.loads(read_ir(name))
+    R = len(irj["gpus"])
+    comms = gc3.init_all([0] * R)
+    try:
+        for c in comms:
+            for k, v in cfg.items():
+                if k != "proto":
+                    c.set_config(k, v)
+            i = c.register_ir(ir_path(name))
+            if "proto" in cfg:
+                c.set_protocol(i, cfg["proto"])
+        n = input_len(coll, count, R)
+        bufs = [make_input(n, dtype, 0, device="cuda") for _ in range(R)]
+        stream = torch.cuda.Stream()
+        stream.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(stream):
+            run_collective(comms, coll, bufs, count, dtype)  # warm-up: buffers and tables allocated
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            outs = run_collective(comms, coll, bufs, count, dtype)
+        for rep in range(3):
+            fresh = [make_input(n, dtype, 100 * rep + r) for r in range(R)]
+            for b, f in zip(bufs, fresh):
+                b.copy_(f)
+            torch.cuda.synchronize()
+            expected = oracle_collective(irj, coll, [f.clone() for f in fresh], count, dtype)
+            g.replay()
+            torch.cuda.synchronize()
+            assert comms[0].async_error()[0] == 0
+            for r in range(R):
+                assert np.array_equal(to_np_bits(outs[r], dtype), expected[r]), (rep, r)
+        del g
+    finally:
+        for c in comms:
+            c.destroy()
