@@ -39,6 +39,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges cost nothing without an attached tool
+
 #include "../../include/gc3.h"
 #include "devplan.hpp"
 #include "ir.hpp"
@@ -376,6 +378,8 @@ struct DeviceState {
   // work buffers and the work-queue tables, so collectives issued on different streams must not
   // overlap (NCCL orders a communicator's kernels the same way)
   cudaEvent_t last_done = nullptr;
+  cudaEvent_t launch_done = nullptr;                    // joins the other participating streams after a launch
+  std::map<cudaStream_t, cudaEvent_t> stream_events;    // per participating stream, created once
   cudaStream_t last_stream = nullptr;
   bool has_last = false;
 };
@@ -2096,6 +2100,18 @@ ncclResult_t ensure_buffer(Comm* c, char*& buf, size_t& have, size_t need) {
 }
 
 // Launches one group's collectives that live on one device.
+// The (cached) event a participating stream records before a launch on another stream waits on it.
+ncclResult_t stream_event(DeviceState& ds, cudaStream_t s, cudaEvent_t& ev) {
+  auto f = ds.stream_events.find(s);
+  if (f == ds.stream_events.end()) {
+    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    ds.stream_events[s] = ev;
+  } else {
+    ev = f->second;
+  }
+  return ncclSuccess;
+}
+
 // Per-call exchange of the launch buffers with the ranks of other launches (remote direct and
 // pulled messages, see export_buffer): every local rank posts (registration, offset) of its five
 // launch buffers as its next call record, then each remote rank's record of the same call is read
@@ -2150,7 +2166,16 @@ ncclResult_t exchange_buffers(Clique* cl, const DevicePlan& plan, LaunchArgs& a,
   return ncclSuccess;
 }
 
+struct NvtxRange {  // one range per collective launch (SURVEY.md §5 tracing)
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
 ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
+  char range_name[96];
+  std::snprintf(range_name, sizeof(range_name), "gc3 %s count=%zu dev=%d ranks=%zu", coll_name(ops[0]->coll), ops[0]->count, dev,
+                ops.size());
+  NvtxRange range(range_name);
   DeviceState* ds = nullptr;
   NCCL_TRY(device_state(cl, dev, ds));
   Comm* c0 = ops[0]->comm;
@@ -2265,11 +2290,10 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   for (Pending* q : ops)
     if (q->stream != stream && std::find(others.begin(), others.end(), q->stream) == others.end()) others.push_back(q->stream);
   for (cudaStream_t s : others) {
-    cudaEvent_t ev;
-    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    cudaEvent_t ev = nullptr;
+    NCCL_TRY(stream_event(*ds, s, ev));
     CUDA_TRY(cudaEventRecord(ev, s));
     CUDA_TRY(cudaStreamWaitEvent(stream, ev, 0));
-    CUDA_TRY(cudaEventDestroy(ev));
   }
   // serialise with the previous launch of this device when it went to another stream (same stream:
   // stream order suffices). Under stream capture the graph's own edges order the launches.
@@ -2444,12 +2468,10 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     ds->last_stream = stream;
     ds->has_last = true;
   }
-  for (cudaStream_t s : others) {
-    cudaEvent_t ev;
-    CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-    CUDA_TRY(cudaEventRecord(ev, stream));
-    CUDA_TRY(cudaStreamWaitEvent(s, ev, 0));
-    CUDA_TRY(cudaEventDestroy(ev));
+  for (cudaStream_t s : others) {  // the launch stream's event: recorded once, waited on by every other stream
+    if (!ds->launch_done) CUDA_TRY(cudaEventCreateWithFlags(&ds->launch_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ds->launch_done, stream));
+    CUDA_TRY(cudaStreamWaitEvent(s, ds->launch_done, 0));
   }
   return ncclSuccess;
 }
@@ -2752,6 +2774,8 @@ static void release_comm(Comm* c) {
       if (ds.d_df_q) cudaFree(ds.d_df_q);
       if (ds.d_mail) cudaFree(ds.d_mail);
       if (ds.last_done) cudaEventDestroy(ds.last_done);
+      if (ds.launch_done) cudaEventDestroy(ds.launch_done);
+      for (auto& [st, ev] : ds.stream_events) cudaEventDestroy(ev);
       cudaFreeHost(ds.h_err);
     }
     g_cliques.erase(cl->key);

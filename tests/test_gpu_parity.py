@@ -416,7 +416,7 @@ def test_dataflow_mode_is_selected_and_mails_rrs_messages():
         assert plan["mode"] == 2
         assert plan["mail_messages"] == 8  # one rrs -> rrc message per rank
         # small messages (fewer than two items per unit) stay on static lanes by default
-        assert comms[0].query_plan("allreduce", 8 << 20, "float32")["mode"] == 0
+        assert comms[0].query_plan("allreduce", 8 * 65536, "float32")["mode"] == 0
     finally:
         for c in comms:
             c.destroy()
