@@ -121,6 +121,9 @@ struct Config {
                                      // measured: LL ~2x faster than Simple below ~1 MiB, BASELINE §5.2)
   int64_t ll128_max_bytes = 0;       // ... and LL128 above ll_max_bytes up to this many (0: never)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
+  int gen = 1;                       // built-in AllReduce per size tier (builtin_for); 0: one ring
+  int64_t gen_small = 1 << 20;       // ... multi-channel ring with LL lines up to this many bytes
+  int64_t gen_large = 8 << 20;       // ... single ring up to this many, multi-channel ring above
   int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
   int select = 0;                    // among matching IRs pick the lowest timed-model prediction
   int64_t stage_kb = 0;              // bytes per stage (0: automatic, 3+ stages per unit)
@@ -136,9 +139,11 @@ struct Config {
   int64_t df_min_tile = 128 << 10;   // dataflow: smallest tile (unless the chunk is smaller; measured
                                      // best on C3 / C4 / C5-RS: 64-128 KiB, per-item costs ~3 us)
   int df_policy = 1;                 // dataflow scheduling: bit 0 continuations (depth first)
+  int df_window = 0;                 // dataflow: tiles in flight ahead of the finished items (0: unbounded)
   int remote = 1;                    // direct / pulled messages to ranks of other launches through
                                      // registered user buffers (exchange_buffers); 0: FIFO only
   int tma_remote = 0;                // bulk copies on thread blocks with a cross-GPU connection
+  int l2_prefetch = 0;               // bulk pipelines prefetch this many pieces ahead into L2 (0: off)
 };
 
 Config config_from_env() {
@@ -164,6 +169,9 @@ Config config_from_env() {
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
   c.ll128_max_bytes = env_int("GC3_LL128_MAX_BYTES", c.ll128_max_bytes);
   c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
+  c.gen = static_cast<int>(env_int("GC3_GEN", c.gen));
+  c.gen_small = env_int("GC3_GEN_SMALL", c.gen_small);
+  c.gen_large = env_int("GC3_GEN_LARGE", c.gen_large);
   c.smem_kb = env_int("GC3_SMEM_KB", c.smem_kb);
   c.select = static_cast<int>(env_int("GC3_SELECT", c.select));
   c.stage_kb = env_int("GC3_STAGE_KB", c.stage_kb);
@@ -176,7 +184,9 @@ Config config_from_env() {
   c.df_min_tile = env_int("GC3_DF_MIN_TILE", c.df_min_tile);
   c.remote = static_cast<int>(env_int("GC3_REMOTE", c.remote));
   c.df_policy = static_cast<int>(env_int("GC3_DF_POLICY", c.df_policy));
+  c.df_window = static_cast<int>(env_int("GC3_DF_WINDOW", c.df_window));
   c.tma_remote = static_cast<int>(env_int("GC3_TMA_REMOTE", c.tma_remote));
+  c.l2_prefetch = static_cast<int>(env_int("GC3_L2_PREFETCH", c.l2_prefetch));
   return c;
 }
 
@@ -2235,6 +2245,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.stage_bytes = cp.stage_bytes;
   a.tma_ops = c0->cfg.tma;
   a.tma_sys_ops = c0->cfg.tma_remote ? 0xff : 0;
+  a.l2_prefetch = c0->cfg.l2_prefetch;
   a.tma_min = c0->cfg.tma_min;
   a.l2hint = c0->cfg.l2hint;
   a.discard = c0->cfg.discard;
@@ -2420,6 +2431,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     a.df_n = plan.df_n;
     a.df_nroots = plan.df_nroots;
     a.df_policy = c0->cfg.df_policy;
+    a.df_window = c0->cfg.df_window;
   }
   if (cp.wq) {  // claim counter reset + progress table (epoch-tagged, never reset)
     DeviceGuard gw(dev);
@@ -2553,23 +2565,52 @@ ncclResult_t register_program(Comm* comm, std::unique_ptr<RankIR> ir, int* ir_id
   return ncclSuccess;
 }
 
-// A call no registered IR matches runs the runtime's built-in program for its collective
-// (builtin_program): registered here, before any launch of the group, on every communicator this
+// Built-in program for a call of `bytes` (selection bytes): comm-time generated, per size tier
+// (the paper's mechanism: programs with disjoint size ranges, ir.hpp:112-116). With
+// config gen (default) AllReduce uses three tiers, the measured best of the generated family on a
+// B200 (8 ranks): up to gen_small bytes the ring on min(R, 8) channels x 4
+// instances with LL lines (1 KiB: 28 us vs 65-80 us for one ring), up to gen_large bytes the
+// single-channel ring (4 MiB: 87 us vs 114 us), above it the multi-channel ring again (Simple,
+// dataflow mode: 64 MiB 0.33 ms vs 0.38 ms). Other collectives: the single-ring / direct programs.
+bool builtin_for(const Config& cfg, const std::string& coll, int R, uint64_t bytes, Program& out) {
+  if (!cfg.gen || coll != "allreduce") return builtin_program(coll, R, out);
+  const int C = std::min(R, 8);
+  if (bytes <= static_cast<uint64_t>(cfg.gen_small)) {
+    if (!generate_program("ring", coll, R, C, 4, out)) return false;
+    out.proto = Proto::ll;
+    out.min_bytes = 0;
+    out.max_bytes = static_cast<uint64_t>(cfg.gen_small);
+  } else if (bytes <= static_cast<uint64_t>(cfg.gen_large)) {
+    if (!generate_program("ring", coll, R, 1, 1, out)) return false;
+    out.min_bytes = static_cast<uint64_t>(cfg.gen_small) + 1;
+    out.max_bytes = static_cast<uint64_t>(cfg.gen_large);
+  } else {
+    if (!generate_program("ring", coll, R, C, 4, out)) return false;
+    out.min_bytes = static_cast<uint64_t>(cfg.gen_large) + 1;
+    out.max_bytes = 1ull << 40;
+  }
+  return true;
+}
+
+// A call no registered IR matches runs the runtime's built-in program for its collective and size
+// tier (builtin_for): registered here, before any launch of the group, on every communicator this
 // process hosts in the clique, in rank order — every process meets the first such call of a
-// collective at the same point of the call sequence, so IR ids stay aligned across ranks.
+// collective and tier at the same point of the call sequence, so IR ids stay aligned across ranks.
 ncclResult_t register_builtins(std::vector<Pending>& pend) {
   for (Pending& q : pend) {
     Comm* c = q.comm;
     if (!c->cfg.builtin || select_ir(c, q.coll, q.count, q.dtype) >= 0) continue;
     const std::string coll = coll_name(q.coll);
+    const uint64_t bytes = selection_bytes(q.coll, q.count, dtype_size(q.dtype), c->nranks);
     for (int r = 0; r < c->nranks; ++r) {
       Comm* lc = c->clique->local[r];
       if (!lc) continue;
       bool have = false;
-      for (const auto& ir : lc->irs) have = have || (ir->builtin && ir->prog.collective == coll);
+      for (const auto& ir : lc->irs)
+        have = have || (ir->builtin && ir->prog.collective == coll && bytes >= ir->prog.min_bytes && bytes <= ir->prog.max_bytes);
       if (have) continue;
       auto ir = std::make_unique<RankIR>();
-      if (!builtin_program(coll, lc->nranks, ir->prog)) break;
+      if (!builtin_for(lc->cfg, coll, lc->nranks, bytes, ir->prog)) break;
       ir->builtin = true;
       NCCL_TRY(register_program(lc, std::move(ir), nullptr));
     }
@@ -2933,6 +2974,9 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
   else if (k == "ll128_max_bytes") c.ll128_max_bytes = value;
   else if (k == "builtin") c.builtin = static_cast<int>(value);
+  else if (k == "gen") c.gen = static_cast<int>(value);
+  else if (k == "gen_small") c.gen_small = value;
+  else if (k == "gen_large") c.gen_large = value;
   else if (k == "smem_kb") c.smem_kb = value;
   else if (k == "select") c.select = static_cast<int>(value);
   else if (k == "stage_kb") c.stage_kb = value;
@@ -2942,7 +2986,9 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "df") c.df = static_cast<int>(value);
   else if (k == "remote") c.remote = static_cast<int>(value);
   else if (k == "df_policy") c.df_policy = static_cast<int>(value);
+  else if (k == "df_window") c.df_window = static_cast<int>(value);
   else if (k == "tma_remote") c.tma_remote = static_cast<int>(value);
+  else if (k == "l2_prefetch") c.l2_prefetch = static_cast<int>(value);
   else if (k == "df_items") c.df_items = static_cast<int>(value);
   else if (k == "df_max_tile") c.df_max_tile = value;
   else if (k == "df_min_tile") c.df_min_tile = value;
@@ -3295,6 +3341,13 @@ ncclResult_t gc3IrGenerate(const char* algo, const char* collective, int nranks,
   if (!algo || !collective || !ir) return ncclInvalidArgument;
   auto h = std::make_unique<gc3Ir>();
   if (!generate_program(algo, collective, nranks, channels, instances, h->p)) return ncclInvalidArgument;
+  *ir = h.release();
+  return ncclSuccess;
+}
+ncclResult_t gc3IrBuiltinSized(const char* collective, int nranks, uint64_t bytes, gc3Ir_t* ir) {
+  if (!collective || !ir) return ncclInvalidArgument;
+  auto h = std::make_unique<gc3Ir>();
+  if (!builtin_for(config_from_env(), collective, nranks, bytes, h->p)) return ncclInvalidArgument;
   *ir = h.release();
   return ncclSuccess;
 }

@@ -108,6 +108,7 @@ def lib():
         "gc3IrResultWrites": [vp, ctypes.POINTER(i), ctypes.POINTER(vp)],
         "gc3IrBuiltin": [cp, i, ctypes.POINTER(vp)],
         "gc3IrGenerate": [cp, cp, i, i, i, ctypes.POINTER(vp)],
+        "gc3IrBuiltinSized": [cp, i, ctypes.c_uint64, ctypes.POINTER(vp)],
         "gc3IrPredict": [vp, ctypes.c_int64, i, i, ctypes.POINTER(ctypes.c_double)],
         "gc3SimDefaults": [ctypes.POINTER(SimConfig)],
         "gc3IrSimulate": [vp, ctypes.POINTER(SimConfig), ctypes.POINTER(SimReport)],
@@ -164,10 +165,14 @@ class IR:
         self._h = h
 
     @classmethod
-    def builtin(cls, collective, nranks):
-        """The runtime's built-in program for `collective` on nranks ranks."""
+    def builtin(cls, collective, nranks, nbytes=None):
+        """The runtime's built-in program for `collective` on nranks ranks; with nbytes (per-rank
+        buffer bytes) the one a call of that size runs (AllReduce size tiers)."""
         h = ctypes.c_void_p()
-        check(lib().gc3IrBuiltin(collective.encode(), nranks, ctypes.byref(h)))
+        if nbytes is None:
+            check(lib().gc3IrBuiltin(collective.encode(), nranks, ctypes.byref(h)))
+        else:
+            check(lib().gc3IrBuiltinSized(collective.encode(), nranks, nbytes, ctypes.byref(h)))
         return cls._wrap(h)
 
     @classmethod

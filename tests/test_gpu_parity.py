@@ -275,17 +275,22 @@ def test_work_queue_mode(name, count, dtype, wq):
 
 
 @pytest.mark.parametrize("coll,count,dtype", [("allreduce", 8 * 1000 + 5, "float32"), ("allgather", 4096, "bfloat16"),
-                                              ("reducescatter", 3000, "int32"), ("alltoall", 2048, "float32")])
+                                              ("reducescatter", 3000, "int32"), ("alltoall", 2048, "float32"),
+                                              ("allreduce", 1 << 20, "float32"), ("allreduce", 3 << 20, "float32")])
 def test_builtin_programs_without_registration(coll, count, dtype):
     """Drop-in use: collectives on communicators with no registered IR run the runtime's built-in
-    programs (the reference compiler's ring / direct algorithms), bit-exact vs the oracle running
-    the same program; a registered IR for the collective takes precedence afterwards."""
+    programs (comm-time generated, op for op the reference compiler's ring / direct algorithms;
+    AllReduce per size tier), bit-exact vs the oracle running the same program; a registered IR for
+    the collective takes precedence afterwards."""
     from paper_2201_11840_b200 import gc3
     from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
     R = 8
     comms = gc3.init_all([0] * R)
     try:
-        irj = json.loads(gc3.IR.builtin(coll, R).serialize())
+        esize = {"float32": 4, "bfloat16": 2, "int32": 4}[dtype]
+        sel = count * esize * (1 if coll == "allreduce" else R)  # size_range measure (selection bytes)
+        builtin = gc3.IR.builtin(coll, R, sel)
+        irj = json.loads(builtin.serialize())
         inputs = [make_input(input_len(coll, count, R), dtype, 3 + r) for r in range(R)]
         expected = oracle_collective(irj, coll, [x.clone() for x in inputs], count, dtype)
         for it in range(2):  # the second call reuses the registered built-in
@@ -294,7 +299,7 @@ def test_builtin_programs_without_registration(coll, count, dtype):
             assert comms[0].async_error()[0] == 0
             for r in range(R):
                 assert np.array_equal(to_np_bits(outs[r], dtype), expected[r]), (it, r)
-        assert comms[0].query_plan(coll, count, dtype)["name"] == f"builtin_{coll}_{R}"
+        assert comms[0].query_plan(coll, count, dtype)["name"] == irj["name"]
         name = {"allreduce": "hier_ar_2x4_par1", "allgather": "ring_ag_8", "reducescatter": "ring_rs_8",
                 "alltoall": "twostep_a2a_2x4"}[coll]
         for c in comms:

@@ -55,6 +55,24 @@ def raw(rep):
     return res
 
 
+def stall_reasons(rep, top=10):
+    """Kernel-wide warp-stall reasons (smsp__pcsamp_warps_issue_stalled_* sample counts, raw page)."""
+    text = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(text)))
+    if len(rows) < 3:
+        return []
+    hdr, vals = rows[0], rows[2]
+    out = []
+    for k, v in zip(hdr, vals):
+        if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("_not_issued"):
+            try:
+                out.append((float(v.replace(",", "")), k[len("smsp__pcsamp_warps_issue_stalled_"):]))
+            except ValueError:
+                pass
+    tot = sum(x[0] for x in out) or 1
+    return [(n / tot, k) for n, k in sorted(out, reverse=True)[:top]]
+
+
 def stalls(rep, top=8):
     """Top SASS instructions by warp-stall samples."""
     text = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
@@ -134,6 +152,10 @@ def main():
         if st:
             md += ["", "## Top stall instructions (warp-stall samples, SASS)", "", "| share | address | instruction |", "|---|---|---|"]
             md += [f"| {s:.1%} | {ln} | `{src_.replace('|', '/')}` |" for s, ln, src_ in st]
+        sr = stall_reasons(rep)
+        if sr:
+            md += ["", "## Warp-stall reasons (kernel-wide samples)", "", "| share | reason |", "|---|---|"]
+            md += [f"| {s_:.1%} | {k} |" for s_, k in sr]
     os.makedirs(outdir, exist_ok=True)
     with open(os.path.join(outdir, f"{tag}_{cfg}.md"), "w") as f:
         f.write("\n".join(md) + "\n")
