@@ -430,14 +430,7 @@ struct Tma {
                   // written by thread 0 at the end of an op, read by the unit's threads in a later one
   uint64_t pol;     // L2 policy for the stores of the current op (0: none)
   uint64_t pol_rd;  // L2 policy for the bulk loads (0: none)
-  int pf;           // L2 prefetch distance in pieces (0: off): the loads of piece p also prefetch piece
-                    // p + pf of each operand into L2, so the bulk loads (bounded by shared memory)
-                    // hit L2 instead of waiting for HBM
 };
-
-__device__ __forceinline__ void bulk_prefetch_l2(const void* gmem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
-}
 
 // Copies `count` segments of `nbytes` (segment j: a + j*sa -> o0 + j*s0 [, o1 + j*s1]).
 // Called by thread 0 of the unit; returns after every store has completed (async-proxy writes
@@ -459,15 +452,6 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
   };
   const uint32_t base = *m.seq;
   const int64_t prime = min(static_cast<int64_t>(m.stages), total);
-  auto prefetch = [&](int64_t q) {  // piece q of the source into L2
-    if (m.pf <= 0 || q >= total) return;
-    const char* src;
-    char *d0, *d1;
-    uint32_t bytes;
-    piece(q, src, d0, d1, bytes);
-    bulk_prefetch_l2(src, bytes);
-  };
-  for (int64_t q = prime; q < min(prime + m.pf, total); ++q) prefetch(q);
   for (int64_t p = 0; p < prime; ++p) {
     const char* src;
     char *d0, *d1;
@@ -510,7 +494,6 @@ static __device__ void tma_copy(Tma& m, const char* a, int64_t sa, char* o0, int
       uint64_t* bar = m.bar + rg % m.stages;
       mbar_expect_tx(bar, nbytes_p);
       bulk_load(m.stage + static_cast<size_t>(rg % m.stages) * SB, nsrc, nbytes_p, bar, m.pol_rd);
-      prefetch(np + m.pf);
     }
   }
   bulk_wait_all();
@@ -538,16 +521,7 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
     bytes = static_cast<uint32_t>(min(static_cast<int64_t>(P), nbytes - off));
   };
   const uint32_t base = *m.seq;
-  auto prefetch = [&](int64_t q) {  // thread 0: the operands of piece q into L2
-    if (m.pf <= 0 || q >= total) return;
-    int64_t j, off;
-    uint32_t bytes;
-    piece(q, j, off, bytes);
-    bulk_prefetch_l2(a + j * sa + off, bytes);
-    if (RED) bulk_prefetch_l2(b + j * sb + off, bytes);
-  };
   auto issue = [&](int64_t p) {  // thread 0: the operands of piece p into its stage
-    prefetch(p + m.pf);
     int64_t j, off;
     uint32_t bytes;
     piece(p, j, off, bytes);
@@ -560,7 +534,6 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
   };
   if (t == 0) {
     fence_proxy_async_global();  // generic-proxy acquires (deps, flags) -> async-proxy reads
-    for (int64_t q = 0; q < min(static_cast<int64_t>(m.pf), total); ++q) prefetch(q);
     for (int64_t p = 0; p < min(static_cast<int64_t>(m.stages), total); ++p) issue(p);
   }
   for (int64_t p = 0; p < total; ++p) {
@@ -1105,7 +1078,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
   __shared__ uint32_t s_seq[kThreads / 32];
   Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0,
-          (a.l2hint & 2) ? l2_evict_first_policy() : 0, a.l2_prefetch};
+          (a.l2hint & 2) ? l2_evict_first_policy() : 0};
   const uint64_t pol_last = l2_evict_last_policy();
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
@@ -1301,7 +1274,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(cons
   __shared__ uint64_t s_bar[kThreads / 32][kMaxStages];
   __shared__ uint32_t s_seq[kThreads / 32];
   Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0,
-          0, a.l2_prefetch};  // (evict_first loads measured 2% slower on the AllToAll family)
+          0};  // (evict_first loads measured 2% slower on the AllToAll family)
   const uint64_t pol_last = l2_evict_last_policy();
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {
@@ -1363,7 +1336,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
   __shared__ uint32_t s_seq[kThreads / 32];
   __shared__ int64_t s_item[kThreads / 32];
   Tma tma{s_stage + static_cast<size_t>(uib) * a.tma_stages * a.stage_bytes, a.stage_bytes, s_bar[uib], a.tma_stages, &s_seq[uib], 0,
-          (a.l2hint & 2) ? l2_evict_first_policy() : 0, a.l2_prefetch};
+          (a.l2hint & 2) ? l2_evict_first_policy() : 0};
   const uint64_t pol_last = l2_evict_last_policy();
   if (t == 0) s_seq[uib] = 0;
   if (t == 0 && a.tma_stages > 0) {

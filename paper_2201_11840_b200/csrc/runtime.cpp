@@ -143,7 +143,6 @@ struct Config {
   int remote = 1;                    // direct / pulled messages to ranks of other launches through
                                      // registered user buffers (exchange_buffers); 0: FIFO only
   int tma_remote = 0;                // bulk copies on thread blocks with a cross-GPU connection
-  int l2_prefetch = 0;               // bulk pipelines prefetch this many pieces ahead into L2 (0: off)
 };
 
 Config config_from_env() {
@@ -186,7 +185,6 @@ Config config_from_env() {
   c.df_policy = static_cast<int>(env_int("GC3_DF_POLICY", c.df_policy));
   c.df_window = static_cast<int>(env_int("GC3_DF_WINDOW", c.df_window));
   c.tma_remote = static_cast<int>(env_int("GC3_TMA_REMOTE", c.tma_remote));
-  c.l2_prefetch = static_cast<int>(env_int("GC3_L2_PREFETCH", c.l2_prefetch));
   return c;
 }
 
@@ -2245,7 +2243,6 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.stage_bytes = cp.stage_bytes;
   a.tma_ops = c0->cfg.tma;
   a.tma_sys_ops = c0->cfg.tma_remote ? 0xff : 0;
-  a.l2_prefetch = c0->cfg.l2_prefetch;
   a.tma_min = c0->cfg.tma_min;
   a.l2hint = c0->cfg.l2hint;
   a.discard = c0->cfg.discard;
@@ -2988,7 +2985,6 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "df_policy") c.df_policy = static_cast<int>(value);
   else if (k == "df_window") c.df_window = static_cast<int>(value);
   else if (k == "tma_remote") c.tma_remote = static_cast<int>(value);
-  else if (k == "l2_prefetch") c.l2_prefetch = static_cast<int>(value);
   else if (k == "df_items") c.df_items = static_cast<int>(value);
   else if (k == "df_max_tile") c.df_max_tile = value;
   else if (k == "df_min_tile") c.df_min_tile = value;
