@@ -1447,23 +1447,34 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
           asm volatile("discard.global.L2 [%0], 128;" ::"l"(in + j * chunk_bytes + off) : "memory");
     }
     // publish, one successor per thread: release the unit's data (gathered by the barrier above),
-    // count the predecessor in; the last one makes the item ready: the first such becomes this
-    // unit's continuation, the others go to the ready queue
-    for (int k = t; k < nd.nsucc; k += n) {
+    // count the predecessor in; the last one makes the item ready. Successors 0..31 are counted by
+    // warp 0 and the lowest-index ready one becomes this unit's continuation (the runtime lists
+    // message receivers first: they read what this item just produced, still in L2); every other
+    // ready item goes to the queue
+    auto count_in = [&](int k) -> int64_t {
       const DfSucc sc = a.df_succ[nd.succ + k];
       int32_t* cnt = a.df_cnt + tile * nn + sc.node;
       fence_acq_rel(false);
-      if (atomicAdd(cnt, 1) + 1 == sc.indeg) {
-        __threadfence();  // acquire the other predecessors' releases (read through the counter)
-        *cnt = 0;         // ready: reset for the next launch
-        const int64_t ready = tile * nn + sc.node;
-        if (!(a.df_policy & 1) ||
-            atomicCAS(reinterpret_cast<unsigned long long*>(&s_cont[uib]), static_cast<unsigned long long>(-1LL),
-                      static_cast<unsigned long long>(ready)) != static_cast<unsigned long long>(-1LL)) {
-          const int32_t pos = atomicAdd(push_ctr, 1);
-          st_release32(a.df_q + pos, static_cast<int32_t>(ready) + 1);
-        }
+      if (atomicAdd(cnt, 1) + 1 != sc.indeg) return -1;
+      __threadfence();  // acquire the other predecessors' releases (read through the counter)
+      *cnt = 0;         // ready: reset for the next launch
+      return tile * nn + sc.node;
+    };
+    auto push = [&](int64_t ready) {
+      const int32_t pos = atomicAdd(push_ctr, 1);
+      st_release32(a.df_q + pos, static_cast<int32_t>(ready) + 1);
+    };
+    if (t < 32) {
+      const int64_t ready = t < nd.nsucc ? count_in(t) : -1;
+      const unsigned ready_mask = __ballot_sync(0xffffffffu, ready >= 0);
+      if (ready >= 0) {
+        if ((a.df_policy & 1) && t == __ffs(ready_mask) - 1) s_cont[uib] = ready;
+        else push(ready);
       }
+    }
+    for (int k = t < 32 ? t + n : t; k < nd.nsucc; k += n) {
+      const int64_t ready = count_in(k);
+      if (ready >= 0) push(ready);
     }
     unit_sync(uw, bar_id, n);
     if (t == 0) {

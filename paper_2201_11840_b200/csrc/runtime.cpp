@@ -1494,7 +1494,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   plan.df_mail_chunks = 0;
   plan.df_mail_msgs = 0;
   if (static_cast<int>(plan.ranks.size()) == p.ranks() && HbGraph(p).ok) {
-    std::vector<std::set<int>> succ(ops.size());
+    std::vector<std::set<int>> succ(ops.size()), msg_succ(ops.size());
     std::vector<int> indeg(ops.size(), 0);
     auto node = [&](int r, int t, int s) { return tbs[launch_index[{r, t}]].op_begin + s; };
     df_nodes.assign(ops.size(), DfNode{});
@@ -1518,6 +1518,7 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
           if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0 && sd.rank >= 0) {
             const int x = node(sd.rank, sd.tb, sd.step);
             succ[x].insert(v);
+            msg_succ[x].insert(v);
             if (!(eff[r][t][s] & (kInDirect | kInPull))) {  // a mailed message
               df_nodes[v].in_mail = static_cast<int32_t>(plan.df_mail_chunks);
               df_nodes[x].out_mail = static_cast<int32_t>(plan.df_mail_chunks);
@@ -1533,9 +1534,13 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       fits = fits && succ[u].size() < 32768;
       for (int v : succ[u]) indeg[v]++;
     }
+    // successors in priority order for the continuation (interp_df_kernel): the receivers of the
+    // node's message first (they read what it just produced), then the rest
     for (size_t u = 0; u < ops.size(); ++u) {
       df_nodes[u].succ = static_cast<int32_t>(df_succ.size());
-      for (int v : succ[u]) df_succ.push_back(DfSucc{v, indeg[v]});
+      for (int pass = 0; pass < 2; ++pass)
+        for (int v : succ[u])
+          if (msg_succ[u].count(v) == (pass == 0 ? 1u : 0u)) df_succ.push_back(DfSucc{v, indeg[v]});
     }
     for (size_t u = 0; u < ops.size(); ++u) {
       df_nodes[u].indeg = static_cast<int16_t>(indeg[u]);
