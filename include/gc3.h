@@ -238,6 +238,8 @@ typedef struct {
                               processor-shared device-memory resource per GPU of this rate */
   int lanes;               /* units per thread block, lane l taking tiles l, l + lanes, ... (0 or 1: one) */
   int group;               /* tiles per op-major group inside a lane (0 or 1: tile-major, Fig. 4) */
+  double op_us;            /* device-memory mode: fixed cost of every op per tile */
+  int msg_read_passes;     /* device-memory mode: extra passes of a reducing receive reading its message */
 } gc3SimConfig;
 typedef struct {
   int completed;           /* 0: deadlock (see `deadlock`) */

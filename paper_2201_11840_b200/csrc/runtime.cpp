@@ -3294,6 +3294,7 @@ ncclResult_t gc3SimDefaults(gc3SimConfig* cfg) {
   cfg->copy_gbps = d.copy_gbps;
   cfg->chunk_bytes = d.chunk_bytes;
   cfg->launch_us = d.launch_us;
+  cfg->msg_read_passes = d.msg_read_passes;
   return ncclSuccess;
 }
 static SimParams sim_params(const gc3SimConfig* cfg) {
@@ -3315,6 +3316,8 @@ static SimParams sim_params(const gc3SimConfig* cfg) {
   sp.hbm_gbps = cfg->hbm_gbps;
   sp.lanes = std::max(1, cfg->lanes);
   sp.group = std::max(1, cfg->group);
+  sp.op_us = cfg->op_us;
+  sp.msg_read_passes = cfg->msg_read_passes;
   return sp;
 }
 ncclResult_t gc3IrSimulate(gc3Ir_t ir, const gc3SimConfig* cfg, gc3SimReport* report) {

@@ -51,6 +51,7 @@ struct Running {
   int res;           // resource of the current flow
   double local;      // local bytes (device-memory resource on)
   int hbm;           // device-memory resource of the op's GPU (-1: off)
+  bool local_done;   // the local flow (device-memory mode) has run
 };
 
 int local_passes(Opcode o) {
@@ -198,8 +199,9 @@ SimReport simulate(const Program& p, const SimParams& sp) {
     if (op_sends(op.op) && s.conn_out >= 0) conns[s.conn_out].sent++;
     s.running = true;
     const int hbm = hbm_of(gpu[s.rank]);
-    Running x{ti, kLocal, hbm >= 0 ? now : now + local_us(op, bytes), 0.0, bytes * op.count, -1, -1,
-              bytes * op.count * local_passes(op.op), hbm};
+    const int passes = local_passes(op.op) + ((op.op == Opcode::rrc || op.op == Opcode::rrcs || op.op == Opcode::rrs) ? sp.msg_read_passes : 0);
+    Running x{ti, kLocal, hbm >= 0 ? now + sp.op_us : now + local_us(op, bytes), 0.0, bytes * op.count, -1, -1,
+              bytes * op.count * passes, hbm, hbm < 0};
     if (op_sends(op.op) && s.conn_out >= 0) {
       x.link = conns[s.conn_out].link;
       if (hbm >= 0 && links[x.link].cls == 0) {  // same GPU: the message's bytes are the ops' local passes
@@ -207,12 +209,7 @@ SimReport simulate(const Program& p, const SimParams& sp) {
         x.bytes = 0;
       }
     }
-    if (hbm >= 0 && x.local > 0) {
-      x.phase = kLocalFlow;
-      x.remaining = x.local;
-      x.res = hbm;
-      links[hbm].flows.push_back(ti);
-    }
+    if (hbm >= 0 && x.local <= 0) x.local_done = true;
     run.push_back(x);
   };
   auto finish = [&](int ti) {
@@ -259,7 +256,12 @@ SimReport simulate(const Program& p, const SimParams& sp) {
       for (size_t k = 0; k < run.size(); ++k) {
         Running& x = run[k];
         if ((x.phase == kLocal || x.phase == kAlpha) && x.end_us <= now) {
-          if (x.phase == kLocal && x.link >= 0) {
+          if (x.phase == kLocal && !x.local_done) {  // fixed per-op cost done: the local bytes flow
+            x.phase = kLocalFlow;
+            x.remaining = x.local;
+            x.res = x.hbm;
+            links[x.hbm].flows.push_back(x.tb);
+          } else if (x.phase == kLocal && x.link >= 0) {
             x.phase = kAlpha;
             x.end_us = now + links[x.link].alpha_us;
           } else if (x.phase == kAlpha || x.link < 0) {
@@ -303,6 +305,7 @@ SimReport simulate(const Program& p, const SimParams& sp) {
       if (x.phase == kLocalFlow) {  // local work done: the message (if any) follows
         x.phase = kLocal;
         x.end_us = now;
+        x.local_done = true;
         continue;
       }
       finish(x.tb);

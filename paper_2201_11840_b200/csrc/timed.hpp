@@ -44,6 +44,10 @@ struct SimParams {
   // same-GPU messages then pay only their alpha -- the loopback calibration, where all ranks share
   // one GPU's HBM.
   double hbm_gbps = 0.0;
+  double op_us = 0.0;          // fixed cost of every op per tile (device-memory mode): the interpreter's
+                               // per-op synchronisation (barriers, release fence, flags)
+  int msg_read_passes = 1;     // device-memory mode: extra passes of a reducing receive (rrc / rrcs / rrs)
+                               // that reads its message from a FIFO slot or the sender's span
   // Lanes (the runtime's parallelism): every thread block runs as `lanes` independent
   // units, lane l taking tiles l, l + lanes, ...; each connection has its FIFO slots per lane.
   int lanes = 1;

@@ -35,7 +35,8 @@ class SimConfig(ctypes.Structure):
                 ("alpha_us", ctypes.c_double * 3), ("gbps", ctypes.c_double * 3), ("gamma_gbps", ctypes.c_double),
                 ("copy_gbps", ctypes.c_double), ("protocol", ctypes.c_int), ("slots", ctypes.c_int),
                 ("chunk_bytes", ctypes.c_int64), ("tile_bytes", ctypes.c_int64), ("launch_us", ctypes.c_double),
-                ("hbm_gbps", ctypes.c_double), ("lanes", ctypes.c_int), ("group", ctypes.c_int)]
+                ("hbm_gbps", ctypes.c_double), ("lanes", ctypes.c_int), ("group", ctypes.c_int),
+                ("op_us", ctypes.c_double), ("msg_read_passes", ctypes.c_int)]
 
 
 class SimReport(ctypes.Structure):

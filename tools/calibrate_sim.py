@@ -94,7 +94,8 @@ class Sim:
     def predict(self, p, prm):
         ir, cb, tile, R, L = self.prepare(p)
         r = ir.simulate(cb, tile, lanes=L, group=p["group"], rank_gpu=[0] * R, alpha_us=[prm["alpha"], 2.0, 8.0], gbps=[1e9, 770.0, 50.0],
-                        gamma_gbps=1e9, copy_gbps=1e9, hbm_gbps=prm["hbm"], launch_us=prm["launch"])
+                        gamma_gbps=1e9, copy_gbps=1e9, hbm_gbps=prm["hbm"], launch_us=prm["launch"], op_us=prm.get("op", 0.0),
+                        msg_read_passes=1)
         return r["makespan_us"]
 
 
@@ -102,13 +103,15 @@ def fit(sim, pts):
     """Grid over (alpha, device memory rate); the launch cost is additive, so for each grid point the
     best launch is a 1-D scan over the zero-launch predictions."""
     best = None
-    for alpha in [0.5 * k for k in range(1, 13)]:
-        for hbm in [500 * k for k in range(6, 15)]:
-            base = [sim.predict(p, {"alpha": alpha, "hbm": hbm, "launch": 0.0}) for p in pts]
-            for launch in [0.5 * k for k in range(0, 81)]:
-                worst = max(abs(math.log((b + launch) / p["us"])) for b, p in zip(base, pts))
-                if best is None or worst < best[0]:
-                    best = (worst, {"alpha": alpha, "hbm": float(hbm), "launch": launch})
+    for alpha in [0.5 * k for k in range(0, 9)]:
+        for op in [0.5 * k for k in range(0, 7)]:
+            for hbm in [500 * k for k in range(8, 15)]:
+                q = {"alpha": alpha, "hbm": float(hbm), "launch": 0.0, "op": op}
+                base = [sim.predict(p, q) for p in pts]
+                for launch in [0.5 * k for k in range(0, 81)]:
+                    worst = max(abs(math.log((b + launch) / p["us"])) for b, p in zip(base, pts))
+                    if best is None or worst < best[0]:
+                        best = (worst, dict(q, launch=launch))
     return best[1], best[0]
 
 
@@ -127,7 +130,8 @@ def main():
              "`tools/calibrate_sim.py`: measured device times (bench.py --quick, Simple) vs the simulator running the IR",
              "on the launch's lanes, measured tile size, all ranks on GPU 0 and one processor-shared",
              "device-memory resource.", "",
-             f"Fitted: alpha = {prm['alpha']} us per message, device memory = {prm['hbm']} GB/s, launch = {prm['launch']} us; "
+             f"Fitted: alpha = {prm['alpha']} us per message, {prm['op']} us per op and tile, device memory = {prm['hbm']} GB/s, "
+             f"launch = {prm['launch']} us; reducing receives read their message (+1 pass); "
              f"worst |error| = {100 * (math.exp(worst) - 1):.1f} %.", "",
              "| point | bytes / rank | measured us | predicted us | error |", "|---|---|---|---|---|"]
     for name, b, us, pred, err in rows:
