@@ -2397,7 +2397,9 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     // peers get it as recvbuff's registration plus that shift
     anchor[slot] = result ? recv : nullptr;
   }
-  if (!plan.remote_ranks.empty()) NCCL_TRY(exchange_buffers(cl, plan, a, anchor));
+  // (line-protocol launches move every message through the FIFO lines: nothing to exchange; every
+  // rank decides this the same way, so the per-rank call sequences stay aligned)
+  if (!plan.remote_ranks.empty() && !cp.ll) NCCL_TRY(exchange_buffers(cl, plan, a, anchor));
   if (cp.df) {  // ready-queue counters reset; self-resetting tables sized for this tile count; mailbox
     DeviceGuard gw(dev);
     const size_t items = static_cast<size_t>(plan.df_n) * static_cast<size_t>(cp.ntiles);
