@@ -204,9 +204,9 @@ ncclResult_t gc3IrLaneMultipliers(gc3Ir_t ir, char** json);
  * "alltoall") on nranks ranks when no registered IR matches a call (see gc3RegisterIR). */
 ncclResult_t gc3IrBuiltin(const char* collective, int nranks, gc3Ir_t* ir);
 /* The built-in program a call of `bytes` (per-rank buffer bytes, the size_range measure) runs when no
- * registered IR matches: AllReduce per size tier (multi-channel ring with LL lines / single ring /
- * multi-channel ring, each with its size_range; config gen, gen_small, gen_large), the other
- * collectives as gc3IrBuiltin. */
+ * registered IR matches: AllReduce per size tier (multi-channel ring with LL lines / with LL128 lines /
+ * single ring / multi-channel ring, each with its size_range; config gen, gen_small, gen_ll128,
+ * gen_large), the other collectives as gc3IrBuiltin. */
 ncclResult_t gc3IrBuiltinSized(const char* collective, int nranks, uint64_t bytes, gc3Ir_t* ir);
 /* Comm-time program generation (compiler in the loop): algo "ring" (allreduce on
  * `channels` rings, chunk k on channel k % channels; allgather / reducescatter on one), "allpairs"

@@ -659,6 +659,95 @@ static bool allpairs_allreduce(int R, Program& out) {
   return true;
 }
 
+// Hierarchical AllReduce over N nodes x G GPUs (rank = node * G + local index),
+// R = N * G chunks per rank seen as G blocks of N chunks: (1) a ReduceScatter ring inside every
+// node on channel 0 leaves local rank g owning block g reduced over its node; (2) on channel 1 a
+// ring AllReduce across the N nodes among the ranks with local index g completes block g (its N
+// chunks, one per node); (3) an AllGather ring inside every node on channel 2 distributes the
+// blocks. Phase 2 waits for phase 1 (the owning rrc), phase 3's first send for phase 2's last op,
+// both declared as deps. Our own layout of the reference's hier_ar program (same final state,
+// race free: tests/test_builtin_irs.py), not its exact thread-block order.
+static bool hierarchical_allreduce(int N, int G, Program& out) {
+  if (N < 2 || G < 2) return false;
+  const int R = N * G;
+  Program p;
+  p.collective = "allreduce";
+  p.proto = Proto::simple;
+  p.inplace = true;
+  p.nchunks[0] = p.nchunks[1] = R;
+  auto mk = [](Opcode o, int chunk, int count) {
+    Op x;
+    x.op = o;
+    x.src_buf = x.dst_buf = Buf::input;
+    x.src_off = x.dst_off = chunk;
+    x.count = count;
+    return x;
+  };
+  auto finish = [](ThreadBlock& tb, std::vector<std::pair<int, Op>>& steps) {
+    std::stable_sort(steps.begin(), steps.end(), [](const auto& a, const auto& b) { return a.first < b.first; });
+    for (auto& [k, o] : steps) {
+      o.step = static_cast<int>(tb.ops.size());
+      tb.ops.push_back(o);
+    }
+  };
+  for (int r = 0; r < R; ++r) {
+    const int n = r / G, l = r % G;
+    Gpu g;
+    g.rank = r;
+    // (1) intra-node ReduceScatter of the G blocks (N chunks each): block b's chain starts at local
+    // b + 1 and ends (rrc) at its owner b; RS step s = (l - b - 1) mod G
+    ThreadBlock t1;
+    t1.id = 0;
+    t1.send_peer = n * G + (l + 1) % G;
+    t1.recv_peer = n * G + (l + G - 1) % G;
+    t1.channel = 0;
+    std::vector<std::pair<int, Op>> s1;
+    for (int b = 0; b < G; ++b) {
+      const int s = ((l - b - 1) % G + G) % G;
+      s1.push_back({s, mk(s == 0 ? Opcode::send : s == G - 1 ? Opcode::rrc : Opcode::rrcs, b * N, N)});
+    }
+    finish(t1, s1);
+    t1.ops.back().has_dep = true;  // the owning rrc: phase 2 waits for it
+    // (2) ring AllReduce across the nodes on block l: chunk l*N + k is owned by node k
+    ThreadBlock t2;
+    t2.id = 1;
+    t2.send_peer = ((n + 1) % N) * G + l;
+    t2.recv_peer = ((n + N - 1) % N) * G + l;
+    t2.channel = 1;
+    std::vector<std::pair<int, Op>> s2;
+    for (int k = 0; k < N; ++k) {
+      const int s = ((n - k - 1) % N + N) % N;  // RS step
+      const Opcode rs = s == 0 ? Opcode::send : (s == N - 2 && N >= 3) ? Opcode::rrs : Opcode::rrcs;
+      s2.push_back({s, mk(rs, l * N + k, 1)});
+      const int a = ((n - k) % N + N) % N;  // AG step
+      if (a >= 1) s2.push_back({N - 1 + a, mk(a == N - 1 ? Opcode::recv : Opcode::rcs, l * N + k, 1)});
+    }
+    finish(t2, s2);
+    t2.ops.front().deps.push_back({0, static_cast<int>(t1.ops.size()) - 1});
+    t2.ops.back().has_dep = true;  // phase 3's first send waits for it
+    // (3) intra-node AllGather of the blocks: block b leaves its owner b; AG step a = (l - b) mod G
+    ThreadBlock t3;
+    t3.id = 2;
+    t3.send_peer = t1.send_peer;
+    t3.recv_peer = t1.recv_peer;
+    t3.channel = 2;
+    std::vector<std::pair<int, Op>> s3;
+    for (int b = 0; b < G; ++b) {
+      const int a = ((l - b) % G + G) % G;
+      s3.push_back({a, mk(a == 0 ? Opcode::send : a == G - 1 ? Opcode::recv : Opcode::rcs, b * N, N)});
+    }
+    finish(t3, s3);
+    t3.ops.front().deps.push_back({1, static_cast<int>(t2.ops.size()) - 1});
+    g.tbs.push_back(t1);
+    g.tbs.push_back(t2);
+    g.tbs.push_back(t3);
+    p.gpus.push_back(std::move(g));
+  }
+  p.name = "builtin_hier_allreduce_" + std::to_string(N) + "x" + std::to_string(G);
+  out = std::move(p);
+  return true;
+}
+
 bool generate_program(const std::string& algo, const std::string& collective, int R, int channels, int instances, Program& out) {
   if (R < 2 || channels < 1 || instances < 1 || instances > 64) return false;
   Program p;
@@ -671,6 +760,9 @@ bool generate_program(const std::string& algo, const std::string& collective, in
   } else if (algo == "allpairs") {
     if (collective != "allreduce" || channels != 1) return false;
     if (!allpairs_allreduce(R, p)) return false;
+  } else if (algo == "hier") {  // channels = GPUs per node (R = nodes x channels)
+    if (collective != "allreduce" || channels < 2 || R % channels) return false;
+    if (!hierarchical_allreduce(R / channels, channels, p)) return false;
   } else {
     return false;
   }

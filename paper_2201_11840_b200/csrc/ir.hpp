@@ -128,7 +128,8 @@ bool uniform_counts(const Program& p);
 bool builtin_program(const std::string& collective, int nranks, Program& out, int channels = 1);
 // Comm-time program generation (compiler in the loop): algo "ring" (allreduce with
 // `channels` rings: chunk k on channel k % channels; allgather / reducescatter: one ring), "direct"
-// (alltoall), "allpairs" (allreduce), each replicated into `instances` instances (the reference's
+// (alltoall), "allpairs" (allreduce), "hier" (allreduce over nranks / channels nodes of `channels`
+// GPUs), each replicated into `instances` instances (the reference's
 // parallelize(k), program.hpp:366-419). False for an unsupported combination.
 bool generate_program(const std::string& algo, const std::string& collective, int nranks, int channels, int instances, Program& out);
 

@@ -122,7 +122,8 @@ struct Config {
   int64_t ll128_max_bytes = 0;       // ... and LL128 above ll_max_bytes up to this many (0: never)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
   int gen = 1;                       // built-in AllReduce per size tier (builtin_for); 0: one ring
-  int64_t gen_small = 1 << 20;       // ... multi-channel ring with LL lines up to this many bytes
+  int64_t gen_small = 512 << 10;     // ... multi-channel ring with LL lines up to this many bytes
+  int64_t gen_ll128 = 2 << 20;       // ... with LL128 lines up to this many
   int64_t gen_large = 8 << 20;       // ... single ring up to this many, multi-channel ring above
   int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
   int select = 0;                    // among matching IRs pick the lowest timed-model prediction
@@ -143,6 +144,7 @@ struct Config {
   int remote = 1;                    // direct / pulled messages to ranks of other launches through
                                      // registered user buffers (exchange_buffers); 0: FIFO only
   int tma_remote = 0;                // bulk copies on thread blocks with a cross-GPU connection
+  int force_sys = 0;                 // testing: treat other launches' ranks as other GPUs (DevTb::sys)
 };
 
 Config config_from_env() {
@@ -171,6 +173,7 @@ Config config_from_env() {
   c.gen = static_cast<int>(env_int("GC3_GEN", c.gen));
   c.gen_small = env_int("GC3_GEN_SMALL", c.gen_small);
   c.gen_large = env_int("GC3_GEN_LARGE", c.gen_large);
+  c.gen_ll128 = env_int("GC3_GEN_LL128", c.gen_ll128);
   c.smem_kb = env_int("GC3_SMEM_KB", c.smem_kb);
   c.select = static_cast<int>(env_int("GC3_SELECT", c.select));
   c.stage_kb = env_int("GC3_STAGE_KB", c.stage_kb);
@@ -185,6 +188,7 @@ Config config_from_env() {
   c.df_policy = static_cast<int>(env_int("GC3_DF_POLICY", c.df_policy));
   c.df_window = static_cast<int>(env_int("GC3_DF_WINDOW", c.df_window));
   c.tma_remote = static_cast<int>(env_int("GC3_TMA_REMOTE", c.tma_remote));
+  c.force_sys = static_cast<int>(env_int("GC3_FORCE_SYS", c.force_sys));
   return c;
 }
 
@@ -1352,6 +1356,10 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
       d.peer_slot = tb.send_peer >= 0 ? vslot_of(tb.send_peer) : -1;
       d.recv_slot = tb.recv_peer >= 0 ? vslot_of(tb.recv_peer) : -1;
       d.sys = ((tb.send_peer >= 0 && gpu_of[tb.send_peer] != my_gpu) || (tb.recv_peer >= 0 && gpu_of[tb.recv_peer] != my_gpu)) ? 1 : 0;
+      // config force_sys (testing): connections to ranks of other launches behave as if those ranks
+      // were on another GPU (.sys scope, no bulk copies) -- the N-GPU code path, on one GPU
+      if (c0->cfg.force_sys && ((tb.send_peer >= 0 && slot_of(tb.send_peer) < 0) || (tb.recv_peer >= 0 && slot_of(tb.recv_peer) < 0)))
+        d.sys = 1;
       if (d.sys) plan.sys_scope = true;
       const bool in_local = d.recv_slot >= 0;
       for (size_t s = 0; s < tb.ops.size(); ++s) {
@@ -2571,26 +2579,34 @@ ncclResult_t register_program(Comm* comm, std::unique_ptr<RankIR> ir, int* ir_id
 
 // Built-in program for a call of `bytes` (selection bytes): comm-time generated, per size tier
 // (the paper's mechanism: programs with disjoint size ranges, ir.hpp:112-116). With
-// config gen (default) AllReduce uses three tiers, the measured best of the generated family on a
-// B200 (8 ranks, BASELINE.md §5): up to gen_small bytes the ring on min(R, 8) channels x 4
-// instances with LL lines (1 KiB: 28 us vs 65-80 us for one ring), up to gen_large bytes the
-// single-channel ring (4 MiB: 87 us vs 114 us), above it the multi-channel ring again (Simple,
+// config gen (default) AllReduce uses four tiers, the measured best of the generated family on a
+// B200 (8 ranks, BASELINE.md §6.3): up to gen_small bytes the ring on min(R, 8) channels x 4
+// instances with LL lines (1 KiB: 28 us vs 65-80 us for one ring), up to gen_ll128 bytes the same
+// program with LL128 lines (2 MiB: 58 us vs 86 us LL, 85 us one ring), up to gen_large bytes the
+// single-channel ring (4 MiB: 87 us vs 100 us), above it the multi-channel ring again (Simple,
 // dataflow mode: 64 MiB 0.33 ms vs 0.38 ms). Other collectives: the single-ring / direct programs.
 bool builtin_for(const Config& cfg, const std::string& coll, int R, uint64_t bytes, Program& out) {
   if (!cfg.gen || coll != "allreduce") return builtin_program(coll, R, out);
   const int C = std::min(R, 8);
-  if (bytes <= static_cast<uint64_t>(cfg.gen_small)) {
+  const uint64_t small = static_cast<uint64_t>(cfg.gen_small), mid = std::max(small, static_cast<uint64_t>(cfg.gen_ll128)),
+                 large = std::max(mid, static_cast<uint64_t>(cfg.gen_large));
+  if (bytes <= small) {
     if (!generate_program("ring", coll, R, C, 4, out)) return false;
     out.proto = Proto::ll;
     out.min_bytes = 0;
-    out.max_bytes = static_cast<uint64_t>(cfg.gen_small);
-  } else if (bytes <= static_cast<uint64_t>(cfg.gen_large)) {
+    out.max_bytes = small;
+  } else if (bytes <= mid) {
+    if (!generate_program("ring", coll, R, C, 4, out)) return false;
+    out.proto = Proto::ll128;
+    out.min_bytes = small + 1;
+    out.max_bytes = mid;
+  } else if (bytes <= large) {
     if (!generate_program("ring", coll, R, 1, 1, out)) return false;
-    out.min_bytes = static_cast<uint64_t>(cfg.gen_small) + 1;
-    out.max_bytes = static_cast<uint64_t>(cfg.gen_large);
+    out.min_bytes = mid + 1;
+    out.max_bytes = large;
   } else {
     if (!generate_program("ring", coll, R, C, 4, out)) return false;
-    out.min_bytes = static_cast<uint64_t>(cfg.gen_large) + 1;
+    out.min_bytes = large + 1;
     out.max_bytes = 1ull << 40;
   }
   return true;
@@ -2981,6 +2997,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "gen") c.gen = static_cast<int>(value);
   else if (k == "gen_small") c.gen_small = value;
   else if (k == "gen_large") c.gen_large = value;
+  else if (k == "gen_ll128") c.gen_ll128 = value;
   else if (k == "smem_kb") c.smem_kb = value;
   else if (k == "select") c.select = static_cast<int>(value);
   else if (k == "stage_kb") c.stage_kb = value;
@@ -2992,6 +3009,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "df_policy") c.df_policy = static_cast<int>(value);
   else if (k == "df_window") c.df_window = static_cast<int>(value);
   else if (k == "tma_remote") c.tma_remote = static_cast<int>(value);
+  else if (k == "force_sys") c.force_sys = static_cast<int>(value);
   else if (k == "df_items") c.df_items = static_cast<int>(value);
   else if (k == "df_max_tile") c.df_max_tile = value;
   else if (k == "df_min_tile") c.df_min_tile = value;

@@ -25,7 +25,7 @@ def _free_port():
     return p
 
 
-def _worker(proc, nproc, port, name, coll, count, dtype, proto, q, remote=1):
+def _worker(proc, nproc, port, name, coll, count, dtype, proto, q, remote=1, force_sys=0):
     import torch.distributed as dist
     from paper_2201_11840_b200 import gc3
     from gpu_util import input_len, make_input, oracle_collective, run_collective, to_np_bits
@@ -42,6 +42,7 @@ def _worker(proc, nproc, port, name, coll, count, dtype, proto, q, remote=1):
             comms = [gc3.init_rank(R, uid[0], proc * per + k) for k in range(per)]
         for c in comms:
             c.set_config("remote", remote)
+            c.set_config("force_sys", force_sys)
             c.set_config("tma_min", 4096)  # these small calls take the bulk-copy paths too
             i = c.register_ir(ir_path(name))
             if proto:
@@ -97,15 +98,31 @@ def test_two_processes_share_a_gpu(name, coll, count, dtype, proto, remote):
             assert (info["remote_messages"] > 0) == bool(remote), info
 
 
-def _run(name, coll, count, dtype, proto, remote):
+def _run(name, coll, count, dtype, proto, remote, force_sys=0):
     import torch.multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, proto, q, remote)) for p in range(2)]
+    procs = [ctx.Process(target=_worker, args=(p, 2, port, name, coll, count, dtype, proto, q, remote, force_sys)) for p in range(2)]
     for p in procs:
         p.start()
     results = [q.get(timeout=240) for _ in procs]
     for p in procs:
         p.join(timeout=60)
     return results
+
+
+@pytest.mark.parametrize("name,coll,count,dtype,proto", [
+    ("ring_ar_8_ch1", "allreduce", 8 * 40000, "float32", None),
+    ("hier_ar_2x4_par1", "allreduce", 8 * 30000, "bfloat16", None),
+    ("twostep_a2a_2x4", "alltoall", 30000, "float32", None),
+    ("ring_rs_8", "reducescatter", 20000, "int32", "ll128")])
+def test_two_processes_with_cross_gpu_code_path(name, coll, count, dtype, proto):
+    """The N-GPU code path on one GPU (config force_sys): thread blocks with a connection to the
+    other process use .sys-scope fences, flags and lines and the register path (no bulk copies),
+    while direct / pulled messages still cross the process boundary; bit-exact vs the oracle."""
+    for proc, ok, err, info in _run(name, coll, count, dtype, proto, 1, force_sys=1):
+        assert ok, (proc, err)
+        assert info["sys_scope"] == 1, info
+        if proto is None:
+            assert info["remote_messages"] > 0, info

@@ -276,7 +276,8 @@ def test_work_queue_mode(name, count, dtype, wq):
 
 @pytest.mark.parametrize("coll,count,dtype", [("allreduce", 8 * 1000 + 5, "float32"), ("allgather", 4096, "bfloat16"),
                                               ("reducescatter", 3000, "int32"), ("alltoall", 2048, "float32"),
-                                              ("allreduce", 1 << 20, "float32"), ("allreduce", 3 << 20, "float32")])
+                                              ("allreduce", 1 << 18, "float32"), ("allreduce", 1 << 20, "float32"),
+                                              ("allreduce", 3 << 20, "float32")])
 def test_builtin_programs_without_registration(coll, count, dtype):
     """Drop-in use: collectives on communicators with no registered IR run the runtime's built-in
     programs (comm-time generated, op for op the reference compiler's ring / direct algorithms;
@@ -449,6 +450,36 @@ def test_dataflow_ragged_and_repeated(name, count):
             assert comms[0].async_error()[0] == 0
             for r in range(R):
                 assert np.array_equal(to_np_bits(outs[r], "float32"), expected[r]), (it, r)
+    finally:
+        for c in comms:
+            c.destroy()
+
+
+@pytest.mark.parametrize("algo,R,C,K", [("allpairs", 8, 1, 1), ("hier", 8, 4, 1), ("hier", 8, 2, 1), ("ring", 8, 8, 4),
+                                        ("ring", 8, 2, 2), ("ring", 4, 4, 2)])
+@pytest.mark.parametrize("dtype,proto", [("float32", None), ("bfloat16", None), ("float32", "ll"), ("float32", "ll128")])
+def test_generated_programs_on_the_gpu(algo, R, C, K, dtype, proto):
+    """Comm-time generated programs (gc3IrGenerate: ring channels x instances, all-pairs,
+    hierarchical) registered as IR text and run through the C ABI: bit-exact vs the oracle running
+    the same program."""
+    from paper_2201_11840_b200 import gc3
+    from gpu_util import make_input, oracle_collective, run_collective, to_np_bits
+    text = gc3.IR.generate(algo, "allreduce", R, C, K).serialize()
+    irj = json.loads(text)
+    comms = gc3.init_all([0] * R)
+    try:
+        for c in comms:
+            i = c.register_ir(text)
+            if proto:
+                c.set_protocol(i, proto)
+        count = irj["nchunks"]["input"] * 3000 + 7
+        inputs = [make_input(count, dtype, 50 + r) for r in range(R)]
+        expected = oracle_collective(irj, "allreduce", [x.clone() for x in inputs], count, dtype)
+        outs = run_collective(comms, "allreduce", inputs, count, dtype)
+        torch.cuda.synchronize()
+        assert comms[0].async_error()[0] == 0
+        for r in range(R):
+            assert np.array_equal(to_np_bits(outs[r], dtype), expected[r]), (algo, r)
     finally:
         for c in comms:
             c.destroy()
