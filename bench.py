@@ -173,6 +173,8 @@ def setup_comms(cfg, args, R, rank, world, local_rank, dist):
             c.set_config("lanes", args.lanes)
         if args.tile_bytes:
             c.set_config("tile_bytes", args.tile_bytes)
+        if getattr(args, "builtin", False):
+            continue  # no registration: every call runs the runtime's built-in program for its size
         i = c.register_ir(path, args.instances)
         if cfg["proto"]:
             c.set_protocol(i, cfg["proto"])
@@ -318,7 +320,7 @@ def run_gc3(args, cfg):
         dist.destroy_process_group()
 
 
-def verify_outputs(cfg, comms, count, stream=None, dist=None, seed=0x5EED):
+def verify_outputs(cfg, comms, count, stream=None, dist=None, seed=0x5EED, ir_json=None):
     """Parity gate of a timed configuration: one more collective on fresh seeded inputs, checked
     exactly. AllToAll / AllGather outputs must be the exact permutation of the inputs; reductions
     must equal the CPU oracle's result (oracle/, used here only as the checker) bit for bit.
@@ -374,8 +376,11 @@ def verify_outputs(cfg, comms, count, stream=None, dist=None, seed=0x5EED):
         t = t.contiguous()
         return t.view(torch.int16).numpy().view(np.uint16) if t.element_size() == 2 else t.view(torch.int32).numpy().view(np.uint32)
 
-    with open(os.path.join(IR_DIR, cfg["ir"] + ".ir.json")) as f:
-        irj = _json.load(f)
+    if ir_json is not None:  # the program the runtime ran (e.g. a built-in), given by the caller
+        irj = ir_json
+    else:
+        with open(os.path.join(IR_DIR, cfg["ir"] + ".ir.json")) as f:
+            irj = _json.load(f)
     odt = {"bfloat16": 9, "float16": 6}.get(dt, dt)
     want = collective(irj, coll, [bits(hins[r] if r in hins else host_input(r)) for r in range(R)], count, odt, "sum",
                       mode="threaded")
@@ -663,14 +668,19 @@ def run_sweep(args, cfg):
         sizes.append(b)
         b *= 2
     tdt = getattr(torch, cfg["dtype"])
-    for proto in args.sweep_protos.split(","):
+    for proto in (["builtin"] if args.builtin else args.sweep_protos.split(",")):
         for c in comms:
-            c.set_protocol(0, proto)
+            if not args.builtin:
+                c.set_protocol(0, proto)
         for nbytes in sizes:
             count = per_rank_count(cfg, nbytes, R)
             n_in = input_elems(cfg["coll"], count, R)
+            irj = None
+            if args.builtin:  # the built-in program this size runs (size tiers), for the parity gate
+                sel = count * ESIZE[cfg["dtype"]] * (1 if cfg["coll"] == "allreduce" else R)
+                irj = json.loads(gc3.IR.builtin(cfg["coll"], R, sel).serialize())
             if cfg["coll"] in ("alltoall", "allgather") or nbytes <= (64 << 20):
-                verified = verify_outputs(cfg, comms, count, stream)
+                verified = verify_outputs(cfg, comms, count, stream, ir_json=irj)
             else:
                 verified = verify_int_sum(cfg, comms, nbytes, stream)
             ins = [torch.randn(n_in, device="cuda").to(tdt) for _ in comms]
@@ -702,7 +712,8 @@ def run_sweep(args, cfg):
             graph_us = graph_time_us(step, stream) if args.graph and nbytes <= args.graph_max else None
             err = comms[0].async_error()
             plan = comms[0].query_plan(cfg["coll"], count, cfg["dtype"])
-            print(json.dumps({"config": args.config, "ir": cfg["ir"], "ranks": R, "proto": proto, "bytes": nbytes, "us": round(ms * 1e3, 2),
+            print(json.dumps({"config": args.config, "ir": plan["name"] if args.builtin else cfg["ir"], "ranks": R, "proto": proto,
+                              "bytes": nbytes, "us": round(ms * 1e3, 2),
                               "graph_us": graph_us,
                               "algbw_gbs": round(nbytes / (ms * 1e-3) / 1e9, 2),
                               "busbw_gbs": round(nbytes / (ms * 1e-3) / 1e9 * bus_factor(cfg["coll"], R), 2),
@@ -818,6 +829,8 @@ def main():
     ap.add_argument("--sweep-max", type=int, default=1 << 30)
     ap.add_argument("--sweep-protos", default="simple,ll,ll128")
     ap.add_argument("--graph", action="store_true", help="sweep: also time collectives captured in a CUDA graph")
+    ap.add_argument("--builtin", action="store_true",
+                    help="sweep: register nothing, every size runs the runtime's built-in program (size tiers)")
     ap.add_argument("--graph-max", type=int, default=8 << 20)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
