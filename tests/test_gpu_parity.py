@@ -418,7 +418,7 @@ def test_dataflow_mode(name, count, dtype, df, tile):
 def test_dataflow_mode_is_selected_and_mails_rrs_messages():
     comms, irj = _setup("hier_ar_2x4_par1")
     try:
-        plan = comms[0].query_plan("allreduce", 8 << 20, "float32")
+        plan = comms[0].query_plan("allreduce", 32 << 20, "float32")
         assert plan["mode"] == 2
         assert plan["mail_messages"] == 8  # one rrs -> rrc message per rank
         # small messages (fewer than two items per unit) stay on static lanes by default
@@ -428,7 +428,7 @@ def test_dataflow_mode_is_selected_and_mails_rrs_messages():
             c.destroy()
     comms, irj = _setup("hier_ar_2x4_par1", df=0)
     try:
-        assert comms[0].query_plan("allreduce", 8 << 20, "float32")["mode"] == 0
+        assert comms[0].query_plan("allreduce", 32 << 20, "float32")["mode"] == 0
     finally:
         for c in comms:
             c.destroy()
