@@ -133,8 +133,9 @@ struct Config {
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
   int df = 1;                        // dataflow execution (interp_df_kernel) when every rank is in the
-                                     // launch: 1 = reducing programs with receive-and-forward chains and
-                                     // >= 8 items per unit, 2 = every Simple program, 0 = off
+                                     // launch: 1 = reducing programs with receive-and-forward chains,
+                                     // >= 2 items per unit and >= 16 tiles per chunk, 2 = every Simple
+                                     // program, 0 = off
   int df_items = 4;                  // dataflow: ready items per unit targeted by the tile size
   int64_t df_max_tile = 256 << 10;   // dataflow: largest tile
   int64_t df_min_tile = 128 << 10;   // dataflow: smallest tile (unless the chunk is smaller; measured
@@ -2065,9 +2066,9 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   KernelFn df_fn = df_ok ? interp_kernel_df(cp.redop < 0 ? 0 : dtype, cp.redop) : nullptr;
   // df 1 (default): reducing programs with receive-and-forward chains (measured on B200: C3 1.61 ->
   // 1.39 ms, C4 0.377 -> 0.335 ms, C5-RS 0.230 -> 0.228 ms; the copy-only ring AllGather runs faster
-  // on static lanes) when the launch has at least eight items per unit (C4 at 16 / 32 MiB per rank:
-  // 2-4 items per unit, 247 / 266 us dataflow vs 173 / 241 us static lanes); df 2: every Simple
-  // program
+  // on static lanes) when the launch has at least two items per unit and 16 tiles per chunk (C4 at 16
+  // / 32 MiB per rank, 4 / 8 tiles: 247 / 266 us dataflow vs 177 / 243 us static lanes); df 2: every
+  // Simple program
   const int df_units = capacity;
   int64_t df_tile = 0;
   bool use_df = c->cfg.df && df_fn && !cp.ll && !sys_scope && c->cfg.lanes <= 0 && chunk_bytes > 0 &&
@@ -2082,7 +2083,8 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     df_tile = std::max<int64_t>(df_tile / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
     if (chunk_bytes <= df_tile) df_tile = chunk_bytes;
     const int64_t items = static_cast<int64_t>(ds.plans[id].df_n) * ((chunk_bytes + df_tile - 1) / df_tile);
-    if (c->cfg.df == 1) use_df = ir.has_chain && ir.has_reduce && items >= 8LL * df_units;
+    const int64_t tiles = (chunk_bytes + df_tile - 1) / df_tile;
+    if (c->cfg.df == 1) use_df = ir.has_chain && ir.has_reduce && items >= 2LL * df_units && tiles >= 16;
   }
   if (use_df) {
     cp.df = true;
