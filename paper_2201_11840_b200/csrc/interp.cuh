@@ -1453,6 +1453,9 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
     // ready item goes to the queue
     auto count_in = [&](int k) -> int64_t {
       const DfSucc sc = a.df_succ[nd.succ + k];
+      // a successor with this item as its only predecessor is ready now: no counter (its push is a
+      // release store; a continuation stays on this unit)
+      if (sc.indeg == 1) return tile * nn + sc.node;
       int32_t* cnt = a.df_cnt + tile * nn + sc.node;
       fence_acq_rel(false);
       if (atomicAdd(cnt, 1) + 1 != sc.indeg) return -1;
