@@ -614,6 +614,21 @@ ncclResult_t rank_gpu(Comm* c, int r, std::string& out) {
   return ncclSuccess;
 }
 
+// Process id of rank r (from its bootstrap record when it lives in another process).
+ncclResult_t rank_pid(Comm* c, int r, long& out) {
+  Clique* cl = c->clique;
+  if (cl->local[r]) {
+    out = static_cast<long>(getpid());
+    return ncclSuccess;
+  }
+  std::string rec;
+  if (!read_record(shm_dir(cl->key), "rank" + std::to_string(r), rec, c->cfg.timeout_ms + 60000))
+    return set_error(ncclSystemError, "timed out waiting for rank %d's bootstrap record", r);
+  std::istringstream in(rec);
+  in >> out;
+  return ncclSuccess;
+}
+
 // ------------------------------------------------------------------------------- user buffers
 // Direct and pulled messages between ranks of different launches (other processes or GPUs) address
 // the peer's user buffers. As with NCCL user-buffer registration, every allocation a collective
@@ -1236,6 +1251,19 @@ ncclResult_t build_plan(Clique* cl, DeviceState& ds, int id) {
   // and placement), so both ends of a connection agree on its transport.
   plan.remote_ranks.clear();
   bool remote_ok = c0->cfg.remote && static_cast<int>(plan.ranks.size()) < p.ranks() && !direct.empty();
+  // every launch of a process exchanges with the other processes' launches in call order, so every
+  // process must drive exactly one launch per call (one device). Decided from the bootstrap records
+  // (pid and GPU of every rank), identically in every process: if any process hosts ranks on
+  // several devices, every cross-launch message keeps the FIFOs
+  if (remote_ok) {
+    std::map<long, std::string> gpu_of_pid;
+    for (int r = 0; r < p.ranks() && remote_ok; ++r) {
+      long pid = 0;
+      NCCL_TRY(rank_pid(c0, r, pid));
+      auto [it, fresh] = gpu_of_pid.emplace(pid, gpu_of[r]);
+      if (!fresh && it->second != gpu_of[r]) remote_ok = false;
+    }
+  }
   if (remote_ok) {
     for (int r = 0; r < p.ranks(); ++r)
       if (slot_of(r) < 0) plan.remote_ranks.push_back(r);
