@@ -147,6 +147,8 @@ struct LaunchArgs {
   int32_t discard;      // drop consumed FIFO lines from L2 (discard.global.L2)
   int32_t transports;   // mask applied to DevOp::direct (0: every message through the FIFO)
   int32_t tma_sys_ops;  // mask applied to tma_ops on thread blocks with a cross-GPU connection (DevTb::sys)
+  int64_t clip_elems;   // > 0: ragged AllReduce on the caller's buffer, tiles cut at this many elements
+                        // of the rank block (every op moves one chunk, src_off == dst_off)
   int32_t tma_ops;      // bit 0: bulk copies for pure-copy ops, bit 1: staged reductions
   int64_t tma_min;      // bytes below which an op takes the register path
   int32_t l2hint;       // bit 0: evict_last stores of hot data (DevOp::hot), bit 1: evict_first bulk loads

@@ -944,6 +944,15 @@ __device__ GC3_TRANSFER_ATTR void transfer(const DevOp& op, bool in_d, char* src
   }
 }
 
+// Clipped tiles (ragged AllReduce on the caller's buffer): the rank block holds `clip` elements, chunk
+// k covers elements [k * chunk_elems, (k + 1) * chunk_elems) of it, so the tile of an op on chunk k
+// is cut at the block's end (possibly to nothing: the op then only synchronises). 0: no clipping.
+__device__ __forceinline__ int64_t clip_tile(int64_t clip, int64_t chunk_elems, int chunk, int64_t t0, int64_t tlen) {
+  if (clip <= 0) return tlen;
+  const int64_t v = clip - static_cast<int64_t>(chunk) * chunk_elems - t0;
+  return v <= 0 ? 0 : min(v, tlen);
+}
+
 // ------------------------------------------------------------------ the interpreter
 // A "unit" of `unit_warps` warps interprets one (IR thread block, lane): for each tile of the lane,
 // for each op in order:
@@ -1149,10 +1158,10 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
                          : tile < nhb    ? a.n_head * a.small_elems + (tile - a.n_head) * tile_elems
                                          : a.n_head * a.small_elems + a.n_big * tile_elems + (tile - nhb) * a.small_elems;
       const int64_t tlen = tile < a.n_head || tile >= nhb ? a.small_elems : tile_elems;
-      const int64_t tbytes = min(tlen, chunk_elems - t0) * R::kEsize;
       const int64_t t0_bytes = t0 * R::kEsize;
       c.tile = tile;
       const DevOp op = ops[s];
+      const int64_t tbytes = clip_tile(a.clip_elems, chunk_elems, op.src_off, t0, min(tlen, chunk_elems - t0)) * R::kEsize;
       tma.pol = op.hot ? pol_last : 0;
       const bool recv = is_recv(op.opcode), send = is_send(op.opcode);
       const int tr = op.direct & a.transports;
@@ -1420,7 +1429,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
     char* const* const peer = s_bufs + kBufs * (nd.peer_slot >= 0 ? nd.peer_slot : 0);
     char* const* const rpeer = s_bufs + kBufs * (nd.recv_slot >= 0 ? nd.recv_slot : 0);
     const int64_t t0 = tile * tile_elems;
-    const int64_t tbytes = min(tile_elems, chunk_elems - t0) * R::kEsize;
+    const int64_t tbytes = clip_tile(a.clip_elems, chunk_elems, op.src_off, t0, min(tile_elems, chunk_elems - t0)) * R::kEsize;
     const int64_t t0_bytes = t0 * R::kEsize;
     tma.pol = op.hot ? pol_last : 0;
     const bool in_d = (op.direct & kInDirect) != 0, in_p = (op.direct & kInPull) != 0;

@@ -121,6 +121,7 @@ struct Config {
                                      // measured: LL ~2x faster than Simple below ~1 MiB, BASELINE §5.2)
   int64_t ll128_max_bytes = 0;       // ... and LL128 above ll_max_bytes up to this many (0: never)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
+  int clip = 1;                      // ragged AllReduce on the caller's buffer with clipped tiles (clip_ok IRs)
   int gen = 1;                       // built-in AllReduce per size tier (builtin_for); 0: one ring
   int64_t gen_small = 512 << 10;     // ... multi-channel ring with LL lines up to this many bytes
   int64_t gen_ll128 = 2 << 20;       // ... with LL128 lines up to this many
@@ -173,6 +174,7 @@ Config config_from_env() {
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
   c.ll128_max_bytes = env_int("GC3_LL128_MAX_BYTES", c.ll128_max_bytes);
   c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
+  c.clip = static_cast<int>(env_int("GC3_CLIP", c.clip));
   c.gen = static_cast<int>(env_int("GC3_GEN", c.gen));
   c.gen_small = env_int("GC3_GEN_SMALL", c.gen_small);
   c.gen_large = env_int("GC3_GEN_LARGE", c.gen_large);
@@ -329,6 +331,9 @@ struct RankIR {
   int lanes = 1;  // lanes provisioned in the arena
   bool has_reduce = false;
   bool has_chain = false;  // an op both receives and sends (rcs / rrcs / rrs): multi-hop chains
+  bool clip_ok = false;    // AllReduce whose ops each move one chunk in place and whose messages land
+                           // in the chunk they left: ragged calls run on the caller's buffer
+                           // (LaunchArgs::clip_elems) instead of padded work buffers
   uint8_t lane_mask = 0;   // transports assumed by the lane multipliers (transport_mask)
   bool builtin = false;    // registered by the runtime (builtin_program), selected after user IRs
   std::map<int64_t, double> predicted;  // timed-model microseconds per chunk size (config "select")
@@ -2270,6 +2275,10 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   bool ragged = false;
   const int64_t ce = chunk_elems_for(ir0.prog, p0.coll, p0.count, c0->nranks, &ragged);
   const int cblk = (p0.coll == kAllReduce || p0.coll == kAllGather) ? ir0.prog.nchunks[0] : ir0.prog.nchunks[0] / c0->nranks;
+  // ragged AllReduce on the caller's buffer: tiles clipped at the block's end (16-byte multiples
+  // keep the bulk, LL and LL128 paths valid) instead of staging through padded work buffers
+  const bool clip = ragged && p0.coll == kAllReduce && c0->cfg.clip && ir0.clip_ok && !cp.wq &&
+                    (p0.count * esize) % 16 == 0 && (static_cast<size_t>(ce) * esize) % 16 == 0;
   struct PostCopy {  // result copies after the launch (cudaMemcpy2DAsync arguments)
     char* dst;
     size_t dpitch;
@@ -2283,6 +2292,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
   a.tbs = plan.d_tbs;
   a.ops = plan.d_ops;
   a.deps = plan.d_deps;
+  a.clip_elems = clip ? static_cast<int64_t>(p0.count * esize / cp.kesize) : 0;
   a.chans = plan.d_chans;
   a.sems = plan.d_sems;
   a.ntbs = plan.ntbs;
@@ -2384,7 +2394,7 @@ ncclResult_t launch_device(Clique* cl, int dev, std::vector<Pending*>& ops) {
     char* result = nullptr;  // ReduceScatter: recvbuff shifted to the owned block's offset (result_writes)
     switch (p0.coll) {
       case kAllReduce:  // in-place IR on `input` (core.hpp:305-327)
-        if (ragged) {
+        if (ragged && !clip) {
           NCCL_TRY(ensure_buffer(c, c->work, c->work_bytes, pblk));
           CUDA_TRY(cudaMemcpyAsync(c->work, send, blk, cudaMemcpyDeviceToDevice, stream));
           in = out = c->work;
@@ -2568,13 +2578,25 @@ ncclResult_t register_program(Comm* comm, std::unique_ptr<RankIR> ir, int* ir_id
     else if (coll == "alltoall" && (cout != cin || cin % R)) bad = "needs nchunks.output == nchunks.input, divisible by the rank count";
     if (bad) return set_error(ncclInvalidUsage, "%s IR %s %s", coll.c_str(), p.name.c_str(), bad);
   }
+  ir->clip_ok = ir->prog.collective == "allreduce";
   for (const auto& g : ir->prog.gpus)
     for (const auto& tb : g.tbs)
       for (const auto& op : tb.ops) {
         if (op_reduces(op.op)) ir->has_reduce = true;
         if (op_receives(op.op) && op_sends(op.op)) ir->has_chain = true;
         if (op_sends(op.op) || op_receives(op.op)) ir->max_count = std::max(ir->max_count, op.count);
+        if (op.op != Opcode::nop && (op.count != 1 || op.src_off != op.dst_off)) ir->clip_ok = false;
       }
+  if (ir->clip_ok) {  // every message lands in the chunk it left (same clip length at both ends)
+    const auto snd = matched_senders(ir->prog);
+    for (int r = 0; r < ir->prog.ranks(); ++r)
+      for (size_t t = 0; t < ir->prog.gpus[r].tbs.size(); ++t)
+        for (size_t s2 = 0; s2 < ir->prog.gpus[r].tbs[t].ops.size(); ++s2) {
+          const auto& x = snd[r][t][s2];
+          if (x.rank >= 0 && ir->prog.gpus[x.rank].tbs[x.tb].ops[x.step].src_off != ir->prog.gpus[r].tbs[t].ops[s2].src_off)
+            ir->clip_ok = false;
+        }
+  }
   ir->slots = std::max(1, comm->cfg.slots);
   ir->slot_bytes = std::max<int64_t>(comm->cfg.slot_bytes / 256 * 256, 256);
   {  // lanes provisioned: enough for ~2 CUDA blocks per SM when one rank owns a device
@@ -3034,6 +3056,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
   else if (k == "ll128_max_bytes") c.ll128_max_bytes = value;
   else if (k == "builtin") c.builtin = static_cast<int>(value);
+  else if (k == "clip") c.clip = static_cast<int>(value);
   else if (k == "gen") c.gen = static_cast<int>(value);
   else if (k == "gen_small") c.gen_small = value;
   else if (k == "gen_large") c.gen_large = value;

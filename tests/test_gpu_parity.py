@@ -483,3 +483,22 @@ def test_generated_programs_on_the_gpu(algo, R, C, K, dtype, proto):
     finally:
         for c in comms:
             c.destroy()
+
+
+@pytest.mark.parametrize("name", ["ring_ar_8_ch1", "ring_ar_8_ch8_inst4", "allpairs_ar_8", "ring_ar_4_ch4_inst4"])
+@pytest.mark.parametrize("proto,cfg", [(None, {}), ("ll", {}), ("ll128", {}), (None, {"df": 2, "df_min_tile": 4096}),
+                                       (None, {"clip": 0})])
+@pytest.mark.parametrize("size", ["big", "small"])
+def test_ragged_allreduce_clipped_in_place(name, proto, cfg, size):
+    """Ragged AllReduce (count not divisible by the IR's chunks) runs on the caller's buffer with
+    tiles clipped at the block's end (LaunchArgs::clip_elems, 16-byte multiples) -- including chunks
+    that are cut short or left empty -- bit-exact vs the oracle's padded semantics; clip 0 stages
+    through the padded work buffers instead."""
+    irj = json.loads(read_ir(name))
+    c = irj["nchunks"]["input"]
+    # f32, 16-byte multiples. big: chunks of 4096 elements, the last one 4 short; small: chunks of 8
+    # elements, the block short by the largest multiple of 4 below c (several chunks empty when c > 8)
+    count = c * 4096 - 4 if size == "big" else 8 * c - 4 * ((c - 1) // 4)
+    assert -(-count // c) == (4096 if size == "big" else 8) and count % c
+    _check(name, count, "float32", proto=proto, **cfg)
+    _check(name, count, "float32", proto=proto, inplace=True, **cfg)
