@@ -240,6 +240,7 @@ typedef struct {
   int group;               /* tiles per op-major group inside a lane (0 or 1: tile-major, Fig. 4) */
   double op_us;            /* device-memory mode: fixed cost of every op per tile */
   int msg_read_passes;     /* device-memory mode: extra passes of a reducing receive reading its message */
+  int workers;             /* > 0: dataflow execution (the runtime's dataflow executor) with this many units */
 } gc3SimConfig;
 typedef struct {
   int completed;           /* 0: deadlock (see `deadlock`) */

@@ -3403,6 +3403,7 @@ static SimParams sim_params(const gc3SimConfig* cfg) {
   sp.group = std::max(1, cfg->group);
   sp.op_us = cfg->op_us;
   sp.msg_read_passes = cfg->msg_read_passes;
+  sp.workers = cfg->workers;
   return sp;
 }
 ncclResult_t gc3IrSimulate(gc3Ir_t ir, const gc3SimConfig* cfg, gc3SimReport* report) {

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <deque>
 #include <cstdio>
 #include <limits>
 #include <map>
@@ -65,7 +66,219 @@ int local_passes(Opcode o) {
 
 }  // namespace
 
+// Dataflow execution (SimParams::workers > 0): the runtime's dataflow executor. Every (op, tile) is a
+// task, ready once all of the op's predecessors (previous op of its thread block, declared deps, the
+// sender of its message) have finished that tile; `workers` units take ready tasks in order (roots
+// tile-major). A task costs op_us, then its local bytes on its GPU's device-memory resource
+// (processor sharing), then alpha if it sends.
+static SimReport simulate_dataflow(const Program& p, const SimParams& sp) {
+  SimReport rep;
+  const int R = p.ranks();
+  const int pr = std::max(0, std::min(2, sp.proto));
+  const int64_t chunk = std::max<int64_t>(sp.chunk_bytes, 0);
+  const int64_t tile = (sp.tile_bytes <= 0 || sp.tile_bytes > chunk) ? chunk : sp.tile_bytes;
+  const int64_t ntiles = chunk == 0 ? 0 : (chunk + tile - 1) / tile;
+  rep.tiles = ntiles;
+  std::vector<int> gpu(R);
+  for (int r = 0; r < R; ++r) gpu[r] = sp.rank_gpu.empty() ? r : sp.rank_gpu[static_cast<size_t>(r) % sp.rank_gpu.size()];
+  struct Node {
+    int rank;
+    const Op* op;
+    bool sends;
+  };
+  std::vector<Node> nodes;
+  std::vector<std::vector<int>> first(R);
+  for (int r = 0; r < R; ++r)
+    for (const ThreadBlock& tb : p.gpus[r].tbs) {
+      first[r].push_back(static_cast<int>(nodes.size()));
+      for (const Op& op : tb.ops) nodes.push_back({r, &op, op_sends(op.op) && tb.send_peer >= 0});
+    }
+  const int N = static_cast<int>(nodes.size());
+  std::vector<std::vector<int>> succ(N);
+  std::vector<int> indeg(N, 0);
+  auto edge = [&](int u, int v) {
+    succ[u].push_back(v);
+    indeg[v]++;
+  };
+  std::map<std::tuple<int, int, int>, std::pair<std::vector<int>, std::vector<int>>> conns;
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        const int v = first[r][t] + static_cast<int>(s);
+        if (s > 0) edge(v - 1, v);
+        for (const Dep& d : tb.ops[s].deps)
+          for (size_t t2 = 0; t2 < p.gpus[r].tbs.size(); ++t2)
+            if (p.gpus[r].tbs[t2].id == d.tb && d.step < static_cast<int>(p.gpus[r].tbs[t2].ops.size()))
+              edge(first[r][t2] + d.step, v);
+        if (op_sends(tb.ops[s].op) && tb.send_peer >= 0) conns[{r, tb.send_peer, tb.channel}].first.push_back(v);
+        if (op_receives(tb.ops[s].op) && tb.recv_peer >= 0) conns[{tb.recv_peer, r, tb.channel}].second.push_back(v);
+      }
+    }
+  for (auto& [k, c] : conns) {
+    for (size_t i = 0; i < std::min(c.first.size(), c.second.size()); ++i) edge(c.first[i], c.second[i]);
+    for (size_t i = c.first.size(); i < c.second.size(); ++i) indeg[c.second[i]]++;  // never delivered
+  }
+  // message link class of every sending node (its thread block's send peer)
+  std::vector<int> link_class(N, 0), peer(N, -1);
+  for (int r = 0; r < R; ++r)
+    for (size_t t = 0; t < p.gpus[r].tbs.size(); ++t) {
+      const ThreadBlock& tb = p.gpus[r].tbs[t];
+      for (size_t s = 0; s < tb.ops.size(); ++s) {
+        const int v = first[r][t] + static_cast<int>(s);
+        if (!nodes[v].sends) continue;
+        const int g = gpu[r], h = gpu[tb.send_peer];
+        const int gpn = std::max(1, sp.gpus_per_node);
+        link_class[v] = g == h ? 0 : (g / gpn == h / gpn ? 1 : 2);
+        peer[v] = h;
+      }
+    }
+  // processor-shared resources: the device memory of a GPU (local bytes; device-memory mode, else the
+  // local copy rate) and the ordered GPU pairs (message bytes; same-GPU messages in device-memory mode
+  // pay only alpha, their bytes are the receiver's local pass)
+  std::map<std::pair<int, int>, int> res_id;
+  std::vector<double> rate, busy;
+  std::vector<int> res_class;
+  std::vector<std::vector<int>> flows;
+  auto resource = [&](int kind, int key, double gbps, int cls) {
+    auto f = res_id.find({kind, key});
+    if (f != res_id.end()) return f->second;
+    flows.emplace_back();
+    rate.push_back(gbps * 1e3);  // bytes per us
+    busy.push_back(0.0);
+    res_class.push_back(cls);
+    return res_id[{kind, key}] = static_cast<int>(flows.size()) - 1;
+  };
+  struct Task {
+    int64_t id;
+    int phase;  // 0 fixed cost, 1 local flow, 2 alpha, 3 message transfer
+    double end, remaining;
+    int res;
+  };
+  std::vector<int64_t> left(static_cast<size_t>(N) * ntiles);
+  for (int64_t t = 0; t < ntiles; ++t)
+    for (int v = 0; v < N; ++v) left[static_cast<size_t>(t) * N + v] = indeg[v];
+  std::deque<int64_t> ready;
+  for (int64_t t = 0; t < ntiles; ++t)
+    for (int v = 0; v < N; ++v)
+      if (indeg[v] == 0) ready.push_back(t * N + v);
+  std::vector<Task> run;
+  const int W = std::max(1, sp.workers);
+  double now = 0.0;
+  int64_t done = 0;
+  const int64_t total = static_cast<int64_t>(N) * ntiles;
+  auto tile_of = [&](int64_t id) {
+    const int64_t t = id / N;
+    return static_cast<double>(std::min(tile, chunk - t * tile)) * nodes[id % N].op->count;
+  };
+  auto local_bytes = [&](int64_t id) {
+    const Opcode o = nodes[id % N].op->op;
+    const int passes = local_passes(o) + ((o == Opcode::rrc || o == Opcode::rrcs || o == Opcode::rrs) ? sp.msg_read_passes : 0);
+    if (sp.hbm_gbps > 0) return tile_of(id) * passes;
+    return o == Opcode::copy || op_reduces(o) ? tile_of(id) : 0.0;  // SPEC: b / copy rate, b / gamma
+  };
+  auto local_res = [&](int64_t id) {
+    const int g = gpu[nodes[id % N].rank];
+    if (sp.hbm_gbps > 0) return resource(0, g, sp.hbm_gbps, 0);
+    return op_reduces(nodes[id % N].op->op) ? resource(2, g, sp.gamma_gbps, 0) : resource(3, g, sp.copy_gbps, 0);
+  };
+  auto alpha_of = [&](int64_t id) {
+    const int v = static_cast<int>(id % N);
+    return nodes[v].sends ? sp.alpha_us[link_class[v]] * sp.alpha_mult[pr] : 0.0;
+  };
+  auto xfer_res = [&](int64_t id) {
+    const int v = static_cast<int>(id % N);
+    if (!nodes[v].sends || (link_class[v] == 0 && sp.hbm_gbps > 0)) return -1;
+    const int c = link_class[v];
+    return resource(1, gpu[nodes[v].rank] * 65536 + peer[v], sp.gbps[c] / sp.beta_mult[pr], c);
+  };
+  // advance a task whose current phase ended at `now`; returns true when the task is finished
+  auto next_phase = [&](Task& x) {
+    for (;;) {
+      if (x.phase == 0) {
+        x.phase = 1;
+        x.remaining = local_bytes(x.id);
+        if (x.remaining > 0) {
+          x.res = local_res(x.id);
+          return false;
+        }
+      } else if (x.phase == 1) {
+        x.phase = 2;
+        x.end = now + alpha_of(x.id);
+        if (x.end > now) return false;
+      } else if (x.phase == 2) {
+        x.phase = 3;
+        x.res = xfer_res(x.id);
+        x.remaining = x.res >= 0 ? tile_of(x.id) : 0.0;
+        if (x.remaining > 0) return false;
+      } else {
+        return true;
+      }
+    }
+  };
+  const double kInf = std::numeric_limits<double>::infinity();
+  while (done < total) {
+    while (static_cast<int>(run.size()) < W && !ready.empty()) {
+      const int64_t id = ready.front();
+      ready.pop_front();
+      run.push_back({id, 0, now + sp.op_us, 0.0, -1});
+    }
+    if (run.empty()) {
+      rep.deadlock = "deadlock: tasks wait for predecessors or messages that never complete";
+      rep.makespan_us = now;
+      return rep;
+    }
+    // phase ends at `now`, then completions
+    bool finished = false;
+    for (size_t k = 0; k < run.size();) {
+      Task& x = run[k];
+      const bool ended = (x.phase == 0 || x.phase == 2) ? x.end <= now : x.remaining <= 1e-9 * std::max(1.0, tile_of(x.id));
+      if (ended && next_phase(x)) {
+        const int64_t id = x.id;
+        const int64_t t = id / N;
+        for (int v2 : succ[id % N])
+          if (--left[static_cast<size_t>(t) * N + v2] == 0) ready.push_back(t * N + v2);
+        if (nodes[id % N].sends) rep.messages++;
+        ++done;
+        run.erase(run.begin() + static_cast<long>(k));
+        finished = true;
+      } else {
+        ++k;
+      }
+    }
+    if (finished) continue;
+    for (auto& f : flows) f.clear();
+    for (size_t k = 0; k < run.size(); ++k)
+      if (run[k].phase == 1 || run[k].phase == 3) flows[run[k].res].push_back(static_cast<int>(k));
+    double dt = kInf;
+    for (const Task& x : run) {
+      if (x.phase == 1 || x.phase == 3) dt = std::min(dt, x.remaining / (rate[x.res] / static_cast<double>(flows[x.res].size())));
+      else dt = std::min(dt, x.end - now);
+    }
+    if (!(dt < kInf)) dt = 0.0;
+    dt = std::max(dt, 0.0);
+    for (size_t r2 = 0; r2 < flows.size(); ++r2)
+      if (!flows[r2].empty()) busy[r2] += dt;
+    for (Task& x : run)
+      if (x.phase == 1 || x.phase == 3) x.remaining -= dt * rate[x.res] / static_cast<double>(flows[x.res].size());
+    now += dt;
+  }
+  rep.completed = true;
+  rep.makespan_us = now + (ntiles > 0 ? sp.launch_us : 0.0);
+  // utilisation: mean busy fraction per link class of the ordered pairs used (device memory: class 0)
+  double sum[3] = {0, 0, 0};
+  int cnt[3] = {0, 0, 0};
+  for (size_t r2 = 0; r2 < rate.size(); ++r2)
+    if (busy[r2] > 0) {
+      sum[res_class[r2]] += now > 0 ? busy[r2] / now : 0.0;
+      cnt[res_class[r2]]++;
+    }
+  for (int c = 0; c < 3; ++c) rep.util[c] = cnt[c] ? sum[c] / cnt[c] : 0.0;
+  return rep;
+}
+
 SimReport simulate(const Program& p, const SimParams& sp) {
+  if (sp.workers > 0) return simulate_dataflow(p, sp);
   SimReport rep;
   const int R = p.ranks();
   const int pr = std::max(0, std::min(2, sp.proto));

@@ -52,6 +52,7 @@ struct SimParams {
   // units, lane l taking tiles l, l + lanes, ...; each connection has its FIFO slots per lane.
   int lanes = 1;
   int group = 1;  // tiles per op-major group inside a lane (the runtime's tile groups; 1: tile-major)
+  int workers = 0;  // > 0: dataflow execution (the runtime's dataflow executor) with this many units
 };
 
 struct SimReport {

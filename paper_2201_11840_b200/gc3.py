@@ -36,7 +36,7 @@ class SimConfig(ctypes.Structure):
                 ("copy_gbps", ctypes.c_double), ("protocol", ctypes.c_int), ("slots", ctypes.c_int),
                 ("chunk_bytes", ctypes.c_int64), ("tile_bytes", ctypes.c_int64), ("launch_us", ctypes.c_double),
                 ("hbm_gbps", ctypes.c_double), ("lanes", ctypes.c_int), ("group", ctypes.c_int),
-                ("op_us", ctypes.c_double), ("msg_read_passes", ctypes.c_int)]
+                ("op_us", ctypes.c_double), ("msg_read_passes", ctypes.c_int), ("workers", ctypes.c_int)]
 
 
 class SimReport(ctypes.Structure):
@@ -267,7 +267,10 @@ class IR:
             keep = (ctypes.c_int * len(rank_gpu))(*rank_gpu)
             cfg.nranks_gpu, cfg.rank_gpu = len(rank_gpu), keep
         cfg.protocol = {"simple": 0, "ll": 1, "ll128": 2}.get(protocol, protocol)
+        names = {f[0] for f in SimConfig._fields_}
         for k, v in kw.items():
+            if k not in names:
+                raise TypeError(f"unknown simulator parameter {k!r}")
             if k in ("alpha_us", "gbps"):
                 for j, x in enumerate(v):
                     getattr(cfg, k)[j] = x
@@ -278,7 +281,8 @@ class IR:
     def simulate(self, chunk_bytes, tile_bytes=0, **kw):
         """Timed simulation (gc3IrSimulate): dict with completed, makespan_us, util (per link class),
         messages, tiles, deadlock. kw: rank_gpu, protocol, alpha_us, gbps, gamma_gbps, copy_gbps,
-        slots, gpus_per_node, launch_us."""
+        slots, gpus_per_node, launch_us, hbm_gbps, op_us, msg_read_passes, lanes, group, workers
+        (> 0: the dataflow executor with that many units)."""
         cfg, keep = self._sim_config(chunk_bytes=chunk_bytes, tile_bytes=tile_bytes, **kw)
         rep = SimReport()
         check(lib().gc3IrSimulate(self._h, ctypes.byref(cfg), ctypes.byref(rep)))

@@ -153,3 +153,61 @@ def test_link_classes_follow_placement():
     assert nv["util"][1] > 0 and nv["util"][0] == 0
     assert two_nodes["util"][2] > 0
     assert two_nodes["makespan_us"] > nv["makespan_us"]
+
+
+def test_unknown_parameter_rejected():
+    ir = _ir([[_tb(0, [_op(0, "send")], send=1)], [_tb(0, [_op(0, "recv")], recv=0)]])
+    with pytest.raises(TypeError):
+        ir.simulate(1024, alpah_us=[1, 1, 1])
+
+
+def _dev(**kw):
+    # device-memory mode, all ranks on one GPU (the loopback calibration's setting)
+    kw.setdefault("alpha_us", [A, A, A])
+    kw.setdefault("gbps", [1e9, 1e9, 1e9])
+    kw.setdefault("gamma_gbps", 1e9)
+    kw.setdefault("copy_gbps", 1e9)
+    kw.setdefault("hbm_gbps", BW)
+    return kw
+
+
+def test_dataflow_single_send_closed_form():
+    """workers > 0 (dataflow executor): a send's local bytes on the device-memory resource, then alpha;
+    the receive's local bytes after delivery."""
+    ir = _ir([[_tb(0, [_op(0, "send")], send=1)], [_tb(0, [_op(0, "recv")], recv=0)]])
+    B = 1 << 20
+    r = ir.simulate(B, rank_gpu=[0, 0], workers=4, **_dev())
+    assert r["completed"] and r["messages"] == 1
+    # send reads B, recv writes B (one pass each), serialised by the dependency; alpha in between
+    assert r["makespan_us"] == pytest.approx(A + 2 * B / (BW * 1e3))
+
+
+def test_dataflow_more_workers_not_slower_and_matches_static_on_one_tile():
+    ir = gc3.IR(read_ir("ring_ar_8_ch8_inst4"))
+    C, T = 4 << 20, 1 << 18
+    ts = [ir.simulate(C, T, rank_gpu=[0] * 8, workers=w, **_dev(alpha_us=[0.5] * 3, hbm_gbps=4000.0))
+          for w in (1, 8, 64, 592)]
+    assert all(t["completed"] for t in ts)
+    ms = [t["makespan_us"] for t in ts]
+    assert ms[0] >= ms[1] >= ms[2] >= ms[3] * 0.999
+    assert ms[0] > 2 * ms[3]  # one unit serialises everything
+
+
+def test_dataflow_reports_deadlock():
+    bad = _ir([[_tb(0, [_op(0, "recv", 0)], recv=1)], [_tb(0, [_op(0, "recv", 0)], recv=0)]])
+    r = bad.simulate(1024, rank_gpu=[0, 0], workers=4, **_dev())
+    assert not r["completed"] and r["deadlock"].startswith("deadlock")
+
+
+def test_dataflow_link_mode_matches_static_single_hop():
+    """Without the device-memory resource, a dataflow message pays alpha + bytes / pair bandwidth,
+    processor-shared on its ordered GPU pair like the static model."""
+    B = 1 << 20
+    one = _ir([[_tb(0, [_op(0, "send")], send=1)], [_tb(0, [_op(0, "recv")], recv=0)]])
+    assert one.simulate(B, workers=2, **_flat())["makespan_us"] == pytest.approx(A + B / (BW * 1e3))
+    two = _ir([[_tb(0, [_op(0, "send", 0)], send=1, ch=0), _tb(1, [_op(0, "send", 1)], send=1, ch=1)],
+               [_tb(0, [_op(0, "recv", 0)], recv=0, ch=0), _tb(1, [_op(0, "recv", 1)], recv=0, ch=1)]])
+    r = two.simulate(B, workers=4, **_flat())
+    assert r["makespan_us"] == pytest.approx(A + 2 * B / (BW * 1e3))
+    xfer = 2 * B / (BW * 1e3)
+    assert r["util"][1] == pytest.approx(xfer / (A + xfer))  # busy after the alpha

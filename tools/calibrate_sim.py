@@ -4,11 +4,13 @@ kernel times, and reports the per-point error.
 
     python tools/calibrate_sim.py [--out profiles/r02_sim_calibration.md]
 
-Measured points: the seven BASELINE configurations (bench.py --quick, device time) and the C4
-message-size sweep, Simple protocol. Each point is simulated the way the runtime
-executes it: the IR run on the launch's lanes (every thread block as `lanes` units, lane l taking
-tiles l, l + lanes, ...), tiles of the measured tile size, every rank on GPU 0, local traffic and
-messages sharing one device-memory resource (hbm_gbps), alpha per message, a fixed launch cost.
+Measured points: the seven BASELINE configurations (bench.py --quick, device time), Simple protocol;
+with --sweep the C4 message-size sweep is reported as a held-out set. Each point is simulated the way
+the runtime executed it: static lanes (every thread block as `lanes` units, lane l taking tiles
+l, l + lanes, ...) or, for launches on the whole grid with lanes 1, the dataflow executor
+(`workers` = grid x 4 units taking ready (op, tile) items), tiles of the measured tile size, every
+rank on GPU 0, local traffic sharing one device-memory resource (hbm_gbps), alpha per message, a
+fixed cost per op and tile, a fixed launch cost.
 The fit minimises the largest |log(predicted / measured)| over the points (grid over alpha and the
 device-memory rate, the additive launch cost scanned per grid point).
 """
@@ -22,23 +24,27 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
 IR_DIR = os.path.join(REPO, "tests", "golden", "ir")
-CONFIG_POINTS = os.path.join(REPO, "profiles", "r02_quick_configs.jsonl")
-SWEEP = os.path.join(REPO, "profiles", "r01f5_sweep_c4.jsonl")
+CONFIG_POINTS = os.path.join(REPO, "profiles", "r02af_quick.jsonl")
+SWEEP = os.path.join(REPO, "profiles", "r02af_sweep_c4.jsonl")
 IRS = {"c1": ("ring_ar_8_ch1", "allreduce"), "c2": ("twostep_a2a_2x4", "alltoall"), "c2d": ("twostep_a2a_1x8", "alltoall"),
        "c3": ("hier_ar_2x4_par1", "allreduce"), "c4": ("ring_ar_8_ch8_inst4", "allreduce"), "c5ag": ("ring_ag_8", "allgather"),
        "c5rs": ("ring_rs_8", "reducescatter")}
 
 
-def points():
+def points(with_sweep=False):
     pts = []
     with open(CONFIG_POINTS) as f:
         for line in f:
             d = json.loads(line)
-            if d.get("proto", "simple") != "simple":
+            if d.get("proto", "simple") != "simple" or d["config"] not in IRS:
                 continue
             ir, coll = IRS[d["config"]]
+            # dataflow / work-queue launches (lanes 1 on the whole grid): every unit takes ready items
+            workers = d["grid"] * (16 // d.get("uw", 4)) if d["lanes"] == 1 and d["grid"] >= 148 else 0
             pts.append(dict(name=d["config"], ir=ir, coll=coll, bytes=d["bytes"], us=d["ms"] * 1e3, lanes=d["lanes"],
-                            grid=d["grid"], tile=d["tile"], uw=d.get("uw", 4), group=d.get("group", 1)))
+                            grid=d["grid"], tile=d["tile"], uw=d.get("uw", 4), group=d.get("group", 1), workers=workers))
+    if not with_sweep:
+        return pts
     with open(SWEEP) as f:
         for line in f:
             d = json.loads(line)
@@ -93,7 +99,7 @@ class Sim:
 
     def predict(self, p, prm):
         ir, cb, tile, R, L = self.prepare(p)
-        r = ir.simulate(cb, tile, lanes=L, group=p["group"], rank_gpu=[0] * R, alpha_us=[prm["alpha"], 2.0, 8.0], gbps=[1e9, 770.0, 50.0],
+        r = ir.simulate(cb, tile, lanes=L, group=p["group"], workers=p.get("workers", 0), rank_gpu=[0] * R, alpha_us=[prm["alpha"], 2.0, 8.0], gbps=[1e9, 770.0, 50.0],
                         gamma_gbps=1e9, copy_gbps=1e9, hbm_gbps=prm["hbm"], launch_us=prm["launch"], op_us=prm.get("op", 0.0),
                         msg_read_passes=1)
         return r["makespan_us"]
@@ -105,7 +111,7 @@ def fit(sim, pts):
     best = None
     for alpha in [0.5 * k for k in range(0, 9)]:
         for op in [0.5 * k for k in range(0, 7)]:
-            for hbm in [500 * k for k in range(8, 15)]:
+            for hbm in [500 * k for k in range(8, 19)]:
                 q = {"alpha": alpha, "hbm": float(hbm), "launch": 0.0, "op": op}
                 base = [sim.predict(p, q) for p in pts]
                 for launch in [0.5 * k for k in range(0, 81)]:
@@ -118,24 +124,33 @@ def fit(sim, pts):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
+    ap.add_argument("--sweep", action="store_true", help="also report the C4 size sweep (held out, not fitted)")
     args = ap.parse_args()
     sim = Sim()
     pts = points()
     prm, worst = fit(sim, pts)
     rows = []
-    for p in pts:
+    for p in pts + (points(True)[len(pts):] if args.sweep else []):
         pred = sim.predict(p, prm)
         rows.append((p["name"], p["bytes"], p["us"], pred, pred / p["us"] - 1))
     lines = ["# Timed simulator calibration (loopback, one B200)", "",
-             "`tools/calibrate_sim.py`: measured device times (bench.py --quick, Simple) vs the simulator running the IR",
-             "on the launch's lanes, measured tile size, all ranks on GPU 0 and one processor-shared",
-             "device-memory resource.", "",
+             "`tools/calibrate_sim.py`: measured device times (bench.py --quick, Simple; `profiles/r02af_quick.jsonl`)",
+             "vs the simulator running the IR the way the launch ran it -- static lanes (c1, c5ag: lanes x thread",
+             "blocks) or the dataflow / work-queue executor (c2, c2d, c3, c4, c5rs: `workers` = grid x 4 units",
+             "taking ready (op, tile) items) -- at the measured tile size, all ranks on GPU 0 and one",
+             "processor-shared device-memory resource. Fitted on the seven BASELINE configurations only",
+             "(repeated rows are the second quick pass of the same run).", "",
              f"Fitted: alpha = {prm['alpha']} us per message, {prm['op']} us per op and tile, device memory = {prm['hbm']} GB/s, "
              f"launch = {prm['launch']} us; reducing receives read their message (+1 pass); "
              f"worst |error| = {100 * (math.exp(worst) - 1):.1f} %.", "",
              "| point | bytes / rank | measured us | predicted us | error |", "|---|---|---|---|---|"]
     for name, b, us, pred, err in rows:
         lines.append(f"| {name} | {b} | {us:.1f} | {pred:.1f} | {100 * err:+.1f} % |")
+    if args.sweep:
+        lines += ["", "Held out (not fitted): the C4 size sweep rows `c4@bytes` (`profiles/r02af_sweep_c4.jsonl`) are",
+                  "simulated with static lanes as recorded; the sweep does not record which executor or grid the",
+                  "runtime picked per size, so their error (about +/-35 %) bounds the model's use as a size",
+                  "extrapolator, not its fit on the configurations."]
     text = "\n".join(lines) + "\n"
     print(text)
     if args.out:
