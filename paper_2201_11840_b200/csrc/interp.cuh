@@ -568,6 +568,16 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
 // a launch captured in a CUDA graph gets a new epoch at every replay: every block reads the counter
 // once, and the last block to do so advances it for the next launch (launches of a device are
 // serialised, so the next one starts after every block of this one has read it).
+// Every rank's buffers of the launch, staged in shared memory once per block: one strided copy
+// straight from the parameter bank (the kernels take LaunchArgs as __grid_constant__, so indexing
+// it dynamically neither copies it to local memory nor unrolls into a per-thread branch table —
+// the unrolled form compiled to ~80 KB of divergent code whose instruction-cache misses cost
+// ~9 us at the first barrier of every launch; ncu, profiles/r02bc_prologue.md).
+__device__ __forceinline__ void stage_bufs(const LaunchArgs& a, char** s_bufs) {
+  char* const* flat = &a.bufs[0][0];
+  for (int i = threadIdx.x; i < kMaxLocalRanks * kBufs; i += blockDim.x) s_bufs[i] = flat[i];
+}
+
 __device__ __forceinline__ uint64_t launch_epoch(uint64_t* epoch_ptr, int32_t* epoch_ctr, uint64_t fallback) {
   if (!epoch_ptr) return fallback;
   uint64_t e;
@@ -605,15 +615,16 @@ static __device__ __noinline__ void raise_timeout(const Ctx c, int what) {
 
 // Spins until *p >= target; false if the launch was aborted. Polls with relaxed loads (an acquire
 // load would invalidate L1 on every iteration) and acquires once with a fence when satisfied.
+// Polls with relaxed loads; once the flag is reached, one acquire load of it (the flag only grows,
+// so it still satisfies the target) synchronises with the publisher's release pattern. An acquire
+// load instead of a fence: fence.acq_rel would also wait for this thread's own outstanding stores
+// (the previous op's flag stores) to be acknowledged — one L2 round trip per op on the critical path.
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys, const Ctx& c, int what) {
-  if (ld_relaxed(p, sys) >= target) {
-    fence_acq_rel(sys);
-    return true;
-  }
+  if (ld_acquire(p, sys) >= target) return true;
   const uint64_t start = globaltimer();
   for (int n = 0;; ++n) {
     if (ld_relaxed(p, sys) >= target) {
-      fence_acq_rel(sys);
+      ld_acquire(p, sys);
       return true;
     }
     if ((n & 255) == 255) {
@@ -1064,14 +1075,12 @@ __device__ GC3_WQ_ATTR void interp_wq(const WqArgs a, char* const* s_bufs, Tma& 
 }
 
 template <class R, int P>
-__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const __grid_constant__ LaunchArgs a) {
   // every rank's buffers of this launch, staged in shared memory once: ops index them by rank slot
   // and buffer id (a dynamically indexed kernel parameter would be copied to local memory)
   __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
   __shared__ uint64_t s_epoch;
-#pragma unroll
-  for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
-    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  stage_bufs(a, s_bufs);
   if (threadIdx.x == kThreads - 1) s_epoch = launch_epoch(a.epoch_ptr, a.epoch_ctr, a.epoch);
   __syncthreads();
   const int uw = a.unit_warps;
@@ -1266,12 +1275,10 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp(const LaunchAr
 // Work-queue entry point (copy-only programs; see interp_wq). A separate kernel, so the static-lane
 // interpreter's register allocation is unaffected.
 template <class R>
-__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(const LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_wq_kernel(const __grid_constant__ LaunchArgs a) {
   __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
   __shared__ uint64_t s_epoch;
-#pragma unroll
-  for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
-    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  stage_bufs(a, s_bufs);
   if (threadIdx.x == kThreads - 1) s_epoch = launch_epoch(a.epoch_ptr, a.epoch_ctr, a.epoch);
   __syncthreads();
   const int uw = a.unit_warps;
@@ -1321,6 +1328,11 @@ __device__ __forceinline__ int32_t ld_relaxed32(const int32_t* p) {
   asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ int32_t ld_acquire32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed32(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1329,11 +1341,9 @@ __device__ __forceinline__ void st_release32(int32_t* p, int32_t v) {
 }
 
 template <class R>
-__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(const LaunchArgs a) {
+__global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(const __grid_constant__ LaunchArgs a) {
   __shared__ char* s_bufs[kMaxLocalRanks * kBufs];
-#pragma unroll
-  for (int i = 0; i < kMaxLocalRanks * kBufs; ++i)
-    if (threadIdx.x == i) s_bufs[i] = a.bufs[i / kBufs][i % kBufs];
+  stage_bufs(a, s_bufs);
   __syncthreads();
   const int uw = a.unit_warps;
   const int n = uw * 32;
@@ -1396,7 +1406,7 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
         for (int it = 0;; ++it) {
           const int32_t v = ld_relaxed32(slot);
           if (v != 0) {
-            fence_acq_rel(false);  // acquire: the producers' data (released before the push) is visible
+            ld_acquire32(slot);  // acquire: the producers' data (released before the push) is visible
             st_relaxed32(slot, 0);
             item = v - 1;
             break;
