@@ -563,11 +563,7 @@ __device__ void tma_stream(Tma& m, const char* a, int64_t sa, const char* b, int
   if (t == 0) *m.seq = base + static_cast<uint32_t>(total);
 }
 
-// ------------------------------------------------------------------ launch epoch
-// The semaphore / progress tag of this launch. Read from device memory (not a kernel argument) so
-// a launch captured in a CUDA graph gets a new epoch at every replay: every block reads the counter
-// once, and the last block to do so advances it for the next launch (launches of a device are
-// serialised, so the next one starts after every block of this one has read it).
+// ------------------------------------------------------------------ launch prologue
 // Every rank's buffers of the launch, staged in shared memory once per block: one strided copy
 // straight from the parameter bank (the kernels take LaunchArgs as __grid_constant__, so indexing
 // it dynamically neither copies it to local memory nor unrolls into a per-thread branch table —
@@ -578,6 +574,10 @@ __device__ __forceinline__ void stage_bufs(const LaunchArgs& a, char** s_bufs) {
   for (int i = threadIdx.x; i < kMaxLocalRanks * kBufs; i += blockDim.x) s_bufs[i] = flat[i];
 }
 
+// The semaphore / progress tag of this launch. Read from device memory (not a kernel argument) so
+// a launch captured in a CUDA graph gets a new epoch at every replay: every block reads the counter
+// once, and the last block to do so advances it for the next launch (launches of a device are
+// serialised, so the next one starts after every block of this one has read it).
 __device__ __forceinline__ uint64_t launch_epoch(uint64_t* epoch_ptr, int32_t* epoch_ctr, uint64_t fallback) {
   if (!epoch_ptr) return fallback;
   uint64_t e;
@@ -590,8 +590,7 @@ __device__ __forceinline__ uint64_t launch_epoch(uint64_t* epoch_ptr, int32_t* e
 }
 
 // ------------------------------------------------------------------ watchdog
-// Everything here is passed by value: taking the address of a kernel parameter would force the
-// whole LaunchArgs into local memory.
+// Everything here is passed by value (a small struct the spin loops keep in registers).
 struct Ctx {
   int32_t* abort_flag;
   uint64_t* err_info;
@@ -614,11 +613,11 @@ static __device__ __noinline__ void raise_timeout(const Ctx c, int what) {
 }
 
 // Spins until *p >= target; false if the launch was aborted. Polls with relaxed loads (an acquire
-// load would invalidate L1 on every iteration) and acquires once with a fence when satisfied.
-// Polls with relaxed loads; once the flag is reached, one acquire load of it (the flag only grows,
-// so it still satisfies the target) synchronises with the publisher's release pattern. An acquire
-// load instead of a fence: fence.acq_rel would also wait for this thread's own outstanding stores
-// (the previous op's flag stores) to be acknowledged — one L2 round trip per op on the critical path.
+// load would invalidate L1 on every iteration); once the flag is reached, one acquire load of it
+// (the flag only grows, so it still satisfies the target) synchronises with the publisher's
+// release pattern. A load rather than a fence: fence.acq_rel would also wait for this thread's own
+// outstanding stores (the previous op's flag stores) to be acknowledged — one L2 round trip per op
+// on the critical path (C1 80.6 -> 75.9 us, profiles/r02be_trace.txt).
 __device__ __forceinline__ bool wait_geq(const uint64_t* p, uint64_t target, bool sys, const Ctx& c, int what) {
   if (ld_acquire(p, sys) >= target) return true;
   const uint64_t start = globaltimer();
