@@ -141,10 +141,12 @@ struct Config {
   int64_t df_max_tile = 256 << 10;   // dataflow: largest tile
   int64_t df_min_tile = 128 << 10;   // dataflow: smallest tile (unless the chunk is smaller; measured
                                      // best on C3 / C4 / C5-RS: 64-128 KiB, per-item costs ~3 us)
-  int df_policy = 1;                 // dataflow scheduling: bit 0 continuations (depth first)
+  int df_policy = 1;                 // dataflow scheduling: bit 0 continuations (depth first); bit 1
+                                     // successor counters with fence + atomic + fence (default: one acq_rel atomic)
   int df_window = 0;                 // dataflow: tiles in flight ahead of the finished items (0: unbounded)
   int64_t df_big_bytes = 1ll << 30;  // dataflow: programs with at least this many bytes of buffers ...
   int64_t df_big_tile = 64 << 10;    // ... use tiles of at most this many bytes
+  int df_waves = 1;                  // dataflow: tile count rounded to whole waves of units (plan_launch)
   int remote = 1;                    // direct / pulled messages to ranks of other launches through
                                      // registered user buffers (exchange_buffers); 0: FIFO only
   int tma_remote = 0;                // bulk copies on thread blocks with a cross-GPU connection
@@ -189,6 +191,7 @@ Config config_from_env() {
   c.df_items = static_cast<int>(env_int("GC3_DF_ITEMS", c.df_items));
   c.df_max_tile = env_int("GC3_DF_MAX_TILE", c.df_max_tile);
   c.df_min_tile = env_int("GC3_DF_MIN_TILE", c.df_min_tile);
+  c.df_waves = static_cast<int>(env_int("GC3_DF_WAVES", c.df_waves));
   c.remote = static_cast<int>(env_int("GC3_REMOTE", c.remote));
   c.df_policy = static_cast<int>(env_int("GC3_DF_POLICY", c.df_policy));
   c.df_window = static_cast<int>(env_int("GC3_DF_WINDOW", c.df_window));
@@ -2123,6 +2126,22 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     const int64_t footprint = static_cast<int64_t>(p.ranks()) * (p.nchunks[0] + (p.inplace ? 0 : p.nchunks[1]) + p.nchunks[2]) * chunk_bytes;
     if (c->cfg.tile_bytes <= 0 && footprint >= c->cfg.df_big_bytes) df_tile = std::min<int64_t>(df_tile, c->cfg.df_big_tile);
     df_tile = std::max<int64_t>(df_tile / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
+    // whole waves: a chain program's items run level by level (width items per tile per level), so
+    // width x tiles just above a multiple of the units leaves a partial wave at every level (C4,
+    // width 32 on 592 units: 20 tiles 0.425 ms, 16 tiles 0.314 ms, 18 tiles 0.303 ms). Round the
+    // tile count to the nearest multiple of units / width when that moves the tile by <= 25 %.
+    if (c->cfg.tile_bytes <= 0 && c->cfg.df_waves && footprint < c->cfg.df_big_bytes && chunk_bytes > df_tile) {
+      const int64_t per_wave = df_units / width;
+      const int64_t tiles0 = (chunk_bytes + df_tile - 1) / df_tile;
+      if (per_wave >= 1) {
+        const int64_t k = std::max<int64_t>(1, (tiles0 + per_wave / 2) / per_wave);
+        const int64_t t1 = (chunk_bytes + k * per_wave - 1) / (k * per_wave);
+        const int64_t tile1 = (t1 + 127) / 128 * 128;
+        if (4 * tile1 >= 3 * df_tile && 4 * tile1 <= 5 * df_tile && tile1 <= c->cfg.df_max_tile &&
+            width * ((chunk_bytes + tile1 - 1) / tile1) <= k * df_units)
+          df_tile = tile1;
+      }
+    }
     if (chunk_bytes <= df_tile) df_tile = chunk_bytes;
     const int64_t items = static_cast<int64_t>(ds.plans[id].df_n) * ((chunk_bytes + df_tile - 1) / df_tile);
     const int64_t tiles = (chunk_bytes + df_tile - 1) / df_tile;
@@ -3078,6 +3097,7 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "df_items") c.df_items = static_cast<int>(value);
   else if (k == "df_max_tile") c.df_max_tile = value;
   else if (k == "df_min_tile") c.df_min_tile = value;
+  else if (k == "df_waves") c.df_waves = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
