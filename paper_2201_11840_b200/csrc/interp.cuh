@@ -1335,6 +1335,14 @@ __device__ __forceinline__ int32_t ld_acquire32(const int32_t* p) {
 __device__ __forceinline__ void st_relaxed32(int32_t* p, int32_t v) {
   asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// one acq_rel read-modify-write: releases this unit's data (gathered by the barrier before it) and,
+// for the last predecessor to arrive, acquires every earlier predecessor's release (their RMWs
+// extend one release sequence on the counter) — a fence, an atomic and a second fence before
+__device__ __forceinline__ int32_t atom_add_acq_rel32(int32_t* p, int32_t v) {
+  int32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
 __device__ __forceinline__ void st_release32(int32_t* p, int32_t v) {
   asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -1475,10 +1483,14 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
       // release store; a continuation stays on this unit)
       if (sc.indeg == 1) return tile * nn + sc.node;
       int32_t* cnt = a.df_cnt + tile * nn + sc.node;
-      fence_acq_rel(false);
-      if (atomicAdd(cnt, 1) + 1 != sc.indeg) return -1;
-      __threadfence();  // acquire the other predecessors' releases (read through the counter)
-      *cnt = 0;         // ready: reset for the next launch
+      if (a.df_policy & 2) {
+        fence_acq_rel(false);
+        if (atomicAdd(cnt, 1) + 1 != sc.indeg) return -1;
+        __threadfence();  // acquire the other predecessors' releases (read through the counter)
+      } else if (atom_add_acq_rel32(cnt, 1) + 1 != sc.indeg) {
+        return -1;
+      }
+      *cnt = 0;  // ready: reset for the next launch
       return tile * nn + sc.node;
     };
     auto push = [&](int64_t ready) {
