@@ -1490,19 +1490,25 @@ __global__ void __launch_bounds__(kThreads, GC3_MINBLOCKS) interp_df_kernel(cons
       } else if (atom_add_acq_rel32(cnt, 1) + 1 != sc.indeg) {
         return -1;
       }
-      *cnt = 0;  // ready: reset for the next launch
-      return tile * nn + sc.node;
+      return tile * nn + sc.node;  // its counter (df_cnt[ready]) is reset after the push
     };
+    // a ready item's counter is reset for the next launch only after its push: the push's release
+    // would otherwise wait for the reset store to be acknowledged
     auto push = [&](int64_t ready) {
       const int32_t pos = atomicAdd(push_ctr, 1);
       st_release32(a.df_q + pos, static_cast<int32_t>(ready) + 1);
+      a.df_cnt[ready] = 0;
     };
     if (t < 32) {
       const int64_t ready = t < nd.nsucc ? count_in(t) : -1;
       const unsigned ready_mask = __ballot_sync(0xffffffffu, ready >= 0);
       if (ready >= 0) {
-        if ((a.df_policy & 1) && t == __ffs(ready_mask) - 1) s_cont[uib] = ready;
-        else push(ready);
+        if ((a.df_policy & 1) && t == __ffs(ready_mask) - 1) {
+          s_cont[uib] = ready;
+          a.df_cnt[ready] = 0;
+        } else {
+          push(ready);
+        }
       }
     }
     for (int k = t < 32 ? t + n : t; k < nd.nsucc; k += n) {

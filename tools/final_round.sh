@@ -15,9 +15,10 @@ for c in c1 c1ap c2 c2d c3 c4 c4auto c5ag c5rs; do timeout 180 python bench.py -
 for c in c1 c4; do timeout 180 python bench.py --config $c --quick --steps 20 --proto ll >> $o/quick.jsonl 2>>$o/quick.err; done
 timeout 900 python bench.py --config c4 --sweep --steps 20 --graph > $o/sweep_c4.jsonl 2> $o/sweep_c4.err
 timeout 600 python bench.py --config c1 --sweep --steps 20 --sweep-max 268435456 --graph > $o/sweep_c1.jsonl 2> $o/sweep_c1.err
+timeout 600 python bench.py --config c4 --sweep --builtin --sweep-max 16777216 --steps 20 --graph > $o/sweep_builtin.jsonl 2> $o/sweep_builtin.err
 timeout 600 python bench.py > $o/bench.json 2> $o/bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $o/bench_ref.json 2> $o/bench_ref.err
-bash tools/gpu_ncu.sh $tag "c2 c3 c4 c5rs c5ag" > /dev/null 2>&1
+bash tools/gpu_ncu.sh $tag "c2 c3 c4 c5rs c5ag c1" > /dev/null 2>&1
 # LL capture of C4 under its own name
 mkdir -p $o/ll
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $o/launches_c4ll.csv \
