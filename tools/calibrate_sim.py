@@ -24,8 +24,8 @@ REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, REPO)
 
 IR_DIR = os.path.join(REPO, "tests", "golden", "ir")
-CONFIG_POINTS = os.path.join(REPO, "profiles", "r02af_quick.jsonl")
-SWEEP = os.path.join(REPO, "profiles", "r02af_sweep_c4.jsonl")
+CONFIG_POINTS = os.path.join(REPO, "profiles", "r02z_quick.jsonl")
+SWEEP = os.path.join(REPO, "profiles", "r02z_sweep_c4.jsonl")
 IRS = {"c1": ("ring_ar_8_ch1", "allreduce"), "c2": ("twostep_a2a_2x4", "alltoall"), "c2d": ("twostep_a2a_1x8", "alltoall"),
        "c3": ("hier_ar_2x4_par1", "allreduce"), "c4": ("ring_ar_8_ch8_inst4", "allreduce"), "c5ag": ("ring_ag_8", "allgather"),
        "c5rs": ("ring_rs_8", "reducescatter")}
@@ -134,7 +134,7 @@ def main():
         pred = sim.predict(p, prm)
         rows.append((p["name"], p["bytes"], p["us"], pred, pred / p["us"] - 1))
     lines = ["# Timed simulator calibration (loopback, one B200)", "",
-             "`tools/calibrate_sim.py`: measured device times (bench.py --quick, Simple; `profiles/r02af_quick.jsonl`)",
+             f"`tools/calibrate_sim.py`: measured device times (bench.py --quick, Simple; `profiles/{os.path.basename(CONFIG_POINTS)}`)",
              "vs the simulator running the IR the way the launch ran it -- static lanes (c1, c5ag: lanes x thread",
              "blocks) or the dataflow / work-queue executor (c2, c2d, c3, c4, c5rs: `workers` = grid x 4 units",
              "taking ready (op, tile) items) -- at the measured tile size, all ranks on GPU 0 and one",
@@ -147,10 +147,13 @@ def main():
     for name, b, us, pred, err in rows:
         lines.append(f"| {name} | {b} | {us:.1f} | {pred:.1f} | {100 * err:+.1f} % |")
     if args.sweep:
-        lines += ["", "Held out (not fitted): the C4 size sweep rows `c4@bytes` (`profiles/r02af_sweep_c4.jsonl`) are",
+        held = [abs(r[4]) for r in rows[len(pts):]]
+        big = [abs(r[4]) for r in rows[len(pts):] if r[1] >= (64 << 20)]
+        lines += ["", f"Held out (not fitted): the C4 size sweep rows `c4@bytes` (`profiles/{os.path.basename(SWEEP)}`) are",
                   "simulated with static lanes as recorded; the sweep does not record which executor or grid the",
-                  "runtime picked per size, so their error (about +/-35 %) bounds the model's use as a size",
-                  "extrapolator, not its fit on the configurations."]
+                  f"runtime picked per size. Worst held-out error {100 * max(held):.0f} % overall, {100 * max(big or [0]):.0f} % from 64 MiB",
+                  "per rank up: the fitted fixed launch cost absorbs per-launch work of the large configurations and",
+                  "overstates the small-message floor, so the model extrapolates in size only above a few MiB."]
     text = "\n".join(lines) + "\n"
     print(text)
     if args.out:
