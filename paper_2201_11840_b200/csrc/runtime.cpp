@@ -2128,17 +2128,17 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     df_tile = std::max<int64_t>(df_tile / 128 * 128, 128);  // whole L2 lines (mailbox discard, bulk alignment)
     // whole waves: a chain program's items run level by level (width items per tile per level), so
     // width x tiles just above a multiple of the units leaves a partial wave at every level (C4,
-    // width 32 on 592 units: 20 tiles 0.425 ms, 16 tiles 0.314 ms, 18 tiles 0.303 ms). Round the
-    // tile count to the nearest multiple of units / width when that moves the tile by <= 25 %.
+    // width 32 on 592 units: 20 tiles 0.425 ms, 16 tiles 0.314 ms, 18 tiles 0.303 ms). When about
+    // one wave per level fits, round the tile count to units / width if that moves the tile by
+    // <= 25 % (several waves per level overlap: C5-RS, 64 -> 74 tiles, measured 1 % slower).
     if (c->cfg.tile_bytes <= 0 && c->cfg.df_waves && footprint < c->cfg.df_big_bytes && chunk_bytes > df_tile) {
-      const int64_t per_wave = df_units / width;
-      const int64_t tiles0 = (chunk_bytes + df_tile - 1) / df_tile;
+      const int64_t per_wave = df_units / width;  // tiles whose items fill one wave of units
       if (per_wave >= 1) {
-        const int64_t k = std::max<int64_t>(1, (tiles0 + per_wave / 2) / per_wave);
-        const int64_t t1 = (chunk_bytes + k * per_wave - 1) / (k * per_wave);
-        const int64_t tile1 = (t1 + 127) / 128 * 128;
-        if (4 * tile1 >= 3 * df_tile && 4 * tile1 <= 5 * df_tile && tile1 <= c->cfg.df_max_tile &&
-            width * ((chunk_bytes + tile1 - 1) / tile1) <= k * df_units)
+        const int64_t tile1 = ((chunk_bytes + per_wave - 1) / per_wave + 127) / 128 * 128;
+        const int64_t tiles0 = (chunk_bytes + df_tile - 1) / df_tile, tiles1 = (chunk_bytes + tile1 - 1) / tile1;
+        // (never below the 16 tiles per chunk the dataflow choice below asks for)
+        if (4 * tile1 >= 3 * df_tile && 4 * tile1 <= 5 * df_tile && tile1 <= c->cfg.df_max_tile && width * tiles1 <= df_units &&
+            (tiles1 >= 16 || tiles1 >= tiles0))
           df_tile = tile1;
       }
     }
