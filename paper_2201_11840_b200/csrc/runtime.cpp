@@ -129,7 +129,8 @@ struct Config {
   int64_t smem_kb = 192;             // shared memory for bulk-engine stages per block (<= 220)
   int select = 0;                    // among matching IRs pick the lowest timed-model prediction
   int64_t stage_kb = 0;              // bytes per stage (0: automatic, 3+ stages per unit)
-  int wq_items = 4;                  // work items per unit targeted by the work-queue tile size
+  int wq_items = 6;                  // work items per unit targeted by the work-queue tile size (measured,
+                                     // C2: 4 -> 0.903, 5 -> 0.911, 6 -> 0.915, 7 -> 0.912, 8 -> 0.900 of the roofline)
   int wq_lag = 0;                    // claim deeper thread blocks' items this many tiles later (0: off)
   int discard = 1;                   // discard consumed FIFO lines from L2
   int group = 0;                     // tiles per op-major group in a lane; 0 = largest deadlock-free
