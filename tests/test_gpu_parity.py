@@ -434,6 +434,30 @@ def test_dataflow_mode_is_selected_and_mails_rrs_messages():
             c.destroy()
 
 
+@pytest.mark.parametrize("waves", [1, 0])
+def test_dataflow_whole_wave_tiles(waves):
+    """Dataflow tile count rounded to one wave of units per level (config df_waves, runtime.cpp
+    plan_launch): C4's program (width 32: 480 nodes over 15 levels) at 64 KiB chunks with 4 KiB
+    minimum tiles takes units / 32 tiles per chunk (18 on a B200, the last one ragged) instead of
+    16; bit-exact vs the oracle either way."""
+    count = 32 * 16384  # 2 MiB per rank, 64 KiB chunks
+    cfg = dict(df_min_tile=4096, df_waves=waves)
+    comms, _ = _setup("ring_ar_8_ch8_inst4", **cfg)
+    try:
+        plan = comms[0].query_plan("allreduce", count, "float32")
+        assert plan["mode"] == 2
+        units = plan["grid"] * (512 // (32 * plan["unit_warps"]))
+        if waves:
+            assert 16 <= plan["ntiles"] and plan["ntiles"] * 32 <= units
+            assert plan["ntiles"] == units // 32 or units // 32 < 16
+        else:
+            assert plan["ntiles"] == 16
+    finally:
+        for c in comms:
+            c.destroy()
+    _check("ring_ar_8_ch8_inst4", count, **cfg)
+
+
 @pytest.mark.parametrize("name,count", [("ring_ar_8_ch1", 8 * 1000 + 3), ("ring_rs_8", 777), ("ring_ag_8", 1001)])
 def test_dataflow_ragged_and_repeated(name, count):
     from gpu_util import make_input, oracle_collective, run_collective, to_np_bits
