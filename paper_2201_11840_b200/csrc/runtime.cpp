@@ -147,7 +147,10 @@ struct Config {
   int df_window = 0;                 // dataflow: tiles in flight ahead of the finished items (0: unbounded)
   int64_t df_big_bytes = 1ll << 30;  // dataflow: programs with at least this many bytes of buffers ...
   int64_t df_big_tile = 64 << 10;    // ... use tiles of at most this many bytes
-  int df_waves = 1;                  // dataflow: tile count rounded to whole waves of units (plan_launch)
+  int df_waves = 2;                  // dataflow: 1 tile count rounded to whole waves of units; 2 also
+                                     // one-wave tiles for reducing chain programs (plan_launch)
+  int64_t df_wave_min_tile = 4 << 10;  // ... down to this tile size
+  int df_wave_max_lanes = 16;          // ... for programs whose static-lane plan has fewer lanes
   int remote = 1;                    // direct / pulled messages to ranks of other launches through
                                      // registered user buffers (exchange_buffers); 0: FIFO only
   int tma_remote = 0;                // bulk copies on thread blocks with a cross-GPU connection
@@ -193,6 +196,8 @@ Config config_from_env() {
   c.df_max_tile = env_int("GC3_DF_MAX_TILE", c.df_max_tile);
   c.df_min_tile = env_int("GC3_DF_MIN_TILE", c.df_min_tile);
   c.df_waves = static_cast<int>(env_int("GC3_DF_WAVES", c.df_waves));
+  c.df_wave_min_tile = env_int("GC3_DF_WAVE_MIN_TILE", c.df_wave_min_tile);
+  c.df_wave_max_lanes = static_cast<int>(env_int("GC3_DF_WAVE_MAX_LANES", c.df_wave_max_lanes));
   c.remote = static_cast<int>(env_int("GC3_REMOTE", c.remote));
   c.df_policy = static_cast<int>(env_int("GC3_DF_POLICY", c.df_policy));
   c.df_window = static_cast<int>(env_int("GC3_DF_WINDOW", c.df_window));
@@ -2147,6 +2152,23 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
     const int64_t items = static_cast<int64_t>(ds.plans[id].df_n) * ((chunk_bytes + df_tile - 1) / df_tile);
     const int64_t tiles = (chunk_bytes + df_tile - 1) / df_tile;
     if (c->cfg.df == 1) use_df = ir.has_chain && ir.has_reduce && items >= 2LL * df_units && tiles >= 16;
+    // one wave per level (df_waves 2): a reducing chain program that runs dataflow anyway, or whose
+    // static-lane plan has fewer than df_wave_max_lanes lanes (tiles that barely pipeline), runs on
+    // the dataflow executor with exactly units ÷ width tiles when that tile is >= df_wave_min_tile
+    // (measured, `profiles/r02bt_one_wave.jsonl`: C4's program 8 MiB 124 -> 88 us, 16 MiB 153 ->
+    // 115 us, 32 MiB 213 -> 169 us, 96 MiB 530 -> 495 us; C3's 4 MiB 176 -> 78 us, 32 MiB 260 ->
+    // 179 us; programs of few thread blocks keep their 64 static lanes: C1 / C5-RS at 4 MiB are
+    // faster there)
+    if (c->cfg.df == 1 && c->cfg.df_waves >= 2 && c->cfg.tile_bytes <= 0 && footprint < c->cfg.df_big_bytes && ir.has_chain &&
+        ir.has_reduce && (use_df || cp.lanes < c->cfg.df_wave_max_lanes)) {
+      const int64_t per_wave = df_units / width;
+      const int64_t tile_w = per_wave >= 1 ? ((chunk_bytes + per_wave - 1) / per_wave + 127) / 128 * 128 : 0;
+      if (per_wave >= 16 && tile_w >= c->cfg.df_wave_min_tile && tile_w <= c->cfg.df_max_tile && tile_w < chunk_bytes &&
+          width * ((chunk_bytes + tile_w - 1) / tile_w) <= df_units) {
+        df_tile = tile_w;
+        use_df = true;
+      }
+    }
   }
   if (use_df) {
     cp.df = true;
@@ -3099,6 +3121,8 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "df_max_tile") c.df_max_tile = value;
   else if (k == "df_min_tile") c.df_min_tile = value;
   else if (k == "df_waves") c.df_waves = static_cast<int>(value);
+  else if (k == "df_wave_min_tile") c.df_wave_min_tile = value;
+  else if (k == "df_wave_max_lanes") c.df_wave_max_lanes = static_cast<int>(value);
   else return set_error(ncclInvalidArgument, "unknown config key %s", key);
   return ncclSuccess;
 }
