@@ -148,9 +148,10 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
  * "tma_min", "discard", "wq" (work-queue mode; 2 = also for chain programs), "wq_items", "taper",
  * "ll_max_bytes" (Simple IRs run LL up to this many bytes per rank), "trace"; dataflow executor:
  * "df" (0 off, 1 reducing chain programs, 2 every Simple program), "df_items", "df_min_tile",
- * "df_max_tile", "df_big_bytes", "df_big_tile", "df_waves" (tile count rounded to whole waves of
- * units), "df_policy" (bit 0 continuations, bit 1 fence + atomic + fence successor counters),
- * "df_window". */
+ * "df_max_tile", "df_big_bytes", "df_big_tile", "df_waves" (1: tile count rounded to whole waves
+ * of units; 2: also one wave per level for reducing chain programs whose static plan has fewer than
+ * "df_wave_max_lanes" lanes, tiles down to "df_wave_min_tile"), "df_policy" (bit 0 continuations,
+ * bit 1 fence + atomic + fence successor counters), "df_window". */
 ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value);
 
 /* In-kernel event log of the last launch on comm's device when config "trace" (GC3_TRACE) is set
