@@ -146,7 +146,9 @@ ncclResult_t gc3QueryPlan(ncclComm_t comm, int collective, size_t count, ncclDat
  * evict_first loads). Launch-time keys: "lanes", "tile_bytes", "timeout_ms", "unit_warps", "group"
  * (0 = automatic), "tma" (bit 0 bulk copies, bit 1 staged reductions, bit 2 register-store copies),
  * "tma_min", "discard", "wq" (work-queue mode; 2 = also for chain programs), "wq_items", "taper",
- * "ll_max_bytes" (Simple IRs run LL up to this many bytes per rank), "trace"; dataflow executor:
+ * "ll_max_bytes" / "ll128_max_bytes" (Simple IRs with >= "ll_wide_tbs" thread blocks per rank run
+ * LL / LL128 up to these many bytes per rank; narrower IRs with >= 8 ops per thread block run LL up
+ * to "ll_narrow_max_bytes"), "trace"; dataflow executor:
  * "df" (0 off, 1 reducing chain programs, 2 every Simple program), "df_items", "df_min_tile",
  * "df_max_tile", "df_big_bytes", "df_big_tile", "df_waves" (1: tile count rounded to whole waves
  * of units; 2: also one wave per level for reducing chain programs whose static plan has fewer than

@@ -119,7 +119,11 @@ struct Config {
   int64_t tma_min = 32 << 10;        // ops moving fewer bytes take the register path
   int64_t ll_max_bytes = 512 << 10;  // Simple IRs run LL up to this many bytes per rank (0: never;
                                      // measured: LL ~2x faster than Simple below ~1 MiB, BASELINE §5.2)
-  int64_t ll128_max_bytes = 0;       // ... and LL128 above ll_max_bytes up to this many (0: never)
+  int64_t ll128_max_bytes = 2 << 20;  // ... and LL128 above ll_max_bytes up to this many (0: never)
+  int ll_wide_tbs = 16;              // both thresholds apply to IRs with this many thread blocks per rank
+                                     // (many short chains); narrower IRs run LL only up to
+  int64_t ll_narrow_max_bytes = 16 << 10;  // this many bytes (measured, profiles/r02bw_*: Simple
+                                     // faster from 16-32 KiB on every narrow BASELINE program)
   int builtin = 1;                   // calls no registered IR matches run the built-in programs
   int clip = 1;                      // ragged AllReduce on the caller's buffer with clipped tiles (clip_ok IRs)
   int gen = 1;                       // built-in AllReduce per size tier (builtin_for); 0: one ring
@@ -179,6 +183,8 @@ Config config_from_env() {
   c.tma_min = env_int("GC3_TMA_MIN", c.tma_min);
   c.ll_max_bytes = env_int("GC3_LL_MAX_BYTES", c.ll_max_bytes);
   c.ll128_max_bytes = env_int("GC3_LL128_MAX_BYTES", c.ll128_max_bytes);
+  c.ll_wide_tbs = static_cast<int>(env_int("GC3_LL_WIDE_TBS", c.ll_wide_tbs));
+  c.ll_narrow_max_bytes = env_int("GC3_LL_NARROW_MAX_BYTES", c.ll_narrow_max_bytes);
   c.builtin = static_cast<int>(env_int("GC3_BUILTIN", c.builtin));
   c.clip = static_cast<int>(env_int("GC3_CLIP", c.clip));
   c.gen = static_cast<int>(env_int("GC3_GEN", c.gen));
@@ -1929,13 +1935,27 @@ ncclResult_t plan_call(Comm* c, DeviceState& ds, int id, int coll, size_t count,
   cp.kesize = ir.has_reduce ? static_cast<int>(esize) : 1;
   const int64_t chunk_bytes = ce * static_cast<int64_t>(esize);
   cp.chunk_elems = chunk_bytes / cp.kesize;
-  // protocol: the override, else the IR's tag; a Simple IR runs LL for messages up to ll_max_bytes
-  // per rank (no fences on the data path: measured ~2x lower latency below ~1 MiB)
+  // protocol: the override, else the IR's tag; a Simple IR with many thread blocks per rank (many
+  // short chains, e.g. 8 channels x 4 instances) runs LL for messages up to ll_max_bytes per rank
+  // and LL128 up to ll128_max_bytes (no fences on the data path: C4's program 1 MiB 52 -> 32 us,
+  // 2 MiB 71 -> 44 us); narrower programs only up to ll_narrow_max_bytes (Simple measured faster
+  // above 16-32 KiB for one ring, all-pairs, hierarchical, two-step, ring AG / RS)
   int proto = ir.proto_override >= 0 ? ir.proto_override : static_cast<int>(p.proto);
   if (ir.proto_override < 0 && proto == kProtoSimple) {
     const uint64_t sb = selection_bytes(coll, count, esize, c->nranks);
-    if (c->cfg.ll_max_bytes > 0 && sb <= static_cast<uint64_t>(c->cfg.ll_max_bytes)) proto = kProtoLL;
-    else if (c->cfg.ll128_max_bytes > 0 && sb <= static_cast<uint64_t>(c->cfg.ll128_max_bytes)) proto = kProtoLL128;
+    size_t tbs_rank = 0, ops_tb = 0;
+    for (const auto& g : p.gpus) {
+      tbs_rank = std::max(tbs_rank, g.tbs.size());
+      for (const auto& tb : g.tbs) ops_tb = std::max(ops_tb, tb.ops.size());
+    }
+    const bool wide = static_cast<int64_t>(tbs_rank) >= c->cfg.ll_wide_tbs;
+    // (narrow programs with short op lists — all-pairs, hierarchical, two-step — measured faster on
+    // Simple at every size tried; long sequential chains gain from LL's cheaper hops)
+    const int64_t ll_max = wide ? c->cfg.ll_max_bytes
+                                : ops_tb >= 8 ? std::min(c->cfg.ll_max_bytes, c->cfg.ll_narrow_max_bytes) : 0;
+    const int64_t ll128_max = wide ? c->cfg.ll128_max_bytes : 0;
+    if (ll_max > 0 && sb <= static_cast<uint64_t>(ll_max)) proto = kProtoLL;
+    else if (ll128_max > 0 && sb <= static_cast<uint64_t>(ll128_max)) proto = kProtoLL128;
   }
   // line protocols move 8-byte words: chunks of other sizes run Simple
   cp.proto = proto != kProtoSimple && chunk_bytes % 8 == 0 ? proto : kProtoSimple;
@@ -3097,6 +3117,8 @@ ncclResult_t gc3SetConfig(ncclComm_t comm, const char* key, int64_t value) {
   else if (k == "tma_min") c.tma_min = value;
   else if (k == "ll_max_bytes") c.ll_max_bytes = value;
   else if (k == "ll128_max_bytes") c.ll128_max_bytes = value;
+  else if (k == "ll_wide_tbs") c.ll_wide_tbs = static_cast<int>(value);
+  else if (k == "ll_narrow_max_bytes") c.ll_narrow_max_bytes = value;
   else if (k == "builtin") c.builtin = static_cast<int>(value);
   else if (k == "clip") c.clip = static_cast<int>(value);
   else if (k == "gen") c.gen = static_cast<int>(value);

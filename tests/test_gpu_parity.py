@@ -441,7 +441,7 @@ def test_dataflow_whole_wave_tiles(waves):
     minimum tiles takes units / 32 tiles per chunk (18 on a B200, the last one ragged) instead of
     16; bit-exact vs the oracle either way."""
     count = 32 * 16384  # 2 MiB per rank, 64 KiB chunks
-    cfg = dict(df_min_tile=4096, df_waves=waves)
+    cfg = dict(df_min_tile=4096, df_waves=waves, ll_max_bytes=0, ll128_max_bytes=0)  # Simple at 2 MiB
     comms, _ = _setup("ring_ar_8_ch8_inst4", **cfg)
     try:
         plan = comms[0].query_plan("allreduce", count, "float32")
