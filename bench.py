@@ -46,6 +46,8 @@ CONFIGS = {
                  desc="All-pairs AllReduce GC3-IR, 8 ranks, fp32 4 MB buffer (small-message alternative to C1)"),
     "c4auto": dict(ir="ring_ar_8_inst4_auto", coll="allreduce", dtype="float32", bytes=64 << 20, proto="simple",
                    desc="Ring AllReduce instances=4, automatic channels"),
+    "c4i1": dict(ir="ring_ar_8_ch8_inst1", coll="allreduce", dtype="float32", bytes=64 << 20, proto=None,
+                 desc="Ring AllReduce channels=8, instances=1 (sweep / quick only)"),
     # C5 at 2 and 4 ranks (sweep / quick only; the 8-rank bench line stays the default contract)
     "c5ag4": dict(ir="ring_ag_4", coll="allgather", dtype="float32", bytes=64 << 20, proto=None, desc="Ring AllGather, 4 ranks"),
     "c5ag2": dict(ir="ring_ag_2", coll="allgather", dtype="float32", bytes=64 << 20, proto=None, desc="Ring AllGather, 2 ranks"),

@@ -120,7 +120,7 @@ struct Config {
   int64_t ll_max_bytes = 512 << 10;  // Simple IRs run LL up to this many bytes per rank (0: never;
                                      // measured: LL ~2x faster than Simple below ~1 MiB, BASELINE §5.2)
   int64_t ll128_max_bytes = 2 << 20;  // ... and LL128 above ll_max_bytes up to this many (0: never)
-  int ll_wide_tbs = 16;              // both thresholds apply to IRs with this many thread blocks per rank
+  int ll_wide_tbs = 8;               // both thresholds apply to IRs with this many thread blocks per rank
                                      // (many short chains); narrower IRs run LL only up to
   int64_t ll_narrow_max_bytes = 16 << 10;  // this many bytes (measured, profiles/r02bw_*: Simple
                                      // faster from 16-32 KiB on every narrow BASELINE program)
